@@ -1,0 +1,290 @@
+"""Benchmark: GATE max-min-fair TE solver iterations/s on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl b200|reference]
+
+A STEP is one solver iteration (kernels.py's five updates + residuals +
+controller, controller.py:225-273) over the whole synthetic instance.  The
+workload at N=1 is BASELINE config 2: a synthetic 500-node WAN (reference
+random_topology(500, seed=500)), all-pairs gravity demands (V = 1.5 x total
+capacity, the reference test-suite convention), k = 8 shortest paths:
+249,500 demands / 1,996,000 paths / 18,282,422 demand-path pairs.
+
+value : iterations/s of the fused device loop (inputs resident in HBM), timed
+        with CUDA events around exactly K iterations after W warm-up iterations.
+e2e   : the same metric through the reference-facing C-ABI call `pf_solve`
+        with HOST buffers: warm-start rates H2D, K iterations, GPU projection,
+        rates + sums D2H, all inside the timed region.
+Working set (~0.5 GB) exceeds the 126 MB L2, so no L2 flush is needed.
+
+--impl reference times the reference algorithm's CPU implementation (the
+exact-order C oracle, oracle/pf_oracle.c, OpenMP over all host cores) on the
+same config; each step is one iteration.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TE solve time to within 1% of optimal max-min (ms); iterations/s at 1/2/4/8 B200"
+CONFIGS = {
+    # name: (nodes, k, volume fraction of total capacity, description)
+    "cfg1": (40, 4, 1.5, "GEANT-sized: random_topology(40), all-pairs gravity, k=4"),
+    "cfg1_v0.3": (40, 4, 0.3, "GEANT-sized, V=0.3*cap (reference stop rule fires)"),
+    "cfg2": (500, 8, 1.5, "synthetic 500-node WAN, all-pairs gravity, k=8 (~18.3M demand-path pairs)"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def build_inputs(name):
+    """Generate (or load the cached) flat instance with this package's
+    generators (pinned to the reference's, tests/test_generators.py)."""
+    import paper_2605_01748_b200 as pf
+    n, k, vol, _ = CONFIGS[name]
+    cache = os.path.join(ROOT, "data", f"{name}.npz")
+    topo = pf.random_topology(n, seed=n)
+    tab = pf.gravity_table(topo, vol * float(topo.capacity.sum()))
+    if os.path.exists(cache):
+        z = np.load(cache)
+        flat = pf.FlatPathSet(z["cpp"], z["pep"], z["pe"])
+    else:
+        t = time.perf_counter()
+        flat = pf.k_shortest_paths(topo, tab, k)
+        log(f"[bench] k_shortest_paths({name}) {time.perf_counter() - t:.1f}s (native, {os.cpu_count()} threads)")
+        try:
+            os.makedirs(os.path.dirname(cache), exist_ok=True)
+            np.savez(cache, cpp=flat.com_path_ptr, pep=flat.path_edge_ptr, pe=flat.path_edges)
+        except OSError:
+            pass
+    return topo, tab, flat
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.th = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return self
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.th:
+            self.th.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if "Active" in r[4 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def profile_traffic(name):
+    """dram bytes per launch from the committed ncu summary (profiles/), if present."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get(name, {}).get("dram_bytes_per_iteration")
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_baseline(flat, tab, topo, budget_s=15.0):
+    """The reference algorithm on the host cores (C oracle, OpenMP): iterations/s
+    on a bounded sample (a few iterations of the same instance)."""
+    from oracle import oracle as O
+    I = O.build_instance(topo.capacity, tab.demand, flat.com_path_ptr, flat.path_edge_ptr, flat.path_edges)
+    threads = O.num_threads()
+    loop = O.Loop(I, O.make_config(gamma=1e-12, max_iterations=10 ** 6))
+    loop.step(1)  # warm
+    t = time.perf_counter()
+    n = 0
+    while True:
+        loop.step(1)
+        n += 1
+        dt = time.perf_counter() - t
+        if dt > budget_s or n >= 200:
+            break
+    return {"value": n / dt, "unit": "iterations/s", "cores": threads, "kind": "port",
+            "sample": f"{n} iterations of the full instance (C oracle, exact reference op order)"}
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    import paper_2605_01748_b200  # noqa: F401  (generators only)
+    from oracle import oracle as O
+    topo, tab, flat = build_inputs(args.config)
+    I = O.build_instance(topo.capacity, tab.demand, flat.com_path_ptr, flat.path_edge_ptr, flat.path_edges)
+    loop = O.Loop(I, O.make_config(gamma=1e-12, max_iterations=10 ** 7))
+    # each step = one iteration; bound the run to a few minutes
+    t0 = time.perf_counter()
+    loop.step(1)
+    t_it = time.perf_counter() - t0
+    budget = 120.0
+    warm = min(args.warmup, max(1, int(10.0 / max(t_it, 1e-6))))
+    steps = min(args.steps, max(3, int(budget / max(t_it, 1e-6))))
+    loop.step(warm)
+    t = time.perf_counter()
+    loop.step(steps)
+    dt = time.perf_counter() - t
+    v = steps / dt
+    line = {"metric": METRIC, "value": v, "unit": "iterations/s", "n_gpus": world, "steps": steps,
+            "warmup": warm, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "description": CONFIGS[args.config][3],
+                       "commodities": I.num_commodities, "paths": I.num_paths, "pairs": I.num_pairs,
+                       "edges": I.num_edges},
+            "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": "iterations/s", "cores": O.num_threads(), "kind": "port",
+                             "sample": f"{steps} iterations of the full instance"},
+            "e2e": {"value": v, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_b200(args):
+    import torch
+
+    import paper_2605_01748_b200 as pf
+    rank, world, local = dist_env()
+    if world > 1:
+        from paper_2605_01748_b200 import distributed as D
+        return D.bench_main(args, sys.modules[__name__])
+    torch.cuda.set_device(local)
+    topo, tab, flat = build_inputs(args.config)
+    inst = pf.build_instance_flat(topo, tab, flat, device=local)
+    C, P, E, NP = inst.num_commodities, inst.num_paths, inst.num_edges, inst.num_pairs
+    cfg = pf.SolverConfig(mode="fast", gamma=1e-12, max_iterations=10 ** 9)
+    solver = pf.Solver(inst, cfg).init()
+    # warm-up (W iterations, untimed)
+    solver.time_loop(max(args.warmup, 3))
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local).start()
+    t_wall = time.perf_counter()
+    ms, ms_it = solver.time_loop(args.steps)  # CUDA events around exactly K iterations (one launch)
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall
+    clk = clocks.stop()
+    value = args.steps / (ms / 1e3)
+
+    # roofline: algorithmic bytes per launch / launch duration
+    b_iter = 36 * NP + 40 * P + 32 * C + 32 * E
+    peak, peak_kind = measured_peaks()
+    achieved = b_iter * args.steps / (ms / 1e3) / 1e9
+    stats = solver.kernel_stats()
+
+    # e2e through the C-ABI with host buffers (pf_solve: H2D warm start, K its, projection, D2H)
+    warm = solver.x()
+    e2e_cfg = pf.SolverConfig(mode="fast", gamma=1e-12, max_iterations=args.steps)
+    pf.solve(inst, pf.SolverConfig(mode="fast", gamma=1e-12, max_iterations=3), warm_start=warm)  # warm
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    res = pf.solve(inst, e2e_cfg, warm_start=warm)
+    e2e_s = time.perf_counter() - t
+    e2e = {"value": args.steps / e2e_s, "unit": "iterations/s", "h2d_bytes_per_step": 8 * P / args.steps,
+           "d2h_bytes_per_step": 8 * (P + C) / args.steps, "projection_ms": res.projection_ms,
+           "call": "pf_solve (host warm start -> K iterations -> GPU projection -> host rates/sums)"}
+
+    cpu = cpu_baseline(flat, tab, topo) if (rank == 0 and not args.no_cpu_baseline) else None
+    line = {
+        "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "description": CONFIGS[args.config][3], "commodities": C,
+                   "paths": P, "pairs": NP, "edges": E, "parallelism": f"dp{world}" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (no flush)", "mode": "fast (fused persistent kernel)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": profile_traffic(args.config), "peak_kind": peak_kind,
+                     "bytes_per_iteration_algorithmic": b_iter,
+                     "bytes_per_iteration_compulsory_this_layout": stats["bytes_per_iter"]},
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "gpu_launches": 1,
+        "wall_s_timed_region": t_wall,
+        "kernel": {"grid": stats["grid"], "tiles": stats["tiles"], "launches_total": stats["launches"]},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,841 @@
+// C-ABI entry points: kernel-level functions, projection, and the solve loop.
+//
+// pf_solve / pf_solver_* reproduce pathfair/controller.py:197-284:
+//   PF_MODE_EXACT  the reference's kernels one-to-one in exact operation order
+//                  (exact.cu) with the scalar controller on the host (the only
+//                  per-iteration host traffic is 5 norms + 2 flags); bitwise
+//                  identical to the reference for alpha <= 1.
+//   PF_MODE_FAST   the fused persistent kernel (fused.cu) with the controller
+//                  evaluated on device; no host round trip per iteration.
+// Both end with the GPU projection (projection.cu).
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstring>
+
+#include "fused.cuh"
+#include "pf_internal.cuh"
+
+namespace pf {
+
+const CommOps *comm_ops(pf_comm *c);  // dist.cu
+
+// numpy pairwise sum on the host (np.mean in optimality_from_sums).
+static double np_pairwise_h(const double *a, int64_t n) {
+    if (n < 8) {
+        double res = 0.0;
+        for (int64_t i = 0; i < n; ++i) res += a[i];
+        return res;
+    } else if (n <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; ++j) r[j] = a[j];
+        int64_t i;
+        for (i = 8; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += a[i];
+        return res;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    return np_pairwise_h(a, n2) + np_pairwise_h(a + n2, n - n2);
+}
+
+// CPython `n ** 2` == libm pow(n, 2.0) (controller.py:133-138); keep the call.
+static double py_sq(double v) {
+    volatile double two = 2.0;
+    return std::pow(v, two);
+}
+
+static double wall() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+__global__ void k_init_cold(InstView I, double *x) {
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= I.P) return;
+    int32_t c = I.path_com[p];
+    x[p] = I.demand[c] / (double)(I.com_path_ptr[c + 1] - I.com_path_ptr[c]);  // controller.py:113-114
+}
+__global__ void k_gather_pairs(InstView I, const double *x, double *y) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < I.NP) y[t] = x[I.pair_path[t]];
+}
+
+struct HostCtrl {
+    double beta = 1.0;
+    int64_t alpha = 0, iteration = 0;
+    double ema_s = -1.0, ema_r = -1.0;
+    int64_t cooldown = 0;
+    bool just_incremented = false, stopped = false;
+};
+
+}  // namespace pf
+
+using namespace pf;
+
+struct pf_solver {
+    const pf_instance *inst = nullptr;
+    pf_config cfg{};
+    std::vector<double> ref_sums;
+    std::vector<double> h_demand;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // exact mode
+    DevState cur, nxt;
+    DevBuf<double> sums_tmp, loads_tmp, pk, pw, wsum, q, root_sums, sqtmp, norms;
+    DevBuf<Flags> flags;
+    HostCtrl ctrl;
+    // fast mode
+    FastSolver *fast = nullptr;
+    // common
+    TraceScratch ts;
+    std::vector<pf_trace_row> trace;
+    double t0 = 0.0;
+    double loop_ms = 0.0, proj_ms = 0.0;
+    int status = PF_OK;
+    int64_t bad_commodity = -1;
+    bool initialized = false, finished = false;
+    DevBuf<double> rates_out, sums_out;
+    pf_comm *comm = nullptr;
+    int64_t global_C = 0;
+
+    int64_t C() const { return inst->idx->C; }
+    int64_t P() const { return inst->idx->P; }
+    int64_t E() const { return inst->idx->E; }
+    int64_t NP() const { return inst->idx->NP; }
+};
+
+namespace pf {
+
+static void validate_config(const pf_config &c) {
+    // controller.py:51-61
+    require(c.gamma > 0, "gamma must be > 0");
+    require(c.residual_ratio > 1 && c.beta_scale > 1, "residual_ratio and beta_scale must be > 1");
+    require(0 < c.beta_min && c.beta_min <= c.beta_max, "beta bounds must satisfy 0 < beta_min <= beta_max");
+    require(c.alpha_target >= -1, "alpha_target must be >= 0");
+    require(c.max_iterations >= 1, "max_iterations must be >= 1");
+    require(c.mode == PF_MODE_EXACT || c.mode == PF_MODE_FAST, "unknown mode");
+}
+
+static double adapt_beta(double beta, double s, double r, const pf_config &c) {  // controller.py:142-150
+    if (r > c.residual_ratio * s)
+        beta = beta * c.beta_scale;
+    else if (s > c.residual_ratio * r)
+        beta = beta / c.beta_scale;
+    double lo = beta > c.beta_min ? beta : c.beta_min;
+    return lo < c.beta_max ? lo : c.beta_max;
+}
+
+static double default_theta(const std::vector<double> &D) {  // oracles.py:51-53
+    double dmax = 0.0;
+    for (double d : D) dmax = d > dmax ? d : dmax;
+    return 1e-6 * (dmax > 0 ? dmax : 1.0);
+}
+
+static double optimality_from_sums(const std::vector<double> &sums, const std::vector<double> &ref, double theta) {
+    if (sums.empty()) return 1.0;  // oracles.py:244-254
+    std::vector<double> r(sums.size());
+    for (size_t i = 0; i < sums.size(); ++i) {
+        double den = ref[i] > theta ? ref[i] : theta;
+        double v = sums[i] / den;
+        r[i] = v < 1.0 ? v : 1.0;
+    }
+    return np_pairwise_h(r.data(), (int64_t)r.size()) / (double)r.size();
+}
+
+static void solver_trace_row(pf_solver *S, const double *d_x, const double *d_root_sums, int64_t iteration,
+                             int64_t alpha, double beta, double s, double r) {
+    InstView I = S->inst->view();
+    pf_trace_row row;
+    row.iteration = iteration;
+    row.alpha = alpha;
+    row.beta = beta;
+    row.s = s;
+    row.r = r;
+    double st[4];
+    trace_stats(I, d_x, d_root_sums, alpha, S->ts, 1e-9, st, S->stream);
+    row.objective = st[0];
+    row.pct_violated = st[1];
+    row.mean_relative_violation = st[2];
+    row.optimality = NAN;
+    if (!S->ref_sums.empty()) {
+        DevBuf<double> proj(S->P()), sums(S->C() + 1);
+        project_device(S->inst, d_x, alpha, proj.p, S->stream);
+        exact_commodity_sums(I, proj.p, sums.p, S->stream);
+        std::vector<double> hs(S->C());
+        d2h(hs.data(), sums.p, S->C(), S->stream);
+        PF_CUDA(cudaStreamSynchronize(S->stream));
+        row.optimality = optimality_from_sums(hs, S->ref_sums, default_theta(S->h_demand));
+    }
+    S->trace.push_back(row);
+}
+
+static void solver_init(pf_solver *S, const double *warm) {
+    DeviceGuard g(S->inst->device());
+    InstView I = S->inst->view();
+    cudaStream_t st = S->stream;
+    S->t0 = wall();
+    S->trace.clear();
+    S->loop_ms = S->proj_ms = 0.0;
+    S->status = PF_OK;
+    S->bad_commodity = -1;
+    S->finished = false;
+    HostCtrl c;
+    c.beta = S->cfg.beta0;
+    if (warm) {  // controller.py:104-111
+        for (int64_t p = 0; p < S->P(); ++p)
+            require(std::isfinite(warm[p]), "warm start contains non-finite rates");
+        c.alpha = S->cfg.alpha_target >= 0 ? S->cfg.alpha_target : 0;
+    }
+    S->ctrl = c;
+    DevBuf<double> x0(S->P() ? S->P() : 1);
+    if (warm)
+        h2d(x0.p, warm, S->P(), st);
+    else if (I.P)
+        k_init_cold<<<ceil_div(I.P, 256), 256, 0, st>>>(I, x0.p);
+    PF_CHECK_LAUNCH();
+    if (S->cfg.mode == PF_MODE_EXACT) {
+        PF_CUDA(cudaMemcpyAsync(S->cur.x.p, x0.p, sizeof(double) * S->P(), cudaMemcpyDeviceToDevice, st));
+        if (I.NP) k_gather_pairs<<<ceil_div(I.NP, 256), 256, 0, st>>>(I, x0.p, S->cur.y.p);
+        PF_CHECK_LAUNCH();
+        PF_CUDA(cudaMemsetAsync(S->cur.dd.p, 0, sizeof(double) * S->C(), st));
+        PF_CUDA(cudaMemsetAsync(S->cur.dc.p, 0, sizeof(double) * S->E(), st));
+        PF_CUDA(cudaMemsetAsync(S->cur.dcon.p, 0, sizeof(double) * S->NP(), st));
+        PF_CUDA(cudaMemsetAsync(S->cur.dn.p, 0, sizeof(double) * S->P(), st));
+    } else {
+        fast_init(S->fast, x0.p, c.alpha, c.beta, st);
+    }
+    PF_CUDA(cudaStreamSynchronize(st));
+    S->initialized = true;
+}
+
+// One iteration of controller.py:225-273 in exact order.  Returns false when stopped.
+static bool exact_step(pf_solver *S) {
+    InstView I = S->inst->view();
+    cudaStream_t st = S->stream;
+    HostCtrl &c = S->ctrl;
+    DevState &cur = S->cur, &nxt = S->nxt;
+    StatePtrs s0{cur.x.p, cur.y.p, cur.dd.p, cur.dc.p, cur.dcon.p, cur.dn.p};
+    exact_update_duals(I, s0, S->sums_tmp.p, S->loads_tmp.p, nxt.dd.p, nxt.dc.p, nxt.dcon.p, nxt.dn.p, st);
+    // update_slacks (controller.py:228) is bookkeeping never read by the loop; skipped.
+    StatePtrs s1{cur.x.p, cur.y.p, nxt.dd.p, nxt.dc.p, nxt.dcon.p, nxt.dn.p};
+    exact_suggest(I, s1, nxt.y.p, st);
+    StatePtrs s2{cur.x.p, nxt.y.p, nxt.dd.p, nxt.dc.p, nxt.dcon.p, nxt.dn.p};
+    exact_coefficients(I, s2, S->pk.p, S->pw.p, S->wsum.p, S->q.p, st);
+    reset_flags(S->flags.p, st);
+    exact_roots(I, S->wsum.p, S->q.p, nxt.dd.p, c.beta, c.alpha, S->root_sums.p, S->flags.p, st);
+    exact_rates(I, S->pk.p, S->pw.p, S->root_sums.p, nxt.dd.p, c.beta, c.alpha, nxt.x.p, st);
+    exact_sqdiff_sum(nxt.x.p, cur.x.p, S->P(), S->sqtmp.p, S->norms.p + 0, st);
+    exact_sqdiff_sum(nxt.dd.p, cur.dd.p, S->C(), S->sqtmp.p, S->norms.p + 1, st);
+    exact_sqdiff_sum(nxt.dc.p, cur.dc.p, S->E(), S->sqtmp.p, S->norms.p + 2, st);
+    exact_sqdiff_sum(nxt.dcon.p, cur.dcon.p, S->NP(), S->sqtmp.p, S->norms.p + 3, st);
+    exact_sqdiff_sum(nxt.dn.p, cur.dn.p, S->P(), S->sqtmp.p, S->norms.p + 4, st);
+    double nrm[5];
+    Flags fl;
+    d2h(nrm, S->norms.p, 5, st);
+    d2h(&fl, S->flags.p, 1, st);
+    PF_CUDA(cudaStreamSynchronize(st));
+    if (fl.bad_coef != INT_MAX) {
+        S->bad_commodity = fl.bad_coef;
+        throw Error(PF_ERR_KERNEL_COEF, "non-finite sum coefficients for commodity " + std::to_string(fl.bad_coef));
+    }
+    if (fl.bad_root != INT_MAX) {
+        S->bad_commodity = fl.bad_root;
+        throw Error(PF_ERR_KERNEL_ROOT, "non-finite sum root for commodity " + std::to_string(fl.bad_root));
+    }
+    std::swap(cur.x, nxt.x);
+    std::swap(cur.y, nxt.y);
+    std::swap(cur.dd, nxt.dd);
+    std::swap(cur.dc, nxt.dc);
+    std::swap(cur.dcon, nxt.dcon);
+    std::swap(cur.dn, nxt.dn);
+    int64_t it = ++c.iteration;
+    // controller.py:131-139 (sqrt of each det_diff_norm, then CPython ** 2)
+    double s = std::sqrt(nrm[0]);
+    double n1 = std::sqrt(nrm[1]), n2 = std::sqrt(nrm[2]), n3 = std::sqrt(nrm[3]), n4 = std::sqrt(nrm[4]);
+    double r = std::sqrt(py_sq(n1) + py_sq(n2) + py_sq(n3) + py_sq(n4));
+    if (!(std::isfinite(s) && std::isfinite(r)))
+        throw Error(PF_ERR_SOLVER, "non-finite iterates at iteration " + std::to_string(it));
+    bool converged = r <= S->cfg.gamma && s <= S->cfg.gamma;
+    if (S->cfg.trace) solver_trace_row(S, cur.x.p, S->root_sums.p, it, c.alpha, c.beta, s, r);
+    int decision = 0;  // controller.py:157-170
+    if (converged) {
+        if (S->cfg.alpha_target >= 0 && c.alpha >= S->cfg.alpha_target)
+            decision = 1;
+        else if (c.just_incremented)
+            decision = 1;
+        else
+            decision = 2;
+    }
+    if (S->cfg.adapt) {  // controller.py:245-266
+        if (c.ema_s < 0.0) {
+            c.ema_s = s;
+            c.ema_r = r;
+        } else {
+            c.ema_s += 0.1 * (s - c.ema_s);
+            c.ema_r += 0.1 * (r - c.ema_r);
+        }
+        if (c.cooldown > 0) {
+            c.cooldown -= 1;
+        } else {
+            double nb = adapt_beta(c.beta, c.ema_s, c.ema_r, S->cfg);
+            if (nb != c.beta) {
+                double f = c.beta / nb;
+                scale_inplace(cur.dd.p, S->C(), f, st);
+                scale_inplace(cur.dc.p, S->E(), f, st);
+                scale_inplace(cur.dcon.p, S->NP(), f, st);
+                scale_inplace(cur.dn.p, S->P(), f, st);
+                c.beta = nb;
+                c.cooldown = 10;
+            }
+        }
+    }
+    c.just_incremented = false;
+    if (decision == 1) {
+        c.stopped = true;
+        return false;
+    }
+    if (decision == 2) {
+        c.alpha += 1;
+        c.just_incremented = true;
+    }
+    return true;
+}
+
+static int64_t solver_run(pf_solver *S, int64_t max_steps) {
+    DeviceGuard g(S->inst->device());
+    require(S->initialized, "solver not initialized");
+    int64_t done = 0;
+    if (S->P() == 0) return 0;
+    if (S->cfg.mode == PF_MODE_EXACT) {
+        PF_CUDA(cudaEventRecord(S->ev0, S->stream));
+        while (done < max_steps && !S->ctrl.stopped && S->ctrl.iteration < S->cfg.max_iterations) {
+            exact_step(S);
+            ++done;
+        }
+        PF_CUDA(cudaEventRecord(S->ev1, S->stream));
+        PF_CUDA(cudaEventSynchronize(S->ev1));
+        float ms = 0.f;
+        PF_CUDA(cudaEventElapsedTime(&ms, S->ev0, S->ev1));
+        S->loop_ms += ms;
+        return done;
+    }
+    // fast mode
+    if (!S->cfg.trace) {
+        float ms = 0.f;
+        done = fast_run(S->fast, max_steps, S->stream, &ms);
+        S->loop_ms += ms;
+        return done;
+    }
+    // fast mode with trace: one device iteration at a time, stats on the fresh x
+    while (done < max_steps) {
+        float ms = 0.f;
+        int64_t k = fast_run(S->fast, 1, S->stream, &ms);
+        S->loop_ms += ms;
+        if (k == 0) break;
+        done += k;
+        FastStatus fs = fast_status(S->fast, S->stream);
+        solver_trace_row(S, fast_x(S->fast), fast_root_sums(S->fast), fs.iteration, fs.alpha_used, fs.beta_used,
+                         fs.s, fs.r);
+        if (fs.stopped || fs.iteration >= S->cfg.max_iterations) break;
+    }
+    return done;
+}
+
+static void solver_status(pf_solver *S, pf_result *res) {
+    std::memset(res, 0, sizeof(*res));
+    if (S->cfg.mode == PF_MODE_EXACT || S->P() == 0) {
+        res->iterations = S->ctrl.iteration;
+        res->alpha = S->ctrl.alpha;
+        res->converged = S->P() == 0 ? 1 : (S->ctrl.stopped ? 1 : 0);
+        res->beta = S->ctrl.beta;
+    } else {
+        FastStatus fs = fast_status(S->fast, S->stream);
+        res->iterations = fs.iteration;
+        res->alpha = fs.alpha;
+        res->converged = fs.stopped;
+        res->beta = fs.beta;
+        if (fs.status != PF_OK) {
+            res->status = fs.status;
+            res->bad_commodity = fs.bad;
+        }
+    }
+    res->status = res->status ? res->status : S->status;
+    if (S->bad_commodity >= 0) res->bad_commodity = S->bad_commodity;
+    res->runtime_s = wall() - S->t0;
+    res->loop_ms = S->loop_ms;
+    res->projection_ms = S->proj_ms;
+}
+
+static const double *solver_x(pf_solver *S) {
+    return S->cfg.mode == PF_MODE_EXACT ? S->cur.x.p : fast_x(S->fast);
+}
+
+static void solver_finish(pf_solver *S, double *rates, double *sums) {
+    DeviceGuard g(S->inst->device());
+    InstView I = S->inst->view();
+    cudaStream_t st = S->stream;
+    if (S->P() == 0) {
+        if (sums)
+            for (int64_t c = 0; c < S->C(); ++c) sums[c] = 0.0;
+        S->finished = true;
+        return;
+    }
+    if (S->cfg.mode == PF_MODE_FAST) {
+        FastStatus fs = fast_status(S->fast, st);
+        if (fs.status == PF_ERR_SOLVER)
+            throw Error(PF_ERR_SOLVER, "non-finite iterates at iteration " + std::to_string(fs.iteration));
+        if (fs.status == PF_ERR_KERNEL_COEF || fs.status == PF_ERR_KERNEL_ROOT) {
+            S->bad_commodity = fs.bad;
+            throw Error(fs.status, std::string(fs.status == PF_ERR_KERNEL_COEF ? "non-finite sum coefficients"
+                                                                                : "non-finite sum root") +
+                                       " for commodity " + std::to_string(fs.bad));
+        }
+    }
+    int64_t alpha = S->cfg.mode == PF_MODE_EXACT ? S->ctrl.alpha : fast_status(S->fast, st).alpha;
+    if (S->rates_out.n < (size_t)S->P()) S->rates_out.alloc(S->P());
+    if (S->sums_out.n < (size_t)S->C() + 1) S->sums_out.alloc(S->C() + 1);
+    PF_CUDA(cudaEventRecord(S->ev0, st));
+    if (S->cfg.project)
+        project_device(S->inst, solver_x(S), alpha, S->rates_out.p, st);  // controller.py:275
+    else
+        PF_CUDA(cudaMemcpyAsync(S->rates_out.p, solver_x(S), sizeof(double) * S->P(), cudaMemcpyDeviceToDevice, st));
+    exact_commodity_sums(I, S->rates_out.p, S->sums_out.p, st);
+    PF_CUDA(cudaEventRecord(S->ev1, st));
+    if (rates) d2h(rates, S->rates_out.p, S->P(), st);
+    if (sums) d2h(sums, S->sums_out.p, S->C(), st);
+    PF_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    PF_CUDA(cudaEventElapsedTime(&ms, S->ev0, S->ev1));
+    S->proj_ms += ms;
+    S->finished = true;
+}
+
+static pf_solver *solver_create(const pf_instance *inst, const pf_config *cfg) {
+    require(inst && cfg, "null argument");
+    validate_config(*cfg);
+    DeviceGuard g(inst->device());
+    std::unique_ptr<pf_solver> S(new pf_solver());
+    S->inst = inst;
+    S->cfg = *cfg;
+    const Index &I = *inst->idx;
+    if (cfg->reference_sums) {
+        S->ref_sums.assign(cfg->reference_sums, cfg->reference_sums + I.C);
+        S->cfg.reference_sums = nullptr;
+    }
+    PF_CUDA(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
+    PF_CUDA(cudaEventCreate(&S->ev0));
+    PF_CUDA(cudaEventCreate(&S->ev1));
+    S->h_demand.resize(I.C);
+    d2h(S->h_demand.data(), inst->demand.p, I.C, S->stream);
+    PF_CUDA(cudaStreamSynchronize(S->stream));
+    if (cfg->mode == PF_MODE_EXACT) {
+        S->cur.alloc(I);
+        S->nxt.alloc(I);
+        S->sums_tmp.alloc(I.C + 1);
+        S->loads_tmp.alloc(I.E + 1);
+        S->pk.alloc(I.P + 1);
+        S->pw.alloc(I.P + 1);
+        S->wsum.alloc(I.C + 1);
+        S->q.alloc(I.C + 1);
+        S->root_sums.alloc(I.C + 1);
+        int64_t mx = std::max(std::max(I.P, I.C), std::max(I.E, I.NP));
+        S->sqtmp.alloc(sqdiff_tmp_len(mx));
+        S->norms.alloc(8);
+        S->flags.alloc(1);
+    } else {
+        S->fast = fast_create(inst, *cfg, S->stream);
+    }
+    return S.release();
+}
+
+static void solver_destroy(pf_solver *S) {
+    if (!S) return;
+    DeviceGuard g(S->inst->device());
+    if (S->fast) fast_destroy(S->fast);
+    if (S->ev0) cudaEventDestroy(S->ev0);
+    if (S->ev1) cudaEventDestroy(S->ev1);
+    if (S->stream) cudaStreamDestroy(S->stream);
+    delete S;
+}
+
+// ---------------------------------------------------------------- kernel-level helpers
+
+struct Upload {
+    DevBuf<double> x, y, dd, dc, dcon, dn;
+    StatePtrs ptrs{};
+    Upload(const pf_instance *inst, const pf_state_view *v, cudaStream_t s) {
+        const Index &I = *inst->idx;
+        auto up = [&](DevBuf<double> &b, const double *h, int64_t n) {
+            b.alloc(n ? n : 1);
+            if (h) h2d(b.p, h, n, s);
+            else PF_CUDA(cudaMemsetAsync(b.p, 0, sizeof(double) * (n ? n : 1), s));
+        };
+        up(x, v->x, I.P);
+        up(y, v->y, I.NP);
+        up(dd, v->dual_demand, I.C);
+        up(dc, v->dual_capacity, I.E);
+        up(dcon, v->dual_consensus, I.NP);
+        up(dn, v->dual_nonneg, I.P);
+        ptrs = StatePtrs{x.p, y.p, dd.p, dc.p, dcon.p, dn.p};
+    }
+};
+
+}  // namespace pf
+
+extern "C" {
+
+int pf_commodity_sums(const pf_instance *inst, const double *rates, double *out) {
+    return guard([&] {
+        require(inst && rates && out, "null argument");
+        DeviceGuard g(inst->device());
+        const Index &I = *inst->idx;
+        cudaStream_t s = inst->stream;
+        DevBuf<double> r(I.P + 1), o(I.C + 1);
+        h2d(r.p, rates, I.P, s);
+        exact_commodity_sums(inst->view(), r.p, o.p, s);
+        d2h(out, o.p, I.C, s);
+        PF_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int pf_edge_loads(const pf_instance *inst, const double *rates, double *out) {
+    return guard([&] {
+        require(inst && rates && out, "null argument");
+        DeviceGuard g(inst->device());
+        const Index &I = *inst->idx;
+        cudaStream_t s = inst->stream;
+        DevBuf<double> r(I.P + 1), o(I.E + 1);
+        h2d(r.p, rates, I.P, s);
+        exact_edge_loads_of_rates(inst->view(), r.p, o.p, s);
+        d2h(out, o.p, I.E, s);
+        PF_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int pf_edge_loads_from_pairs(const pf_instance *inst, const double *pv, double *out) {
+    return guard([&] {
+        require(inst && pv && out, "null argument");
+        DeviceGuard g(inst->device());
+        const Index &I = *inst->idx;
+        cudaStream_t s = inst->stream;
+        DevBuf<double> r(I.NP + 1), o(I.E + 1);
+        h2d(r.p, pv, I.NP, s);
+        exact_edge_loads_from_pairs(inst->view(), r.p, o.p, s);
+        d2h(out, o.p, I.E, s);
+        PF_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int pf_validate_allocation(const pf_instance *inst, const double *rates, double tol, pf_violation *rep,
+                           double *edge_overload, double *commodity_excess) {
+    return guard([&] {
+        require(inst && rates && rep, "null argument");
+        DeviceGuard g(inst->device());
+        const Index &I = *inst->idx;
+        cudaStream_t s = inst->stream;
+        DevBuf<double> r(I.P + 1), ov(I.E + 1), ex(I.C + 1);
+        h2d(r.p, rates, I.P, s);
+        TraceScratch ts;
+        violation_stats(inst->view(), r.p, tol, ov.p, ex.p, ts, rep, s);
+        if (edge_overload) d2h(edge_overload, ov.p, I.E, s);
+        if (commodity_excess) d2h(commodity_excess, ex.p, I.C, s);
+        PF_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int pf_det_diff_norm(int device, const double *a, const double *b, int64_t n, double *out) {
+    return guard([&] {
+        require(out != nullptr, "null argument");
+        ensure_device(device);
+        DeviceGuard g(device);
+        DevBuf<double> da(n + 1), db(n + 1), tmp(sqdiff_tmp_len(n)), o(1);
+        h2d(da.p, a, n, 0);
+        h2d(db.p, b, n, 0);
+        exact_sqdiff_sum(da.p, db.p, n, tmp.p, o.p, 0);
+        double v;
+        d2h(&v, o.p, 1, 0);
+        PF_CUDA(cudaStreamSynchronize(0));
+        *out = std::sqrt(v);
+    });
+}
+
+int pf_update_duals(const pf_instance *inst, const pf_state_view *v, double *dd, double *dc, double *dcon, double *dn) {
+    return guard([&] {
+        require(inst && v, "null argument");
+        DeviceGuard g(inst->device());
+        const Index &I = *inst->idx;
+        cudaStream_t s = inst->stream;
+        Upload U(inst, v, s);
+        DevBuf<double> sums(I.C + 1), loads(I.E + 1), odd(I.C + 1), odc(I.E + 1), odcon(I.NP + 1), odn(I.P + 1);
+        exact_update_duals(inst->view(), U.ptrs, sums.p, loads.p, odd.p, odc.p, odcon.p, odn.p, s);
+        if (dd) d2h(dd, odd.p, I.C, s);
+        if (dc) d2h(dc, odc.p, I.E, s);
+        if (dcon) d2h(dcon, odcon.p, I.NP, s);
+        if (dn) d2h(dn, odn.p, I.P, s);
+        PF_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int pf_update_slacks(const pf_instance *inst, const pf_state_view *v, double *sd, double *sc) {
+    return guard([&] {
+        require(inst && v, "null argument");
+        DeviceGuard g(inst->device());
+        const Index &I = *inst->idx;
+        cudaStream_t s = inst->stream;
+        Upload U(inst, v, s);
+        DevBuf<double> sums(I.C + 1), loads(I.E + 1), osd(I.C + 1), osc(I.E + 1);
+        exact_update_slacks(inst->view(), U.ptrs, v->beta, sums.p, loads.p, osd.p, osc.p, s);
+        if (sd) d2h(sd, osd.p, I.C, s);
+        if (sc) d2h(sc, osc.p, I.E, s);
+        PF_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int pf_update_rate_suggestions(const pf_instance *inst, const pf_state_view *v, double *y) {
+    return guard([&] {
+        require(inst && v && y, "null argument");
+        DeviceGuard g(inst->device());
+        const Index &I = *inst->idx;
+        cudaStream_t s = inst->stream;
+        Upload U(inst, v, s);
+        DevBuf<double> oy(I.NP + 1);
+        exact_suggest(inst->view(), U.ptrs, oy.p, s);
+        d2h(y, oy.p, I.NP, s);
+        PF_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int pf_solve_commodity_sums(const pf_instance *inst, const pf_state_view *v, int64_t alpha, double *sums,
+                            int64_t *bad) {
+    return guard([&] {
+        require(inst && v && sums, "null argument");
+        DeviceGuard g(inst->device());
+        const Index &I = *inst->idx;
+        cudaStream_t s = inst->stream;
+        Upload U(inst, v, s);
+        DevBuf<double> pk(I.P + 1), pw(I.P + 1), ws(I.C + 1), q(I.C + 1), out(I.C + 1);
+        DevBuf<Flags> fl(1);
+        exact_coefficients(inst->view(), U.ptrs, pk.p, pw.p, ws.p, q.p, s);
+        reset_flags(fl.p, s);
+        exact_roots(inst->view(), ws.p, q.p, U.dd.p, v->beta, alpha, out.p, fl.p, s);
+        Flags hf;
+        d2h(&hf, fl.p, 1, s);
+        d2h(sums, out.p, I.C, s);
+        PF_CUDA(cudaStreamSynchronize(s));
+        if (bad) *bad = -1;
+        if (hf.bad_coef != INT_MAX) {
+            if (bad) *bad = hf.bad_coef;
+            throw Error(PF_ERR_KERNEL_COEF, "non-finite sum coefficients for commodity " + std::to_string(hf.bad_coef));
+        }
+        if (hf.bad_root != INT_MAX) {
+            if (bad) *bad = hf.bad_root;
+            throw Error(PF_ERR_KERNEL_ROOT, "non-finite sum root for commodity " + std::to_string(hf.bad_root));
+        }
+    });
+}
+
+int pf_update_rates(const pf_instance *inst, const pf_state_view *v, const double *sums, int64_t alpha, double *x) {
+    return guard([&] {
+        require(inst && v && sums && x, "null argument");
+        DeviceGuard g(inst->device());
+        const Index &I = *inst->idx;
+        cudaStream_t s = inst->stream;
+        Upload U(inst, v, s);
+        DevBuf<double> pk(I.P + 1), pw(I.P + 1), ws(I.C + 1), q(I.C + 1), ds(I.C + 1), ox(I.P + 1);
+        h2d(ds.p, sums, I.C, s);
+        exact_coefficients(inst->view(), U.ptrs, pk.p, pw.p, ws.p, q.p, s);
+        exact_rates(inst->view(), pk.p, pw.p, ds.p, U.dd.p, v->beta, alpha, ox.p, s);
+        d2h(x, ox.p, I.P, s);
+        PF_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+__global__ void k_one_root(double w, double beta, double q, int64_t alpha, double *out) {
+    *out = root_scalar(1.0 + w, w / beta, q, alpha);  // kernels.py:198-203
+}
+
+int pf_solve_sum_equation(double w, double beta, double q, int64_t alpha, double *out) {
+    return guard([&] {
+        require(out != nullptr, "null argument");
+        ensure_device(0);
+        DevBuf<double> o(1);
+        k_one_root<<<1, 1>>>(w, beta, q, alpha, o.p);
+        PF_CHECK_LAUNCH();
+        PF_CUDA(cudaMemcpy(out, o.p, sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
+int pf_score_paths(const pf_instance *inst, const double *rates, int64_t alpha, double *scores) {
+    return guard([&] {
+        require(inst && rates && scores, "null argument");
+        DeviceGuard g(inst->device());
+        const Index &I = *inst->idx;
+        cudaStream_t s = inst->stream;
+        DevBuf<double> r(I.P + 1), o(I.P + 1);
+        h2d(r.p, rates, I.P, s);
+        score_paths_device(inst, r.p, alpha, o.p, s);
+        d2h(scores, o.p, I.P, s);
+        PF_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int pf_project(const pf_instance *inst, const double *rates, int64_t alpha, double *out) {
+    return guard([&] {
+        require(inst && rates && out, "null argument");
+        DeviceGuard g(inst->device());
+        const Index &I = *inst->idx;
+        cudaStream_t s = inst->stream;
+        DevBuf<double> r(I.P + 1), o(I.P + 1);
+        h2d(r.p, rates, I.P, s);
+        project_device(inst, r.p, alpha, o.p, s);
+        d2h(out, o.p, I.P, s);
+        PF_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int pf_solver_create(const pf_instance *inst, const pf_config *cfg, pf_solver **out) {
+    return guard([&] {
+        require(out != nullptr, "null output handle");
+        *out = solver_create(inst, cfg);
+    });
+}
+
+int pf_solver_init(pf_solver *S, const double *warm) {
+    return guard([&] {
+        require(S != nullptr, "null solver");
+        solver_init(S, warm);
+    });
+}
+
+int pf_solver_run(pf_solver *S, int64_t max_steps, int64_t *done) {
+    int64_t d = 0;
+    int st = guard([&] {
+        require(S != nullptr, "null solver");
+        d = solver_run(S, max_steps);
+    });
+    if (done) *done = d;
+    if (S && st != PF_OK) S->status = st;
+    return st;
+}
+
+int pf_solver_result(pf_solver *S, pf_result *res) {
+    return guard([&] {
+        require(S && res, "null argument");
+        solver_status(S, res);
+    });
+}
+
+int pf_solver_finish(pf_solver *S, double *rates, double *sums) {
+    return guard([&] {
+        require(S != nullptr, "null solver");
+        solver_finish(S, rates, sums);
+    });
+}
+
+int pf_solver_get_x(pf_solver *S, double *x) {
+    return guard([&] {
+        require(S && x, "null argument");
+        DeviceGuard g(S->inst->device());
+        d2h(x, solver_x(S), S->P(), S->stream);
+        PF_CUDA(cudaStreamSynchronize(S->stream));
+    });
+}
+
+int pf_solver_get_state(pf_solver *S, double *x, double *y, double *dd, double *dc, double *dcon, double *dn,
+                        double *beta, int64_t *alpha, int64_t *iteration) {
+    return guard([&] {
+        require(S != nullptr, "null solver");
+        DeviceGuard g(S->inst->device());
+        cudaStream_t st = S->stream;
+        if (S->cfg.mode == PF_MODE_EXACT) {
+            if (x) d2h(x, S->cur.x.p, S->P(), st);
+            if (y) d2h(y, S->cur.y.p, S->NP(), st);
+            if (dd) d2h(dd, S->cur.dd.p, S->C(), st);
+            if (dc) d2h(dc, S->cur.dc.p, S->E(), st);
+            if (dcon) d2h(dcon, S->cur.dcon.p, S->NP(), st);
+            if (dn) d2h(dn, S->cur.dn.p, S->P(), st);
+            PF_CUDA(cudaStreamSynchronize(st));
+            if (beta) *beta = S->ctrl.beta;
+            if (alpha) *alpha = S->ctrl.alpha;
+            if (iteration) *iteration = S->ctrl.iteration;
+        } else {
+            fast_export_state(S->fast, x, y, dd, dc, dcon, dn, st);
+            FastStatus fs = fast_status(S->fast, st);
+            if (beta) *beta = fs.beta;
+            if (alpha) *alpha = fs.alpha;
+            if (iteration) *iteration = fs.iteration;
+        }
+    });
+}
+
+int pf_solver_time_loop(pf_solver *S, int64_t iterations, float *ms_total, float *ms_per_iter) {
+    return guard([&] {
+        require(S != nullptr, "null solver");
+        DeviceGuard g(S->inst->device());
+        require(S->cfg.mode == PF_MODE_FAST, "time_loop requires PF_MODE_FAST");
+        float ms = 0.f;
+        int64_t done = fast_run(S->fast, iterations, S->stream, &ms);
+        S->loop_ms += ms;
+        if (ms_total) *ms_total = ms;
+        if (ms_per_iter) *ms_per_iter = done ? ms / (float)done : 0.f;
+    });
+}
+
+int pf_solver_kernel_stats(pf_solver *S, int64_t *launches, int64_t *tiles, int64_t *grid, int64_t *bytes) {
+    return guard([&] {
+        require(S != nullptr, "null solver");
+        if (S->cfg.mode != PF_MODE_FAST) {
+            if (launches) *launches = 0;
+            return;
+        }
+        fast_stats(S->fast, launches, tiles, grid, bytes);
+    });
+}
+
+int pf_solver_attach_comm(pf_solver *S, pf_comm *c, int64_t global_commodities) {
+    return guard([&] {
+        require(S != nullptr, "null solver");
+        require(S->cfg.mode == PF_MODE_FAST, "multi-GPU solves run in PF_MODE_FAST");
+        S->comm = c;
+        S->global_C = global_commodities;
+        fast_set_comm(S->fast, comm_ops(c));
+    });
+}
+
+int pf_solver_destroy(pf_solver *S) {
+    return guard([&] { solver_destroy(S); });
+}
+
+int pf_solve(const pf_instance *inst, const pf_config *cfg, const double *warm, double *rates, double *sums,
+             pf_result *res, pf_trace_row *trace, int64_t trace_cap, int64_t *trace_len) {
+    pf_solver *S = nullptr;
+    int st = guard([&] {
+        require(inst && cfg && res, "null argument");
+        S = solver_create(inst, cfg);
+        solver_init(S, warm);
+        if (S->P() > 0) solver_run(S, cfg->max_iterations);
+        solver_finish(S, rates, sums);
+        solver_status(S, res);
+        if (trace && trace_len) {
+            int64_t n = (int64_t)S->trace.size() < trace_cap ? (int64_t)S->trace.size() : trace_cap;
+            std::memcpy(trace, S->trace.data(), sizeof(pf_trace_row) * (size_t)n);
+            *trace_len = n;
+        }
+    });
+    if (st != PF_OK && S) {
+        res->status = st;
+        res->bad_commodity = S->bad_commodity;
+        if (S->cfg.mode == PF_MODE_EXACT) res->iterations = S->ctrl.iteration;
+    }
+    if (S) {
+        char keep[1024];
+        pf_last_error(keep, sizeof keep);
+        solver_destroy(S);
+        set_error(keep);
+    }
+    return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,478 @@
+// Exact-order kernels: the reference's iterate math with its fp64 operation
+// order preserved (compiled -fmad=false), one kernel per reference step.
+//
+// Each kernel cites the numba kernel / numpy expression it reproduces
+// (pathfair/kernels.py, pathfair/_reduce.py, pathfair/model.py).  These back
+// (a) the kernel-level C-ABI (pf_update_duals ...), (b) PF_MODE_EXACT solves,
+// which are bit-identical to the reference for alpha in {0, 1}, and (c) the
+// model-level reductions used by validation, projection and tracing.
+//
+// Parallel structure: one owner per output element, sequential where the
+// reference is sequential.  Where the reference sums in 32-element chunks
+// (_reduce.py:18-49) each chunk partial is computed by one lane in parallel
+// and the partials are then combined in chunk order, which is the same
+// rounding sequence.  Long sequential chains (the per-edge total of
+// _k_suggest) are walked by one warp with the gathers issued 32-wide.
+#include <climits>
+
+#include "pf_internal.cuh"
+
+namespace pf {
+namespace {
+
+constexpr int BLK = 32;    // _reduce.py:14
+constexpr int PART = 4096; // _reduce.py:15
+
+// _reduce.py:18-33 _sum_range over values[lo:hi] (sequential; used for short segments)
+__device__ __forceinline__ double sum_range(const double *v, int64_t lo, int64_t hi) {
+    double total = 0.0;
+    int64_t i = lo;
+    while (i < hi) {
+        int64_t j = i + BLK;
+        if (j > hi) j = hi;
+        double part = 0.0;
+        for (int64_t t = i; t < j; ++t) part += v[t];
+        total += part;
+        i = j;
+    }
+    return total;
+}
+
+// _reduce.py:52-57 segment_sums (thread per segment)
+__global__ void k_segment_sums(const double *__restrict__ v, const int32_t *__restrict__ ptr, int32_t nseg,
+                               double *__restrict__ out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nseg) out[i] = sum_range(v, ptr[i], ptr[i + 1]);
+}
+
+// _reduce.py:60-65 gather_segment_sums, one warp per edge.  MODE 0: values are
+// per-pair (vals[edge_pairs[t]]); MODE 1: values are per-path rates gathered
+// through pair_path (model.py:305-311 edge_loads).
+template <int MODE>
+__global__ void k_edge_gather_blk(InstView I, const double *__restrict__ vals, double *__restrict__ out) {
+    int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (warp >= I.E) return;
+    int64_t lo = I.edge_pair_ptr[warp], hi = I.edge_pair_ptr[warp + 1];
+    double total = 0.0;
+    for (int64_t base = lo; base < hi; base += BLK * 32) {
+        int64_t cs = base + (int64_t)lane * BLK;
+        double part = 0.0;
+        if (cs < hi) {
+            int64_t ce = cs + BLK < hi ? cs + BLK : hi;
+            for (int64_t t = cs; t < ce; ++t) {
+                int32_t pr = I.edge_pairs[t];
+                double v = MODE == 0 ? vals[pr] : vals[I.pair_path[pr]];
+                part += v;
+            }
+        }
+        int64_t rem = hi - base;
+        int nch = rem >= BLK * 32 ? 32 : (int)((rem + BLK - 1) / BLK);
+        for (int j = 0; j < nch; ++j) total += __shfl_sync(0xffffffffu, part, j);
+    }
+    if (lane == 0) out[warp] = total;
+}
+
+// kernels.py:209-215 (+ _k_dual_consensus :69-73)
+__global__ void k_dual_dd(int32_t C, const double *dd, const double *sums, const double *D, double *out) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < C) out[c] = npmax0(dd[c] + (sums[c] - D[c]));
+}
+__global__ void k_dual_dc(int32_t E, const double *dc, const double *loads, const double *cap, double *out) {
+    int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < E) out[e] = npmax0(dc[e] + (loads[e] - cap[e]));
+}
+__global__ void k_dual_dcon(int32_t NP, const double *dcon, const double *x, const int32_t *pair_path,
+                            const double *y, double *out) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < NP) out[t] = max0(dcon[t] + x[pair_path[t]] - y[t]);
+}
+__global__ void k_dual_dn(int32_t P, const double *dn, const double *x, double *out) {
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < P) out[p] = npmax0(dn[p] - x[p]);
+}
+
+// kernels.py:228-231
+__global__ void k_slack_sd(int32_t C, const double *dd, double beta, const double *D, const double *sums,
+                           double *out) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < C) out[c] = npmax0(dd[c] / beta + (D[c] - sums[c]));
+}
+__global__ void k_slack_sc(int32_t E, const double *dc, double beta, const double *cap, const double *loads,
+                           double *out) {
+    int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < E) out[e] = npmax0(dc[e] / beta + (cap[e] - loads[e]));
+}
+
+// kernels.py:76-100 _k_suggest: warp per edge; the per-edge total is one
+// sequential chain (total += x + dcon) walked 32 gathered values at a time.
+__global__ void k_suggest(InstView I, const double *__restrict__ x, const double *__restrict__ dcon,
+                          const double *__restrict__ dc, double *__restrict__ y) {
+    int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (e >= I.E) return;
+    int32_t lo = I.edge_pair_ptr[e], hi = I.edge_pair_ptr[e + 1];
+    if (hi == lo) return;
+    double total = 0.0;
+    for (int32_t base = lo; base < hi; base += 32) {
+        int32_t t = base + lane;
+        double v = 0.0;
+        if (t < hi) {
+            int32_t pr = I.edge_pairs[t];
+            v = x[I.pair_path[pr]] + dcon[pr];
+        }
+        int n = hi - base < 32 ? hi - base : 32;
+        for (int j = 0; j < n; ++j) total += __shfl_sync(0xffffffffu, v, j);
+    }
+    double adjust = (total + dc[e] - I.capacity[e]) / ((double)I.edge_path_count[e] + 1.0);
+    if (adjust < 0.0) adjust = 0.0;
+    for (int32_t t = lo + lane; t < hi; t += 32) {
+        int32_t pr = I.edge_pairs[t];
+        double v = x[I.pair_path[pr]] + dcon[pr] - adjust;
+        y[pr] = max0(v);
+    }
+}
+
+// kernels.py:103-119 _k_path_coeffs
+__global__ void k_path_coeffs(InstView I, const double *__restrict__ y, const double *__restrict__ dcon,
+                              const double *__restrict__ x_prev, const double *__restrict__ dn,
+                              double *__restrict__ pk, double *__restrict__ pw) {
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= I.P) return;
+    double acc = 0.0;
+    for (int32_t t = I.pair_ptr[p]; t < I.pair_ptr[p + 1]; ++t) acc += y[t] - dcon[t];
+    double h = (double)I.hops[p];
+    if (x_prev[p] < dn[p]) {
+        pk[p] = acc + dn[p];
+        pw[p] = 1.0 / (h + 1.0);
+    } else {
+        pk[p] = acc;
+        pw[p] = 1.0 / h;
+    }
+}
+
+// kernels.py:122-131 _k_com_coeffs
+__global__ void k_com_coeffs(InstView I, const double *__restrict__ pk, const double *__restrict__ pw,
+                             double *__restrict__ wsum, double *__restrict__ q) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= I.C) return;
+    double ws = 0.0, qw = 0.0;
+    for (int32_t p = I.com_path_ptr[c]; p < I.com_path_ptr[c + 1]; ++p) {
+        ws += pw[p];
+        qw += pw[p] * pk[p];
+    }
+    wsum[c] = ws;
+    q[c] = qw;
+}
+
+// kernels.py:267-282 + _k_roots :176-189
+__global__ void k_roots(InstView I, const double *__restrict__ wsum, const double *__restrict__ q,
+                        const double *__restrict__ dd, double beta, int64_t alpha, double *__restrict__ out,
+                        Flags *flags) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= I.C) return;
+    double w = wsum[c], qc = q[c];
+    if (!(isfinite(w) && isfinite(qc))) {
+        atomicMin(&flags->bad_coef, c);
+        out[c] = NAN;
+        return;
+    }
+    double d_eff = I.demand[c] - dd[c];  // kernels.py:275
+    double s = commodity_root(w, qc, d_eff, beta, alpha);
+    out[c] = s;
+    if (!isfinite(s)) atomicMin(&flags->bad_root, c);
+}
+
+// kernels.py:285-296 update_rates (+ _k_rates :192-195)
+__global__ void k_rates(InstView I, const double *__restrict__ pk, const double *__restrict__ pw,
+                        const double *__restrict__ sums, const double *__restrict__ dd, double beta, int64_t alpha,
+                        double *__restrict__ x) {
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= I.P) return;
+    int32_t c = I.path_com[p];
+    double ct = commodity_term(sums[c], I.demand[c], dd[c], beta, alpha);
+    x[p] = pw[p] * (pk[p] + ct);
+}
+
+// _reduce.py:79-99 _sqdiff_partials: one CTA per 4096 block, one lane per 32-chunk.
+__global__ void k_sqdiff_blocks(const double *__restrict__ a, const double *__restrict__ b, int64_t n,
+                                double *__restrict__ out) {
+    __shared__ double parts[PART / BLK];
+    int64_t lo = (int64_t)blockIdx.x * PART;
+    int64_t hi = lo + PART < n ? lo + PART : n;
+    int j = threadIdx.x;  // chunk index, blockDim == 128
+    int64_t cs = lo + (int64_t)j * BLK;
+    double part = 0.0;
+    if (cs < hi) {
+        int64_t ce = cs + BLK < hi ? cs + BLK : hi;
+        for (int64_t t = cs; t < ce; ++t) {
+            double d = a[t] - b[t];
+            part += d * d;
+        }
+    }
+    parts[j] = part;
+    __syncthreads();
+    if (j == 0) {
+        int nch = (int)((hi - lo + BLK - 1) / BLK);
+        double total = 0.0;
+        for (int i = 0; i < nch; ++i) total += parts[i];
+        out[blockIdx.x] = total;
+    }
+}
+
+// _reduce.py:18-33 over the block totals (single thread; nb <= n / 4096).
+__global__ void k_sum_range_1(const double *__restrict__ v, int64_t n, double *__restrict__ out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) *out = sum_range(v, 0, n);
+}
+
+__global__ void k_scale(double *a, int64_t n, double f) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) a[i] = a[i] * f;
+}
+
+__global__ void k_reset_flags(Flags *f) {
+    f->bad_coef = INT_MAX;
+    f->bad_root = INT_MAX;
+    f->bad_edge = INT_MAX;
+    f->pad = 0;
+}
+
+// ---------------- trace / validation helpers
+
+// numpy pairwise_sum (PW_BLOCKSIZE 128) -- np.sum/np.mean order.
+__device__ double np_pairwise(const double *a, int64_t n) {
+    if (n < 8) {
+        double res = 0.0;
+        for (int64_t i = 0; i < n; ++i) res += a[i];
+        return res;
+    } else if (n <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; ++j) r[j] = a[j];
+        int64_t i;
+        for (i = 8; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += a[i];
+        return res;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    return np_pairwise(a, n2) + np_pairwise(a + n2, n - n2);
+}
+
+__global__ void k_np_sum(const double *a, int64_t n, double *out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) *out = np_pairwise(a, n);
+}
+
+// kernels.py:47-66 utility of max(S, 1e-12) (controller.py:175)
+__global__ void k_utility(int32_t C, const double *sums, int64_t alpha, double *u) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    double s = sums[c] > 1e-12 ? sums[c] : 1e-12;
+    if (alpha == 0)
+        u[c] = s - 1.0;
+    else if (alpha == 1)
+        u[c] = log(s);
+    else
+        u[c] = (pow(s, 1.0 - (double)alpha) - 1.0) / (1.0 - (double)alpha);
+}
+
+// model.py:346-362: overload / excess, violation flags and relative violations.
+__global__ void k_violations(InstView I, const double *x, const double *loads, const double *sums, double tol,
+                             double *overload, double *excess, double *rel_e, double *rel_c, int32_t *cnt) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < I.E) {
+        double ov = npmax0(loads[i] - I.capacity[i]);
+        if (overload) overload[i] = ov;
+        bool bad = ov > tol;
+        rel_e[i] = bad ? ov / (I.capacity[i] > 1e-12 ? I.capacity[i] : 1e-12) : NAN;
+        if (bad) atomicAdd(&cnt[0], 1);
+    }
+    if (i < I.C) {
+        double ex = npmax0(sums[i] - I.demand[i]);
+        if (excess) excess[i] = ex;
+        bool bad = ex > tol;
+        rel_c[i] = bad ? ex / (I.demand[i] > 1e-12 ? I.demand[i] : 1e-12) : NAN;
+        if (bad) atomicAdd(&cnt[1], 1);
+    }
+    if (i < I.P && x[i] < -tol) {
+        atomicAdd(&cnt[2], 1);
+    }
+}
+
+__global__ void k_worst_negative(int32_t P, const double *x, double tol, double *out) {
+    // max of -x over x < -tol (single pass, order-free: max is exact)
+    __shared__ double sm[256];
+    double m = 0.0;
+    for (int i = threadIdx.x; i < P; i += blockDim.x)
+        if (x[i] < -tol && -x[i] > m) m = -x[i];
+    sm[threadIdx.x] = m;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s && sm[threadIdx.x + s] > sm[threadIdx.x]) sm[threadIdx.x] = sm[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sm[0];
+}
+
+// Stable compaction of the non-NaN relative violations (edges first, then
+// commodities: np.concatenate order, model.py:358-362) followed by np.mean.
+__global__ void k_compact_mean(const double *rel_e, int32_t E, const double *rel_c, int32_t C, double *tmp,
+                               double *out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int64_t n = 0;
+    for (int32_t i = 0; i < E; ++i)
+        if (!isnan(rel_e[i])) tmp[n++] = rel_e[i];
+    for (int32_t i = 0; i < C; ++i)
+        if (!isnan(rel_c[i])) tmp[n++] = rel_c[i];
+    *out = n ? np_pairwise(tmp, n) / (double)n : 0.0;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- host wrappers
+
+constexpr int TB = 256;
+
+void exact_commodity_sums(const InstView &I, const double *x, double *out, cudaStream_t s) {
+    if (I.C) k_segment_sums<<<ceil_div(I.C, TB), TB, 0, s>>>(x, I.com_path_ptr, I.C, out);
+    PF_CHECK_LAUNCH();
+}
+
+void exact_edge_loads_from_pairs(const InstView &I, const double *pv, double *out, cudaStream_t s) {
+    if (I.E) k_edge_gather_blk<0><<<ceil_div((int64_t)I.E * 32, 128), 128, 0, s>>>(I, pv, out);
+    PF_CHECK_LAUNCH();
+}
+
+void exact_edge_loads_of_rates(const InstView &I, const double *rates, double *out, cudaStream_t s) {
+    if (I.E) k_edge_gather_blk<1><<<ceil_div((int64_t)I.E * 32, 128), 128, 0, s>>>(I, rates, out);
+    PF_CHECK_LAUNCH();
+}
+
+void exact_update_duals(const InstView &I, const StatePtrs &st, double *sums, double *loads, double *dd, double *dc,
+                        double *dcon, double *dn, cudaStream_t s) {
+    exact_commodity_sums(I, st.x, sums, s);
+    exact_edge_loads_from_pairs(I, st.y, loads, s);
+    if (I.C) k_dual_dd<<<ceil_div(I.C, TB), TB, 0, s>>>(I.C, st.dd, sums, I.demand, dd);
+    if (I.E) k_dual_dc<<<ceil_div(I.E, TB), TB, 0, s>>>(I.E, st.dc, loads, I.capacity, dc);
+    if (I.NP) k_dual_dcon<<<ceil_div(I.NP, TB), TB, 0, s>>>(I.NP, st.dcon, st.x, I.pair_path, st.y, dcon);
+    if (I.P) k_dual_dn<<<ceil_div(I.P, TB), TB, 0, s>>>(I.P, st.dn, st.x, dn);
+    PF_CHECK_LAUNCH();
+}
+
+void exact_update_slacks(const InstView &I, const StatePtrs &st, double beta, double *sums, double *loads,
+                         double *sd, double *sc, cudaStream_t s) {
+    exact_commodity_sums(I, st.x, sums, s);
+    exact_edge_loads_from_pairs(I, st.y, loads, s);
+    if (I.C) k_slack_sd<<<ceil_div(I.C, TB), TB, 0, s>>>(I.C, st.dd, beta, I.demand, sums, sd);
+    if (I.E) k_slack_sc<<<ceil_div(I.E, TB), TB, 0, s>>>(I.E, st.dc, beta, I.capacity, loads, sc);
+    PF_CHECK_LAUNCH();
+}
+
+void exact_suggest(const InstView &I, const StatePtrs &st, double *y_out, cudaStream_t s) {
+    if (I.E) k_suggest<<<ceil_div((int64_t)I.E * 32, 128), 128, 0, s>>>(I, st.x, st.dcon, st.dc, y_out);
+    PF_CHECK_LAUNCH();
+}
+
+void exact_coefficients(const InstView &I, const StatePtrs &st, double *pk, double *pw, double *wsum, double *q,
+                        cudaStream_t s) {
+    if (I.P) k_path_coeffs<<<ceil_div(I.P, TB), TB, 0, s>>>(I, st.y, st.dcon, st.x, st.dn, pk, pw);
+    if (I.C) k_com_coeffs<<<ceil_div(I.C, TB), TB, 0, s>>>(I, pk, pw, wsum, q);
+    PF_CHECK_LAUNCH();
+}
+
+void exact_roots(const InstView &I, const double *wsum, const double *q, const double *dd, double beta,
+                 int64_t alpha, double *sums, Flags *flags, cudaStream_t s) {
+    if (I.C) k_roots<<<ceil_div(I.C, 128), 128, 0, s>>>(I, wsum, q, dd, beta, alpha, sums, flags);
+    PF_CHECK_LAUNCH();
+}
+
+void exact_rates(const InstView &I, const double *pk, const double *pw, const double *sums, const double *dd,
+                 double beta, int64_t alpha, double *x_out, cudaStream_t s) {
+    if (I.P) k_rates<<<ceil_div(I.P, TB), TB, 0, s>>>(I, pk, pw, sums, dd, beta, alpha, x_out);
+    PF_CHECK_LAUNCH();
+}
+
+size_t sqdiff_tmp_len(int64_t n) { return (size_t)((n + PART - 1) / PART) + 1; }
+
+void exact_sqdiff_sum(const double *a, const double *b, int64_t n, double *block_tmp, double *out, cudaStream_t s) {
+    if (n == 0) {
+        PF_CUDA(cudaMemsetAsync(out, 0, sizeof(double), s));
+        return;
+    }
+    int64_t nb = (n + PART - 1) / PART;
+    k_sqdiff_blocks<<<(unsigned)nb, PART / BLK, 0, s>>>(a, b, n, block_tmp);
+    k_sum_range_1<<<1, 32, 0, s>>>(block_tmp, nb, out);
+    PF_CHECK_LAUNCH();
+}
+
+void scale_inplace(double *a, int64_t n, double f, cudaStream_t s) {
+    if (n) k_scale<<<ceil_div(n, TB), TB, 0, s>>>(a, n, f);
+    PF_CHECK_LAUNCH();
+}
+
+void reset_flags(Flags *f, cudaStream_t s) {
+    k_reset_flags<<<1, 1, 0, s>>>(f);
+    PF_CHECK_LAUNCH();
+}
+
+static void ensure_trace_scratch(const InstView &I, TraceScratch &ts) {
+    if (ts.loads.n < (size_t)I.E + 1) ts.loads.alloc(I.E + 1);
+    if (ts.sums.n < (size_t)I.C + 1) ts.sums.alloc(I.C + 1);
+    if (ts.rel.n < (size_t)(I.E + I.C) + 1) ts.rel.alloc(I.E + I.C + 1);
+    if (ts.tmp.n < (size_t)(I.E + I.C) + 1) ts.tmp.alloc(I.E + I.C + 1);
+    if (ts.cnt.n < 4) ts.cnt.alloc(4);
+    if (ts.out.n < 8) ts.out.alloc(8);
+}
+
+// controller.py:173-194 _trace_row: objective + pct_violated + mean_relative_violation.
+void trace_stats(const InstView &I, const double *x, const double *root_sums, int64_t alpha, TraceScratch &ts,
+                 double tol, double *host_out4, cudaStream_t s) {
+    ensure_trace_scratch(I, ts);
+    if (I.C) {
+        k_utility<<<ceil_div(I.C, TB), TB, 0, s>>>(I.C, root_sums, alpha, ts.tmp.p);
+        k_np_sum<<<1, 32, 0, s>>>(ts.tmp.p, I.C, ts.out.p + 0);
+    } else {
+        PF_CUDA(cudaMemsetAsync(ts.out.p, 0, sizeof(double), s));
+    }
+    pf_violation rep;
+    violation_stats(I, x, tol, nullptr, nullptr, ts, &rep, s);
+    double obj;
+    d2h(&obj, ts.out.p, 1, s);
+    PF_CUDA(cudaStreamSynchronize(s));
+    host_out4[0] = obj;
+    host_out4[1] = rep.pct_violated;
+    host_out4[2] = rep.mean_relative_violation;
+    host_out4[3] = (double)rep.n_violated;
+}
+
+// model.py:335-369 validate_allocation
+void violation_stats(const InstView &I, const double *x, double tol, double *d_overload, double *d_excess,
+                     TraceScratch &ts, pf_violation *rep, cudaStream_t s) {
+    ensure_trace_scratch(I, ts);
+    exact_edge_loads_of_rates(I, x, ts.loads.p, s);
+    exact_commodity_sums(I, x, ts.sums.p, s);
+    PF_CUDA(cudaMemsetAsync(ts.cnt.p, 0, sizeof(int32_t) * 4, s));
+    int32_t n = I.E > I.C ? I.E : I.C;
+    n = n > I.P ? n : I.P;
+    if (n)
+        k_violations<<<ceil_div(n, TB), TB, 0, s>>>(I, x, ts.loads.p, ts.sums.p, tol, d_overload, d_excess, ts.rel.p,
+                                                     ts.rel.p + I.E, ts.cnt.p);
+    k_compact_mean<<<1, 32, 0, s>>>(ts.rel.p, I.E, ts.rel.p + I.E, I.C, ts.tmp.p, ts.out.p + 1);
+    k_worst_negative<<<1, 256, 0, s>>>(I.P, x, tol, ts.out.p + 2);
+    PF_CHECK_LAUNCH();
+    int32_t cnt[4];
+    double mr[2];
+    d2h(cnt, ts.cnt.p, 4, s);
+    d2h(mr, ts.out.p + 1, 2, s);
+    PF_CUDA(cudaStreamSynchronize(s));
+    int64_t nv = (int64_t)cnt[0] + cnt[1] + cnt[2];
+    int64_t total = (int64_t)I.E + I.C + I.P;
+    rep->n_violated = nv;
+    rep->negative_count = cnt[2];
+    rep->worst_negative = mr[1];
+    rep->pct_violated = total ? 100.0 * (double)nv / (double)total : 0.0;
+    rep->mean_relative_violation = mr[0];
+}
+
+}  // namespace pf

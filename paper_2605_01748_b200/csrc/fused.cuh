@@ -1,0 +1,41 @@
+// Fast mode: fused persistent kernel for the GATE iteration (see fused.cu).
+#pragma once
+
+#include "pf_internal.cuh"
+
+namespace pf {
+
+struct FastSolver;
+
+struct FastStatus {
+    int64_t iteration;   // completed iterations
+    int64_t alpha;       // alpha for the next iteration (after any increment)
+    int64_t alpha_used;  // alpha used by the last completed iteration
+    double beta;         // beta for the next iteration
+    double beta_used;    // beta used by the last completed iteration
+    double s, r;         // residuals of the last completed iteration
+    int32_t stopped;
+    int32_t status;
+    int64_t bad;
+};
+
+FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStream_t s);
+void fast_destroy(FastSolver *f);
+void fast_init(FastSolver *f, const double *d_x0, int64_t alpha0, double beta0, cudaStream_t s);
+// Runs up to max_steps iterations (fewer if the controller stops); returns the count.
+int64_t fast_run(FastSolver *f, int64_t max_steps, cudaStream_t s, float *ms);
+FastStatus fast_status(FastSolver *f, cudaStream_t s);
+const double *fast_x(FastSolver *f);
+const double *fast_root_sums(FastSolver *f);
+void fast_export_state(FastSolver *f, double *x, double *y, double *dd, double *dc, double *dcon, double *dn,
+                       cudaStream_t s);
+void fast_stats(FastSolver *f, int64_t *launches, int64_t *tiles, int64_t *grid, int64_t *bytes_per_iter);
+
+// Multi-GPU hooks (dist.cu): reduce edge partial vectors / residual scalars across ranks.
+struct CommOps {
+    void *ctx;
+    void (*allreduce_sum)(void *ctx, double *buf, int64_t n, cudaStream_t s);
+};
+void fast_set_comm(FastSolver *f, const CommOps *ops);
+
+}  // namespace pf
