@@ -250,16 +250,9 @@ __host__ __device__ __forceinline__ double npmax0(double v) { return v < 0.0 ? 0
 __host__ __device__ __forceinline__ double max0(double v) { return v > 0.0 ? v : 0.0; }    // numba clamp
 __host__ __device__ __forceinline__ double pymax1(double v) { return v > 1.0 ? v : 1.0; }  // max(1.0, v)
 
-// kernels.py:134-173 _root_scalar: root of lin*S - c*S^(-alpha) - q.
-// Compiled with -fmad=false so every op rounds exactly as the reference's.
-__device__ __forceinline__ double root_scalar(double lin, double c, double q, int64_t alpha) {
-    if (alpha == 0) return (q + c) / lin;
-    if (alpha == 1) {
-        double disc = q * q + 4.0 * lin * c;
-        double sq = sqrt(disc);
-        if (q >= 0.0) return (q + sq) / (2.0 * lin);
-        return (2.0 * c) / (sq - q);
-    }
+// kernels.py:153-173: safeguarded Newton + bisection for alpha >= 2 (kept out of
+// line so the fused kernel's register budget is not sized for it).
+static __device__ __noinline__ double root_newton(double lin, double c, double q, int64_t alpha) {
     double a = (double)alpha;
     double tol_f = 1e-10 * pymax1(fabs(q));
     double lo = 1e-12;
@@ -284,6 +277,19 @@ __device__ __forceinline__ double root_scalar(double lin, double c, double q, in
         s = t;
     }
     return s;
+}
+
+// kernels.py:134-173 _root_scalar: root of lin*S - c*S^(-alpha) - q.
+// Compiled with -fmad=false so every op rounds exactly as the reference's.
+__device__ __forceinline__ double root_scalar(double lin, double c, double q, int64_t alpha) {
+    if (alpha == 0) return (q + c) / lin;
+    if (alpha == 1) {
+        double disc = q * q + 4.0 * lin * c;
+        double sq = sqrt(disc);
+        if (q >= 0.0) return (q + sq) / (2.0 * lin);
+        return (2.0 * c) / (sq - q);
+    }
+    return root_newton(lin, c, q, alpha);
 }
 
 // kernels.py:183-189 _k_roots body for one commodity.

@@ -260,7 +260,8 @@ def main():
         for k, v in flat.items():
             arrays[f"{tag}/in/{k}"] = v
         for f in INCIDENCE:
-            digests[f"{tag}/inc/{f}"] = digest(np.asarray(getattr(inst, f), np.int64))
+            dt = np.float64 if f == "demand" else np.int64
+            digests[f"{tag}/inc/{f}"] = digest(np.asarray(getattr(inst, f), dt))
         if vol == 0.3:
             kernel_cases(tag, inst, 5, arrays, digests, verbatim=False)
             snaps = {1, 2, 3, 5, 10, 50, 200, 500, 826, 866, 978}
@@ -284,6 +285,7 @@ def main():
             cap = inst.capacity.copy()
             cap[cut] = 0.0
             arrays[f"{tag}/cut_edges"] = np.sort(cut)
+            arrays[f"{tag}/warm_rates"] = rates
             inst_cut = model.with_conditions(inst, capacity=cap)
             # alpha_target=1 keeps the replay bit-exact (alpha >= 2 goes through numpy's SIMD pow)
             cfgw = controller.SolverConfig(alpha_target=1, max_iterations=400)
