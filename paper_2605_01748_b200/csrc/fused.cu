@@ -1,38 +1,35 @@
-// Fast mode: the whole GATE iteration (controller.py:225-273 with kernels.py's
-// five steps) as ONE persistent, grid-synchronised kernel per run of iterations.
+// Fast mode: the GATE iteration (controller.py:225-273 with kernels.py's five
+// steps) as ONE persistent, grid-synchronised kernel per run of iterations.
 //
-// Layout (built once per instance, TileLayout):
+// Layout (TileLayout, built once per instance):
 //   Commodities are cut into TILES of <= TP consecutive pairs (commodity-major,
 //   the reference's own pair order).  Inside a tile the pairs are stored in
-//   SLOTS sorted by edge id (stable), so every edge's pairs inside a tile form one
-//   contiguous run.  Per slot: `slot_eid` (u16 edge id); per tile-local pair (in
-//   path-major order, stored at the tile's slot base): `pos` (u16 slot of that
-//   pair).  Tiles start at a 64-slot boundary so every per-slot array is 16-byte
-//   aligned per tile.  The only per-pair STATE is dual_consensus (fp64, slot order):
-//   y is never stored -- y_k = max0((x_{k-1} + dcon_k) - adj_k) is recomputed from
-//   per-path x_{k-1}, per-slot dcon_k and per-edge adj_k (bitwise the value
-//   _k_suggest produced), removing 16 B/pair/iteration of HBM traffic.
+//   SLOTS sorted by edge id (stable), so every edge's pairs form one contiguous
+//   run per tile.  Per slot: `slot_eid` (u16); per tile-local pair (path-major,
+//   stored at the tile's slot base): `pos` (u16 slot of that pair).  Tiles start
+//   on a 64-slot boundary.  The only per-pair STATE is dual_consensus (fp64, slot
+//   order, double buffered); y is never stored.
 //
-// One iteration = 3 grid barriers:
-//   ctrl   residual partials -> s, r -> EMA / beta / alpha / stop (every CTA
-//          evaluates the same scalar logic redundantly; no host round trip)
-//   A      per tile: S_c + dual_demand (thread per commodity), dual_nonneg (thread
-//          per path), then per slot: y_{k-1} recompute, dual_consensus update, T value
-//          (x + dcon'); the tile's edge runs are reduced by a block-wide segmented
-//          scan into a CTA-private smem accumulator (no atomics)
-//   R      CTA partials -> per-edge totals in a fixed order; dual_capacity and the
-//          suggestion adjustment per edge (kernels.py:94-96, :212)
-//   B      per tile: y_k, path coefficients K/w (path order, kernels.py:110-119),
-//          commodity coefficients + sum roots (thread per commodity), new rates;
-//          y_k edge runs reduced for the next iteration's capacity dual.
-// Tile inputs are staged into shared memory with cp.async (LDGSTS), double
-// buffered: the copies of tile k+1 are in flight while tile k is computed.
-// Reductions are deterministic (fixed tile->CTA map and operator trees); the
-// per-edge sums differ in association from the reference's sequential sums, so
-// fast mode is tolerance-matched (exact mode is the bitwise path).
+// One pass per iteration.  Iteration k+1 of the reference is
+//   A(k+1): duals_{k+1} from (x_k, y_k, duals_k * f_k)        kernels.py:206-216
+//   E(k+1): dual_capacity_{k+1}, adjustment_{k+1} per edge    kernels.py:88-96, 212
+//   B(k+1): y_{k+1}, coefficients, sum roots, x_{k+1}         kernels.py:235-296
+// and the pass M(k+1) fuses B(k+1) with A(k+2): y_{k+1} and x_{k+1} never leave
+// shared memory before they are consumed by the next dual update, so each pair
+// costs one fp64 read + one fp64 write of dual_consensus per iteration (~20 B
+// with its two u16 indices).  A(k+2) needs the rescale factor f_{k+1} of the
+// controller step that follows B(k+1) (controller.py:251-266); the pass
+// speculates f = 1 (certain during the post-change cooldown and when adapt is
+// off) and a ROLLBACK pass recomputes A(k+2) from the still-intact duals_{k+1}
+// buffers on the rare iterations where beta changes.
 //
-// The dual rescale on a beta change (controller.py:255-266) is applied lazily:
-// the factor is folded into the next read of each dual array.
+// Per iteration: M pass -> grid barrier -> controller (every CTA evaluates the
+// same scalar logic from the residual partials) [-> rollback pass -> barrier]
+// -> edge phase -> barrier.  Edge sums are reduced deterministically: a block
+// segmented scan over each tile's edge runs into CTA-private shared-memory
+// accumulators, then CTA partials in a fixed order.  The association differs
+// from the reference's sequential per-edge sums, so fast mode is
+// tolerance-matched (PF_MODE_EXACT is the bitwise path).
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -46,7 +43,7 @@ namespace cg = cooperative_groups;
 
 namespace pf {
 
-constexpr int NT = 256;        // threads per CTA (several CTAs per SM)
+constexpr int NT = 256;        // threads per CTA (3 CTAs per SM)
 constexpr int TP = 1024;       // max pairs (slots) per tile
 constexpr int ITEMS = TP / NT; // slots per thread in the segmented scan
 constexpr int TPATH = 256;     // max paths per tile
@@ -73,26 +70,26 @@ struct TileLayout {
 
 struct Ctrl {
     double beta, beta_used, ema_s, ema_r, f, s, r;
-    int64_t alpha, alpha_used, iteration, evaluated, cooldown, target;
-    int32_t just_incremented, stopped, status, first, cur, pad;
+    int64_t alpha, alpha_used, iteration, cooldown, target;
+    int32_t just_incremented, stopped, status, xc, db, need_a1, need_edge, pad;
     int64_t bad;
 };
 
 struct Params {
     InstView I;
-    int32_t ntiles, G, nred_items, nslices;
+    int32_t ntiles, G, nslices, pad;
     const TileDesc *desc;
     const uint16_t *slot_eid, *pos;
-    double *dcon, *x0, *x1, *dn, *dd, *dc, *adj;
+    double *dcon[2], *dn[2], *dd[2], *x[2];
+    double *dc, *adj;
     double *partT, *partL;  // [G][E]
     double *sub;            // [2][nslices][E]
-    double *res;            // [G][8]
+    double *res;            // [G][8]: 0 dx | 1..3 (dd, dcon, dn) parity 0 | 4..6 parity 1
     double *res_dc;         // [ngroups]
     int32_t *grp_count;     // [ngroups]
     double *root_sums;      // [C] or null
     Ctrl *ctrl;
     int32_t *err;           // [2]: bad_coef, bad_root (INT_MAX = none)
-    // config
     double gamma, residual_ratio, beta_scale, beta_min, beta_max;
     int64_t alpha_target, max_iterations;
     int32_t adapt;
@@ -100,11 +97,10 @@ struct Params {
 
 // ------------------------------------------------------------------ shared memory
 
-// One staging buffer: every global input of one tile (filled by cp.async).
 struct Stage {
     TileDesc d;
-    double dcon[TP];
-    double x[TPATH], xp[TPATH], dn[TPATH];
+    double dcon[TP];  // duals_k dual_consensus; reused for the T values
+    double xk[TPATH], xo[TPATH], dn[TPATH];
     double D[TCOM], dd[TCOM];
     uint16_t eid[TP], pos[TP];
     int32_t poff[TPATH + 4];  // raw pair_ptr[p0 .. p1]
@@ -112,36 +108,38 @@ struct Stage {
 };
 
 struct Work {
-    double v[TP];
-    double pK[TPATH], pw[TPATH];
+    double y[TP];
+    double pK[TPATH], pw[TPATH], xn[TPATH];
     uint16_t pidx[TP];
-    double wval[NT / 32];
+    double wv1[NT / 32], wv2[NT / 32];
     int32_t wflag[NT / 32];
     double red[NT / 32];
 };
 
 struct Smem {
-    Stage *st[2];
+    Stage *st;
     Work *w;
-    double *acc;
+    double *accT, *accL, *adj;
 };
 
 __device__ __forceinline__ Smem carve(char *base, int E) {
     Smem s;
     char *p = base;
-    s.st[0] = (Stage *)p;
-    p += sizeof(Stage);
-    s.st[1] = (Stage *)p;
+    s.st = (Stage *)p;
     p += sizeof(Stage);
     s.w = (Work *)p;
     p += sizeof(Work);
-    s.acc = (double *)p;
+    s.accT = (double *)p;
+    p += sizeof(double) * E;
+    s.accL = (double *)p;
+    p += sizeof(double) * E;
+    s.adj = (double *)p;
     return s;
 }
 
-static size_t smem_bytes(int E) { return 2 * sizeof(Stage) + sizeof(Work) + sizeof(double) * (size_t)E; }
+static size_t smem_bytes(int E) { return sizeof(Stage) + sizeof(Work) + 3 * sizeof(double) * (size_t)E; }
 
-// ------------------------------------------------------------------ cp.async
+// ------------------------------------------------------------------ cp.async staging
 
 __device__ __forceinline__ void cp16(void *smem, const void *g) {
     unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -155,39 +153,43 @@ __device__ __forceinline__ void cp4(void *smem, const void *g) {
     unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(g));
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+__device__ __forceinline__ void cp_commit_wait_all() {
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::);
 }
 
-enum { MODE_A = 0, MODE_B = 1, MODE_L0 = 2 };
+enum { MODE_M = 0, MODE_RB = 1, MODE_A1 = 2 };
 
-// Issue the copies of one tile's inputs into a staging buffer.
+// Buffers a pass reads/writes (selected from the controller state).
+struct PassIO {
+    const double *dcon_in, *dn_in, *dd_in, *xk, *xo;
+    double *dcon_out, *dn_out, *dd_out, *x_out;
+    double f;
+    int par;  // residual parity of the A-part iteration
+};
+
+// Issue the copies of one tile's inputs, then wait (other CTAs on the SM overlap).
 template <int MODE>
-__device__ __forceinline__ void stage_tile(const Params &P, const TileDesc &d, Stage &st, const double *xk,
-                                           const double *xp) {
+__device__ __forceinline__ void stage_tile(const Params &P, const TileDesc &d, Stage &st, const PassIO &io) {
     const int tid = threadIdx.x;
     const int np = d.np, npath = d.p1 - d.p0, nc = d.c1 - d.c0;
-    if (MODE != MODE_L0)
-        for (int i = tid; i < (np + 1) / 2; i += NT) cp16(&st.dcon[2 * i], &P.dcon[d.sb + 2 * i]);
+    for (int i = tid; i < (np + 1) / 2; i += NT) cp16(&st.dcon[2 * i], &io.dcon_in[d.sb + 2 * i]);
     for (int i = tid; i < (np + 7) / 8; i += NT) {
         cp16(&st.eid[8 * i], &P.slot_eid[d.sb + 8 * i]);
         cp16(&st.pos[8 * i], &P.pos[d.sb + 8 * i]);
     }
     for (int i = tid; i < npath; i += NT) {
-        cp8(&st.x[i], &xk[d.p0 + i]);
-        if (MODE == MODE_A) cp8(&st.xp[i], &xp[d.p0 + i]);
-        if (MODE != MODE_L0) cp8(&st.dn[i], &P.dn[d.p0 + i]);
+        cp8(&st.xk[i], &io.xk[d.p0 + i]);
+        if (MODE == MODE_RB) cp8(&st.xo[i], &io.xo[d.p0 + i]);
+        cp8(&st.dn[i], &io.dn_in[d.p0 + i]);
     }
     for (int i = tid; i <= npath; i += NT) cp4(&st.poff[i], &P.I.pair_ptr[d.p0 + i]);
-    if (MODE != MODE_L0) {
-        for (int i = tid; i <= nc; i += NT) cp4(&st.cpp[i], &P.I.com_path_ptr[d.c0 + i]);
-        for (int i = tid; i < nc; i += NT) {
-            cp8(&st.D[i], &P.I.demand[d.c0 + i]);
-            cp8(&st.dd[i], &P.dd[d.c0 + i]);
-        }
+    for (int i = tid; i <= nc; i += NT) cp4(&st.cpp[i], &P.I.com_path_ptr[d.c0 + i]);
+    for (int i = tid; i < nc; i += NT) {
+        cp8(&st.D[i], &P.I.demand[d.c0 + i]);
+        cp8(&st.dd[i], &io.dd_in[d.c0 + i]);
     }
+    cp_commit_wait_all();
 }
 
 // Block reduction of one double in a fixed tree order (deterministic).
@@ -206,88 +208,106 @@ __device__ double block_sum(double v, double *red) {
     return r;  // valid in thread 0
 }
 
-// Segmented-sum operator on (head flag, value): associative.
-__device__ __forceinline__ void seg_op(int f1, double x1, int &f2, double &x2) {
-    if (!f2) x2 = x1 + x2;
+// Segmented-sum operator on (head flag, value pair): (f1,a1) (+) (f2,a2).
+__device__ __forceinline__ void seg_op2(int f1, double a1, double b1, int &f2, double &a2, double &b2) {
+    if (!f2) {
+        a2 = a1 + a2;
+        b2 = b1 + b2;
+    }
     f2 |= f1;
 }
 
 // Block-wide segmented inclusive scan over the tile's slots (ITEMS consecutive
-// slots per thread) keyed by edge id; the value at the last slot of each edge
-// run is the run total and is added to acc[eid] by the thread owning that slot
-// (each edge has exactly one run per tile: no write conflicts).  The operator
-// tree is fixed, so the result is deterministic.
-__device__ void seg_reduce_runs(const double *vals, const uint16_t *eid, int np, double *acc, Work &W) {
+// slots per thread) keyed by edge id, for two value streams at once.  The value
+// at the last slot of each edge run is that run's total; the thread owning it
+// adds it to acc[eid] (one run per edge per tile: no write conflicts).  Fixed
+// operator tree, so the result is deterministic.
+template <bool TWO>
+__device__ void seg_reduce_runs(const double *v1, const double *v2, const uint16_t *eid, int np, double *acc1,
+                                double *acc2, Work &W) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int base = ITEMS * tid;
     int key[ITEMS + 1];
-    double v[ITEMS];
+    double a[ITEMS], b[ITEMS];
     int h[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         int sl = base + i;
-        key[i] = sl < np ? (int)eid[sl] : -1 - i;
-        v[i] = sl < np ? vals[sl] : 0.0;
+        bool ok = sl < np;
+        key[i] = ok ? (int)eid[sl] : -1 - i;
+        a[i] = ok ? v1[sl] : 0.0;
+        b[i] = (TWO && ok) ? v2[sl] : 0.0;
     }
     key[ITEMS] = base + ITEMS < np ? (int)eid[base + ITEMS] : -100;
     const int kprev = (base > 0 && base - 1 < np) ? (int)eid[base - 1] : -200;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) h[i] = (i == 0 ? key[0] != kprev : key[i] != key[i - 1]);
-    // thread aggregate
     int f = h[0];
-    double x = v[0];
+    double x = a[0], z = b[0];
 #pragma unroll
     for (int i = 1; i < ITEMS; ++i) {
         int fi = h[i];
-        double xi = v[i];
-        seg_op(f, x, fi, xi);
+        double xi = a[i], zi = b[i];
+        seg_op2(f, x, z, fi, xi, zi);
         f = fi;
         x = xi;
+        z = zi;
     }
-    // warp inclusive scan of the thread aggregates
     for (int o = 1; o < 32; o <<= 1) {
         int fo = __shfl_up_sync(0xffffffffu, f, o);
         double xo = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) seg_op(fo, xo, f, x);
+        double zo = TWO ? __shfl_up_sync(0xffffffffu, z, o) : 0.0;
+        if (lane >= o) seg_op2(fo, xo, zo, f, x, z);
     }
     if (lane == 31) {
         W.wflag[warp] = f;
-        W.wval[warp] = x;
+        W.wv1[warp] = x;
+        W.wv2[warp] = z;
     }
     int fe = __shfl_up_sync(0xffffffffu, f, 1);
     double xe = __shfl_up_sync(0xffffffffu, x, 1);
+    double ze = TWO ? __shfl_up_sync(0xffffffffu, z, 1) : 0.0;
     if (lane == 0) {
         fe = 0;
         xe = 0.0;
+        ze = 0.0;
     }
     __syncthreads();
     if (warp == 0) {
-        int wf = lane < NT / 32 ? W.wflag[lane] : 0;
-        double wx = lane < NT / 32 ? W.wval[lane] : 0.0;
+        const bool in = lane < NT / 32;
+        int wf = in ? W.wflag[lane] : 0;
+        double wx = in ? W.wv1[lane] : 0.0, wz = in ? W.wv2[lane] : 0.0;
         for (int o = 1; o < NT / 32; o <<= 1) {
             int fo = __shfl_up_sync(0xffffffffu, wf, o);
             double xo = __shfl_up_sync(0xffffffffu, wx, o);
-            if (lane >= o) seg_op(fo, xo, wf, wx);
+            double zo = __shfl_up_sync(0xffffffffu, wz, o);
+            if (lane >= o) seg_op2(fo, xo, zo, wf, wx, wz);
         }
         int pf_ = __shfl_up_sync(0xffffffffu, wf, 1);
         double px = __shfl_up_sync(0xffffffffu, wx, 1);
-        if (lane < NT / 32) {
+        double pz = __shfl_up_sync(0xffffffffu, wz, 1);
+        if (in) {
             W.wflag[lane] = lane ? pf_ : 0;
-            W.wval[lane] = lane ? px : 0.0;
+            W.wv1[lane] = lane ? px : 0.0;
+            W.wv2[lane] = lane ? pz : 0.0;
         }
     }
     __syncthreads();
     int fp = fe;
-    double xr = xe;
-    seg_op(W.wflag[warp], W.wval[warp], fp, xr);  // exclusive prefix of this thread
+    double xr = xe, zr = ze;
+    seg_op2(W.wflag[warp], W.wv1[warp], W.wv2[warp], fp, xr, zr);  // exclusive prefix of this thread
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         int fi = h[i];
-        double xi = v[i];
-        seg_op(fp, xr, fi, xi);
+        double xi = a[i], zi = b[i];
+        seg_op2(fp, xr, zr, fi, xi, zi);
         fp = fi;
         xr = xi;
-        if (base + i < np && key[i + 1] != key[i]) acc[key[i]] += xi;
+        zr = zi;
+        if (base + i < np && key[i + 1] != key[i]) {
+            acc1[key[i]] += xi;
+            if (TWO) acc2[key[i]] += zi;
+        }
     }
     __syncthreads();
 }
@@ -296,9 +316,9 @@ __device__ void seg_reduce_runs(const double *vals, const uint16_t *eid, int np,
 
 // controller.py:237-273 on the residuals of the iteration just completed.
 __device__ __noinline__ void controller_step(const Params &P, Ctrl &c, double s, double r, int32_t ec, int32_t er) {
-    c.evaluated = c.iteration;
     c.s = s;
     c.r = r;
+    c.f = 1.0;
     if (ec != INT_MAX) {
         c.status = PF_ERR_KERNEL_COEF;
         c.bad = ec;
@@ -323,7 +343,6 @@ __device__ __noinline__ void controller_step(const Params &P, Ctrl &c, double s,
         else
             decision = 2;
     }
-    c.f = 1.0;
     if (P.adapt) {
         if (c.ema_s < 0.0) {
             c.ema_s = s;
@@ -358,31 +377,40 @@ __device__ __noinline__ void controller_step(const Params &P, Ctrl &c, double s,
     }
 }
 
-// Runs in every CTA on its shared-memory copy of the controller state.
+// Every CTA reduces the residual partials in the same fixed order and runs the
+// same scalar controller step on its shared-memory copy of the state.
 __device__ void controller_eval(const Params &P, Ctrl &c) {
     if (threadIdx.x < 32) {
-        double acc[5] = {0, 0, 0, 0, 0};
-        for (int g = threadIdx.x; g < P.G; g += 32)
-            for (int j = 0; j < 5; ++j) acc[j] += __ldcg(&P.res[g * 8 + j]);
-        int ngroups = (P.I.E + RGRP - 1) / RGRP;
+        const int par = (int)(c.iteration & 1);
+        double acc[4] = {0, 0, 0, 0};  // dx, dd, dcon, dn
+        for (int g = threadIdx.x; g < P.G; g += 32) {
+            const double *r = P.res + g * 8;
+            acc[0] += __ldcg(&r[0]);
+            acc[1] += __ldcg(&r[1 + 3 * par]);
+            acc[2] += __ldcg(&r[2 + 3 * par]);
+            acc[3] += __ldcg(&r[3 + 3 * par]);
+        }
         double dcs = 0.0;
+        int ngroups = (P.I.E + RGRP - 1) / RGRP;
         for (int g = threadIdx.x; g < ngroups; g += 32) dcs += __ldcg(&P.res_dc[g]);
-        acc[2] += dcs;
-        for (int j = 0; j < 5; ++j)
+        for (int j = 0; j < 4; ++j)
             for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_down_sync(0xffffffffu, acc[j], o);
-        if (threadIdx.x == 0) controller_step(P, c, sqrt(acc[0]), sqrt(((acc[1] + acc[2]) + acc[3]) + acc[4]),
-                                              __ldcg(&P.err[0]), __ldcg(&P.err[1]));
+        for (int o = 16; o > 0; o >>= 1) dcs += __shfl_down_sync(0xffffffffu, dcs, o);
+        if (threadIdx.x == 0)
+            controller_step(P, c, sqrt(acc[0]), sqrt(((acc[1] + dcs) + acc[2]) + acc[3]), __ldcg(&P.err[0]),
+                            __ldcg(&P.err[1]));
     }
     __syncthreads();
 }
 
 // ------------------------------------------------------------------ edge phase
 
-// Work item (group, slice): lanes = 32 edges of the group, sum CTA partials of
-// the slice in CTA order; the last item of a group combines slices in order and
-// applies kernels.py:212 (dual_capacity) and :94-96 (adjustment).
-__device__ __noinline__ void edge_phase(const Params &P, const Ctrl &c, int g) {
+// Work item (group, slice): lanes = 32 edges of the group, sum the CTA partials
+// of the slice in CTA order; the last item of a group combines the slices in
+// order and applies kernels.py:212 (dual_capacity) and :94-96 (adjustment).
+__device__ __noinline__ void edge_phase(const Params &P, double f) {
     const InstView &I = P.I;
+    const int g = blockIdx.x;
     int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int ngroups = (I.E + RGRP - 1) / RGRP;
     int nitems = ngroups * P.nslices;
@@ -414,7 +442,7 @@ __device__ __noinline__ void edge_phase(const Params &P, const Ctrl &c, int g) {
                     L += __ldcg(&P.sub[(size_t)(P.nslices + k) * I.E + e]);
                 }
                 double cap = I.capacity[e];
-                double dold = __ldcg(&P.dc[e]) * c.f;
+                double dold = __ldcg(&P.dc[e]) * f;
                 double dnew = npmax0(dold + (L - cap));
                 double adj = (T + dnew - cap) / ((double)I.edge_path_count[e] + 1.0);
                 if (adj < 0.0) adj = 0.0;
@@ -432,180 +460,204 @@ __device__ __noinline__ void edge_phase(const Params &P, const Ctrl &c, int g) {
     }
 }
 
-// ------------------------------------------------------------------ sweeps
+// ------------------------------------------------------------------ tile compute
 
-// Per-tile compute of sweep A (kernels.py:206-216 duals of iteration k+1, and the
-// per-edge T = sum(x + dcon') of _k_suggest :88-91).
-__device__ __forceinline__ void tile_A(const Params &P, const TileDesc &d, const Stage &st, Smem &S, double f,
-                                       int first, double &r_dd, double &r_dn, double &r_dcon) {
-    Work &W = *S.w;
-    const int tid = threadIdx.x;
-    const int np = d.np, npath = d.p1 - d.p0, nc = d.c1 - d.c0;
-    if (tid < TPATH) {
-        // per path: dual_nonneg (kernels.py:215) and the slot -> path scatter
-        for (int i = tid; i < npath; i += TPATH) {
-            double dold = st.dn[i] * f;
-            double dnew = npmax0(dold - st.x[i]);
-            P.dn[d.p0 + i] = dnew;
-            double df = dnew - dold;
-            r_dn += df * df;
-            int lo = st.poff[i] - d.t0, hi = st.poff[i + 1] - d.t0;
-            for (int l = lo; l < hi; ++l) W.pidx[st.pos[l]] = (uint16_t)i;
-        }
-    } else {
-        // per commodity: S_c in model.py:297-302 order, dual_demand (kernels.py:211)
-        for (int j = tid - TPATH; j < nc; j += NT - TPATH) {
-            int lo = st.cpp[j] - d.p0, hi = st.cpp[j + 1] - d.p0;
-            double total = 0.0;
-            for (int i = lo; i < hi;) {
-                int k2 = i + 32 < hi ? i + 32 : hi;
-                double part = 0.0;
-                for (int t = i; t < k2; ++t) part += st.x[t];
-                total += part;
-                i = k2;
-            }
-            double dold = st.dd[j] * f;
-            double dnew = npmax0(dold + (total - st.D[j]));
-            P.dd[d.c0 + j] = dnew;
-            double df = dnew - dold;
-            r_dd += df * df;
-        }
-    }
-    __syncthreads();
-    // per slot: y_{k-1} (recomputed), dual_consensus (kernels.py:72), T value (:91)
-    for (int sl = tid; sl < np; sl += NT) {
-        int i = W.pidx[sl];
-        double dk = st.dcon[sl];
-        double y = first ? st.xp[i] : max0(st.xp[i] + dk - P.adj[st.eid[sl]]);
-        double dks = dk * f;
-        double dnew = max0(dks + st.x[i] - y);
-        P.dcon[d.sb + sl] = dnew;
-        double df = dnew - dks;
-        r_dcon += df * df;
-        W.v[sl] = st.x[i] + dnew;
-    }
-    __syncthreads();
-    seg_reduce_runs(W.v, st.eid, np, S.acc, W);
-}
-
-// Per-tile compute of sweep B (kernels.py:235-296 for iteration k+1).
-__device__ __forceinline__ void tile_B(const Params &P, const TileDesc &d, const Stage &st, Smem &S, double beta,
-                                       int64_t alpha, double *xn, double &r_x) {
-    Work &W = *S.w;
-    const int tid = threadIdx.x;
-    const int np = d.np, npath = d.p1 - d.p0, nc = d.c1 - d.c0;
-    // per path: y_k and K_p in path order (kernels.py:98-100, :110-119)
-    for (int i = tid; i < npath; i += NT) {
-        double x = st.x[i];
-        double acc = 0.0;
-        int lo = st.poff[i] - d.t0, hi = st.poff[i + 1] - d.t0;
-        for (int l = lo; l < hi; ++l) {
-            int sl = st.pos[l];
-            double dk = st.dcon[sl];
-            double y = max0(x + dk - P.adj[st.eid[sl]]);
-            W.v[sl] = y;
-            acc += y - dk;
-        }
-        double dn = st.dn[i];
-        double h = (double)(hi - lo);
-        if (x < dn) {
-            W.pK[i] = acc + dn;
-            W.pw[i] = 1.0 / (h + 1.0);
-        } else {
-            W.pK[i] = acc;
-            W.pw[i] = 1.0 / h;
-        }
-    }
-    __syncthreads();
-    // per commodity: W, Q, root, rates (kernels.py:122-131, 176-195, 285-296)
-    for (int j = tid; j < nc; j += NT) {
-        int lo = st.cpp[j] - d.p0, hi = st.cpp[j + 1] - d.p0;
-        int cc = d.c0 + j;
-        double ws = 0.0, qw = 0.0;
-        for (int i = lo; i < hi; ++i) {
-            ws += W.pw[i];
-            qw += W.pw[i] * W.pK[i];
-        }
-        if (!(isfinite(ws) && isfinite(qw))) {
-            atomicMin(&P.err[0], cc);
-            continue;
-        }
-        double D = st.D[j], dd = st.dd[j];
-        double Sc = commodity_root(ws, qw, D - dd, beta, alpha);
-        if (!isfinite(Sc)) atomicMin(&P.err[1], cc);
-        if (P.root_sums) P.root_sums[cc] = Sc;
-        double ct = commodity_term(Sc, D, dd, beta, alpha);
-        for (int i = lo; i < hi; ++i) {
-            double xv = W.pw[i] * (W.pK[i] + ct);
-            xn[d.p0 + i] = xv;
-            double df = xv - st.x[i];
-            r_x += df * df;
-        }
-    }
-    seg_reduce_runs(W.v, st.eid, np, S.acc, W);
-}
-
-// Initial capacity-dual load L(y_0), y_0 = x_0[pair_path] (controller.py:118).
-__device__ __forceinline__ void tile_L0(const TileDesc &d, const Stage &st, Smem &S) {
-    Work &W = *S.w;
-    const int npath = d.p1 - d.p0;
-    for (int i = threadIdx.x; i < npath; i += NT) {
-        int lo = st.poff[i] - d.t0, hi = st.poff[i + 1] - d.t0;
-        for (int l = lo; l < hi; ++l) W.v[st.pos[l]] = st.x[i];
-    }
-    __syncthreads();
-    seg_reduce_runs(W.v, st.eid, d.np, S.acc, W);
-}
-
-// One sweep over this CTA's tiles with double-buffered cp.async staging.
-// Sweep B walks the tiles in reverse so it first re-reads what sweep A wrote last.
+// MODE_M : B(k+1) [y, K/w, roots, x_{k+1}] fused with A(k+2) [duals_{k+2}, T/L]
+// MODE_RB: A(k+2) only, recomputing y_{k+1} from x_k, dcon_{k+1}, adj_{k+1}
+// MODE_A1: A(1) with y_0 = x_0[pair_path] (controller.py:118)
 template <int MODE>
-__device__ __noinline__ void sweep(const Params &P, const Ctrl &c, Smem &S, int g, double *part, double *res3) {
-    const int E = P.I.E;
-    const double *xk = c.cur ? P.x1 : P.x0;
-    double *xo = c.cur ? P.x0 : P.x1;  // x_{k-1} (A: read) / x_{k+1} (B: write)
-    for (int e = threadIdx.x; e < E; e += NT) S.acc[e] = 0.0;
-    const int my = g < P.ntiles ? (P.ntiles - 1 - g) / P.G + 1 : 0;
-    auto tile_of = [&](int k) { return MODE == MODE_B ? g + (my - 1 - k) * P.G : g + k * P.G; };
-    double ra = 0.0, rb = 0.0, rc = 0.0;
-    if (my > 0) {
-        TileDesc d = P.desc[tile_of(0)];
-        stage_tile<MODE>(P, d, *S.st[0], xk, xo);
-        if (threadIdx.x == 0) S.st[0]->d = d;
-        cp_commit();
-    }
-    for (int k = 0; k < my; ++k) {
-        if (k + 1 < my) {
-            TileDesc d = P.desc[tile_of(k + 1)];
-            stage_tile<MODE>(P, d, *S.st[(k + 1) & 1], xk, xo);
-            if (threadIdx.x == 0) S.st[(k + 1) & 1]->d = d;
-            cp_commit();
-            cp_wait<1>();
-        } else {
-            cp_wait<0>();
+__device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, const PassIO &io, Smem &S, double &r_x,
+                                             double &r_dd, double &r_dcon, double &r_dn) {
+    Stage &st = *S.st;
+    Work &W = *S.w;
+    const TileDesc &d = st.d;
+    const int tid = threadIdx.x;
+    const int np = d.np, npath = d.p1 - d.p0, nc = d.c1 - d.c0;
+    const double f = io.f;
+    // paths: y per pair (kernels.py:98-100), slot->path map, K/w (kernels.py:110-119)
+    for (int i = tid; i < npath; i += NT) {
+        const double x = st.xk[i];
+        const double xy = MODE == MODE_RB ? st.xo[i] : x;
+        const int lo = st.poff[i] - d.t0, hi = st.poff[i + 1] - d.t0;
+        double acc = 0.0;
+        for (int l = lo; l < hi; ++l) {
+            const int sl = st.pos[l];
+            W.pidx[sl] = (uint16_t)i;
+            const double dk = st.dcon[sl];
+            const double y = MODE == MODE_A1 ? x : max0(xy + dk - S.adj[st.eid[sl]]);
+            W.y[sl] = y;
+            if (MODE == MODE_M) acc += y - dk;
         }
-        __syncthreads();
-        const Stage &st = *S.st[k & 1];
-        if (MODE == MODE_A)
-            tile_A(P, st.d, st, S, c.f, c.first, ra, rb, rc);
-        else if (MODE == MODE_B)
-            tile_B(P, st.d, st, S, c.beta, c.alpha, xo, ra);
-        else
-            tile_L0(st.d, st, S);
+        if (MODE == MODE_M) {
+            const double dn = st.dn[i];
+            const double h = (double)(hi - lo);
+            if (x < dn) {
+                W.pK[i] = acc + dn;
+                W.pw[i] = 1.0 / (h + 1.0);
+            } else {
+                W.pK[i] = acc;
+                W.pw[i] = 1.0 / h;
+            }
+        }
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < E; e += NT) part[(size_t)g * E + e] = S.acc[e];
-    if (MODE == MODE_A) {
-        double t = block_sum(ra, S.w->red);
-        if (threadIdx.x == 0) res3[1] = t;
-        t = block_sum(rc, S.w->red);
-        if (threadIdx.x == 0) res3[3] = t;
-        t = block_sum(rb, S.w->red);
-        if (threadIdx.x == 0) res3[4] = t;
-    } else if (MODE == MODE_B) {
-        double t = block_sum(ra, S.w->red);
-        if (threadIdx.x == 0) res3[0] = t;
+    // commodities: roots and rates (B), then dual_demand / dual_nonneg (A)
+    for (int j = tid; j < nc; j += NT) {
+        const int lo = st.cpp[j] - d.p0, hi = st.cpp[j + 1] - d.p0;
+        const double D = st.D[j], ddk = st.dd[j];
+        if (MODE == MODE_M) {
+            const int cc = d.c0 + j;
+            double ws = 0.0, qw = 0.0;  // kernels.py:122-131
+            for (int i = lo; i < hi; ++i) {
+                ws += W.pw[i];
+                qw += W.pw[i] * W.pK[i];
+            }
+            double ct = NAN;
+            if (!(isfinite(ws) && isfinite(qw))) {
+                atomicMin(&P.err[0], cc);
+            } else {
+                const double Sc = commodity_root(ws, qw, D - ddk, c.beta, c.alpha);  // kernels.py:176-189
+                if (!isfinite(Sc)) atomicMin(&P.err[1], cc);
+                if (P.root_sums) P.root_sums[cc] = Sc;
+                ct = commodity_term(Sc, D, ddk, c.beta, c.alpha);  // kernels.py:289-294
+            }
+            for (int i = lo; i < hi; ++i) {
+                const double xv = W.pw[i] * (W.pK[i] + ct);  // kernels.py:195
+                W.xn[i] = xv;
+                io.x_out[d.p0 + i] = xv;
+                const double df = xv - st.xk[i];
+                r_x += df * df;
+            }
+        } else {
+            for (int i = lo; i < hi; ++i) W.xn[i] = st.xk[i];
+        }
+        // A: S_c in model.py:297-302 order, dual_demand (kernels.py:211)
+        double total = 0.0;
+        for (int i = lo; i < hi;) {
+            const int k2 = i + 32 < hi ? i + 32 : hi;
+            double part = 0.0;
+            for (int t = i; t < k2; ++t) part += W.xn[t];
+            total += part;
+            i = k2;
+        }
+        const double dold = ddk * f;
+        const double dnew = npmax0(dold + (total - D));
+        io.dd_out[d.c0 + j] = dnew;
+        const double df = dnew - dold;
+        r_dd += df * df;
+        // A: dual_nonneg (kernels.py:215)
+        for (int i = lo; i < hi; ++i) {
+            const double o = st.dn[i] * f;
+            const double n = npmax0(o - W.xn[i]);
+            io.dn_out[d.p0 + i] = n;
+            const double dg = n - o;
+            r_dn += dg * dg;
+        }
     }
+    __syncthreads();
+    // slots: dual_consensus (kernels.py:72) and the T value x + dcon' (kernels.py:91)
+    for (int sl = tid; sl < np; sl += NT) {
+        const int i = W.pidx[sl];
+        const double dks = st.dcon[sl] * f;
+        const double xn = W.xn[i];
+        const double dnew = max0(dks + xn - W.y[sl]);
+        io.dcon_out[d.sb + sl] = dnew;
+        const double df = dnew - dks;
+        r_dcon += df * df;
+        st.dcon[sl] = xn + dnew;
+    }
+    __syncthreads();
+    if (MODE == MODE_RB)
+        seg_reduce_runs<false>(st.dcon, nullptr, st.eid, np, S.accT, nullptr, W);
+    else
+        seg_reduce_runs<true>(st.dcon, W.y, st.eid, np, S.accT, S.accL, W);
+}
+
+template <int MODE>
+__device__ PassIO pass_io(const Params &P, const Ctrl &c) {
+    PassIO io;
+    if (MODE == MODE_M) {  // reads duals_{k+1} (db), x_k (xc); writes the other buffers
+        io.dcon_in = P.dcon[c.db];
+        io.dn_in = P.dn[c.db];
+        io.dd_in = P.dd[c.db];
+        io.xk = P.x[c.xc];
+        io.xo = nullptr;
+        io.dcon_out = P.dcon[c.db ^ 1];
+        io.dn_out = P.dn[c.db ^ 1];
+        io.dd_out = P.dd[c.db ^ 1];
+        io.x_out = P.x[c.xc ^ 1];
+        io.f = 1.0;  // speculative f_{k+1}
+        io.par = (int)((c.iteration + 2) & 1);
+    } else if (MODE == MODE_RB) {  // after the M pass flipped xc/db: duals_{k+1} in db^1, x_{k+1} in xc
+        io.dcon_in = P.dcon[c.db ^ 1];
+        io.dn_in = P.dn[c.db ^ 1];
+        io.dd_in = P.dd[c.db ^ 1];
+        io.xk = P.x[c.xc];
+        io.xo = P.x[c.xc ^ 1];
+        io.dcon_out = P.dcon[c.db];
+        io.dn_out = P.dn[c.db];
+        io.dd_out = P.dd[c.db];
+        io.x_out = nullptr;
+        io.f = c.f;
+        io.par = (int)((c.iteration + 1) & 1);
+    } else {  // A(1): duals_0 in db, x_0 in xc
+        io.dcon_in = P.dcon[c.db];
+        io.dn_in = P.dn[c.db];
+        io.dd_in = P.dd[c.db];
+        io.xk = P.x[c.xc];
+        io.xo = nullptr;
+        io.dcon_out = P.dcon[c.db ^ 1];
+        io.dn_out = P.dn[c.db ^ 1];
+        io.dd_out = P.dd[c.db ^ 1];
+        io.x_out = nullptr;
+        io.f = 1.0;
+        io.par = 1;
+    }
+    return io;
+}
+
+// One pass over this CTA's tiles.  Odd iterations walk the tiles in reverse so a
+// pass first re-reads what the previous pass wrote last (L2 reuse).
+template <int MODE>
+__device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, Smem &S) {
+    const int g = blockIdx.x;
+    const int E = P.I.E;
+    __shared__ PassIO io;  // kept in shared memory: frees ~20 registers per thread
+    if (threadIdx.x == 0) io = pass_io<MODE>(P, c);
+    for (int e = threadIdx.x; e < E; e += NT) {
+        S.accT[e] = 0.0;
+        S.accL[e] = 0.0;
+        S.adj[e] = MODE == MODE_A1 ? 0.0 : __ldcg(&P.adj[e]);
+    }
+    const int my = g < P.ntiles ? (P.ntiles - 1 - g) / P.G + 1 : 0;
+    const bool rev = (c.iteration & 1) != 0;
+    double r_x = 0.0, r_dd = 0.0, r_dcon = 0.0, r_dn = 0.0;
+    for (int k = 0; k < my; ++k) {
+        const int tile = g + (rev ? my - 1 - k : k) * P.G;
+        const TileDesc d = P.desc[tile];
+        __syncthreads();  // previous tile finished with the stage buffer
+        if (threadIdx.x == 0) S.st->d = d;
+        stage_tile<MODE>(P, d, *S.st, io);
+        __syncthreads();
+        tile_compute<MODE>(P, c, io, S, r_x, r_dd, r_dcon, r_dn);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < E; e += NT) {
+        P.partT[(size_t)g * E + e] = S.accT[e];
+        if (MODE != MODE_RB) P.partL[(size_t)g * E + e] = S.accL[e];
+    }
+    double *r = P.res + g * 8;
+    double t;
+    if (MODE == MODE_M) {
+        t = block_sum(r_x, S.w->red);
+        if (threadIdx.x == 0) r[0] = t;
+    }
+    t = block_sum(r_dd, S.w->red);
+    if (threadIdx.x == 0) r[1 + 3 * io.par] = t;
+    t = block_sum(r_dcon, S.w->red);
+    if (threadIdx.x == 0) r[2 + 3 * io.par] = t;
+    t = block_sum(r_dn, S.w->red);
+    if (threadIdx.x == 0) r[3 + 3 * io.par] = t;
 }
 
 // ------------------------------------------------------------------ kernels
@@ -615,64 +667,78 @@ __global__ void __launch_bounds__(NT, 3) k_fused(const __grid_constant__ Params 
     __shared__ Ctrl c;
     Smem S = carve(smem_raw, P.I.E);
     cg::grid_group grid = cg::this_grid();
-    const int g = blockIdx.x;
     if (threadIdx.x == 0) c = *P.ctrl;
     __syncthreads();
+    if (c.need_a1) {
+        pass_tiles<MODE_A1>(P, c, S);
+        grid.sync();
+        if (threadIdx.x == 0) {
+            c.need_a1 = 0;
+            c.db ^= 1;
+            c.need_edge = 1;
+            c.f = 1.0;
+        }
+        __syncthreads();
+    }
     for (;;) {
-        if (c.iteration > c.evaluated) controller_eval(P, c);
+        if (c.need_edge) {
+            edge_phase(P, c.f);
+            grid.sync();
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                c.need_edge = 0;
+                c.f = 1.0;
+            }
+            __syncthreads();
+        }
         if (c.stopped || c.status || c.iteration >= c.target || c.iteration >= P.max_iterations) break;
-        sweep<MODE_A>(P, c, S, g, P.partT, P.res + g * 8);
+        pass_tiles<MODE_M>(P, c, S);
         grid.sync();
-        edge_phase(P, c, g);
-        grid.sync();
-        sweep<MODE_B>(P, c, S, g, P.partL, P.res + g * 8);
         __syncthreads();
         if (threadIdx.x == 0) {
+            c.iteration += 1;
             c.alpha_used = c.alpha;
             c.beta_used = c.beta;
-            c.f = 1.0;
-            c.first = 0;
-            c.cur ^= 1;
-            c.iteration += 1;
+            c.xc ^= 1;
+            c.db ^= 1;
         }
-        grid.sync();
+        __syncthreads();
+        controller_eval(P, c);
+        if (!c.stopped && !c.status && c.f != 1.0) {
+            pass_tiles<MODE_RB>(P, c, S);
+            grid.sync();
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) c.need_edge = 1;
+        __syncthreads();
     }
-    if (g == 0 && threadIdx.x == 0) *P.ctrl = c;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *P.ctrl = c;
 }
 
-__global__ void __launch_bounds__(NT, 3) k_init_L0(const __grid_constant__ Params P) {
-    extern __shared__ __align__(16) char smem_raw[];
-    __shared__ Ctrl c;
-    Smem S = carve(smem_raw, P.I.E);
-    if (threadIdx.x == 0) c = *P.ctrl;
-    __syncthreads();
-    sweep<MODE_L0>(P, c, S, blockIdx.x, P.partL, nullptr);
-}
-
-// Export helpers: reference pair order <- slot order.
-__global__ void k_export_pairs(Params P, const int32_t *pair_tile, const uint16_t *pair_slot, double *y_out,
-                               double *dcon_out) {
+// Export helpers (reference pair order <- slot order), for the state of the last
+// completed iteration k: x_k in x[xc], x_{k-1} in x[xc^1], duals_k in buffer db^1
+// (db holds the speculative duals_{k+1}), adj_k, rescale factor f_k pending.
+__global__ void k_export_pairs(const __grid_constant__ Params P, const int32_t *pair_tile,
+                               const uint16_t *pair_slot, double *y_out, double *dcon_out) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= P.I.NP) return;
-    Ctrl c = *P.ctrl;
-    TileDesc d = P.desc[pair_tile[t]];
-    int sl = d.sb + pair_slot[t];
-    int p = P.I.pair_path[t];
-    const double *xp = c.cur ? P.x0 : P.x1;  // x_{k-1}
-    const double *xk = c.cur ? P.x1 : P.x0;
-    double dk = P.dcon[sl];
-    if (y_out) {
-        if (c.iteration == 0)
-            y_out[t] = xk[p];
-        else
-            y_out[t] = max0(xp[p] + dk - P.adj[P.slot_eid[sl]]);
+    const Ctrl c = *P.ctrl;
+    const TileDesc d = P.desc[pair_tile[t]];
+    const int sl = d.sb + pair_slot[t];
+    const int p = P.I.pair_path[t];
+    if (c.iteration == 0) {
+        if (y_out) y_out[t] = P.x[c.xc][p];
+        if (dcon_out) dcon_out[t] = 0.0;
+        return;
     }
+    const double dk = P.dcon[c.db ^ 1][sl];
+    if (y_out) y_out[t] = max0(P.x[c.xc ^ 1][p] + dk - P.adj[P.slot_eid[sl]]);
     if (dcon_out) dcon_out[t] = dk * c.f;
 }
 
 __global__ void k_scaled_copy(const double *a, int64_t n, const Ctrl *ctrl, double *out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) out[i] = a[i] * ctrl->f;
+    if (i < n) out[i] = ctrl->iteration == 0 ? a[i] : a[i] * ctrl->f;
 }
 
 // ------------------------------------------------------------------ host side
@@ -756,7 +822,8 @@ struct FastSolver {
     std::shared_ptr<TileLayout> L;
     int G = 0, nslices = 1;
     size_t smem = 0;
-    DevBuf<double> dcon, x0, x1, dn, dd, dc, adj, partT, partL, sub, res, res_dc, root_sums;
+    DevBuf<double> dcon[2], dn[2], dd[2], x[2];
+    DevBuf<double> dc, adj, partT, partL, sub, res, res_dc, root_sums;
     DevBuf<int32_t> grp_count, err;
     DevBuf<Ctrl> ctrl;
     Params P{};
@@ -782,7 +849,6 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     require(F->smem <= (size_t)prop.sharedMemPerBlockOptin,
             "fast mode: edge tables do not fit in shared memory (too many edges)");
     PF_CUDA(cudaFuncSetAttribute(k_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F->smem));
-    PF_CUDA(cudaFuncSetAttribute(k_init_L0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F->smem));
     int per_sm = 0;
     PF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused, NT, F->smem));
     require(per_sm >= 1, "fast kernel does not fit on an SM");
@@ -794,11 +860,12 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     F->nslices = std::max(1, std::min(G, warps / std::max(ngroups, 1)));
     F->nslices = std::min(F->nslices, 32);
     int64_t E = I.E ? I.E : 1;
-    F->dcon.alloc(F->L->nslots ? F->L->nslots : 1);
-    F->x0.alloc(I.P ? I.P : 1);
-    F->x1.alloc(I.P ? I.P : 1);
-    F->dn.alloc(I.P ? I.P : 1);
-    F->dd.alloc(I.C ? I.C : 1);
+    for (int b = 0; b < 2; ++b) {
+        F->dcon[b].alloc(F->L->nslots ? F->L->nslots : 1);
+        F->dn[b].alloc(I.P ? I.P : 1);
+        F->dd[b].alloc(I.C ? I.C : 1);
+        F->x[b].alloc(I.P ? I.P : 1);
+    }
     F->dc.alloc(E);
     F->adj.alloc(E);
     F->partT.alloc((size_t)G * E);
@@ -821,11 +888,12 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     P.desc = F->L->desc.p;
     P.slot_eid = F->L->slot_eid.p;
     P.pos = F->L->pos.p;
-    P.dcon = F->dcon.p;
-    P.x0 = F->x0.p;
-    P.x1 = F->x1.p;
-    P.dn = F->dn.p;
-    P.dd = F->dd.p;
+    for (int b = 0; b < 2; ++b) {
+        P.dcon[b] = F->dcon[b].p;
+        P.dn[b] = F->dn[b].p;
+        P.dd[b] = F->dd[b].p;
+        P.x[b] = F->x[b].p;
+    }
     P.dc = F->dc.p;
     P.adj = F->adj.p;
     P.partT = F->partT.p;
@@ -860,13 +928,15 @@ void fast_set_comm(FastSolver *F, const CommOps *ops) { F->comm = ops; }
 
 void fast_init(FastSolver *F, const double *d_x0, int64_t alpha0, double beta0, cudaStream_t s) {
     const Index &I = *F->inst->idx;
-    PF_CUDA(cudaMemcpyAsync(F->x0.p, d_x0, sizeof(double) * I.P, cudaMemcpyDeviceToDevice, s));
-    PF_CUDA(cudaMemcpyAsync(F->x1.p, d_x0, sizeof(double) * I.P, cudaMemcpyDeviceToDevice, s));
-    PF_CUDA(cudaMemsetAsync(F->dcon.p, 0, F->dcon.bytes(), s));
-    PF_CUDA(cudaMemsetAsync(F->dn.p, 0, F->dn.bytes(), s));
-    PF_CUDA(cudaMemsetAsync(F->dd.p, 0, F->dd.bytes(), s));
+    for (int b = 0; b < 2; ++b) {
+        PF_CUDA(cudaMemcpyAsync(F->x[b].p, d_x0, sizeof(double) * I.P, cudaMemcpyDeviceToDevice, s));
+        PF_CUDA(cudaMemsetAsync(F->dcon[b].p, 0, F->dcon[b].bytes(), s));
+        PF_CUDA(cudaMemsetAsync(F->dn[b].p, 0, F->dn[b].bytes(), s));
+        PF_CUDA(cudaMemsetAsync(F->dd[b].p, 0, F->dd[b].bytes(), s));
+    }
     PF_CUDA(cudaMemsetAsync(F->dc.p, 0, F->dc.bytes(), s));
     PF_CUDA(cudaMemsetAsync(F->adj.p, 0, F->adj.bytes(), s));
+    PF_CUDA(cudaMemsetAsync(F->partT.p, 0, F->partT.bytes(), s));
     PF_CUDA(cudaMemsetAsync(F->partL.p, 0, F->partL.bytes(), s));
     PF_CUDA(cudaMemsetAsync(F->res.p, 0, F->res.bytes(), s));
     PF_CUDA(cudaMemsetAsync(F->res_dc.p, 0, F->res_dc.bytes(), s));
@@ -878,18 +948,13 @@ void fast_init(FastSolver *F, const double *d_x0, int64_t alpha0, double beta0, 
     c.ema_s = c.ema_r = -1.0;
     c.f = 1.0;
     c.alpha = c.alpha_used = alpha0;
-    c.iteration = 0;
-    c.evaluated = 0;
-    c.first = 1;
-    c.cur = 0;
     c.s = c.r = NAN;
     c.bad = -1;
+    c.xc = 0;
+    c.db = 0;
+    c.need_a1 = 1;
+    c.need_edge = 0;
     h2d(F->ctrl.p, &c, 1, s);
-    if (I.P) {
-        k_init_L0<<<F->G, NT, F->smem, s>>>(F->P);
-        PF_CHECK_LAUNCH();
-        ++F->launches;
-    }
     PF_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -898,16 +963,14 @@ int64_t fast_run(FastSolver *F, int64_t max_steps, cudaStream_t s, float *ms) {
     d2h(&c, F->ctrl.p, 1, s);
     PF_CUDA(cudaStreamSynchronize(s));
     int64_t start = c.iteration;
-    if (F->inst->idx->P == 0 || max_steps <= 0) {
+    if (F->inst->idx->P == 0 || max_steps <= 0 || c.stopped || c.status) {
         if (ms) *ms = 0.f;
         return 0;
     }
     int64_t target = start + max_steps;
-    // write the new target into the device controller
     PF_CUDA(cudaMemcpyAsync((char *)F->ctrl.p + offsetof(Ctrl, target), &target, sizeof(int64_t),
                             cudaMemcpyHostToDevice, s));
-    Params P = F->P;
-    void *args[] = {&P};
+    void *args[] = {(void *)&F->P};
     PF_CUDA(cudaEventRecord(F->e0, s));
     PF_CUDA(cudaLaunchCooperativeKernel((const void *)k_fused, dim3(F->G), dim3(NT), args, F->smem, s));
     PF_CHECK_LAUNCH();
@@ -942,7 +1005,7 @@ FastStatus fast_status(FastSolver *F, cudaStream_t s) {
 const double *fast_x(FastSolver *F) {
     Ctrl c;
     PF_CUDA(cudaMemcpy(&c, F->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost));
-    return c.cur ? F->x1.p : F->x0.p;
+    return F->x[c.xc].p;
 }
 
 const double *fast_root_sums(FastSolver *F) { return F->root_sums.p; }
@@ -950,15 +1013,19 @@ const double *fast_root_sums(FastSolver *F) { return F->root_sums.p; }
 void fast_export_state(FastSolver *F, double *x, double *y, double *dd, double *dc, double *dcon, double *dn,
                        cudaStream_t s) {
     const Index &I = *F->inst->idx;
-    DevBuf<double> dy(I.NP ? I.NP : 1), ddc(I.NP ? I.NP : 1), tmp(std::max<int64_t>({I.C, I.E, I.P, 1}));
-    if (I.NP) k_export_pairs<<<ceil_div(I.NP, 256), 256, 0, s>>>(F->P, F->L->pair_tile.p, F->L->pair_slot.p, dy.p, ddc.p);
-    PF_CHECK_LAUNCH();
     Ctrl c;
     d2h(&c, F->ctrl.p, 1, s);
     PF_CUDA(cudaStreamSynchronize(s));
-    if (x) d2h(x, c.cur ? F->x1.p : F->x0.p, I.P, s);
+    const int dcur = c.iteration == 0 ? c.db : (c.db ^ 1);
+    DevBuf<double> dy(I.NP ? I.NP : 1), ddc(I.NP ? I.NP : 1), tmp(std::max<int64_t>({I.C, I.E, I.P, 1}));
+    if (I.NP)
+        k_export_pairs<<<ceil_div(I.NP, 256), 256, 0, s>>>(F->P, F->L->pair_tile.p, F->L->pair_slot.p, dy.p,
+                                                           ddc.p);
+    PF_CHECK_LAUNCH();
+    if (x) d2h(x, F->x[c.xc].p, I.P, s);
     if (y) d2h(y, dy.p, I.NP, s);
     if (dcon) d2h(dcon, ddc.p, I.NP, s);
+    PF_CUDA(cudaStreamSynchronize(s));
     auto scaled = [&](const double *src, int64_t n, double *out) {
         if (!out || !n) return;
         k_scaled_copy<<<ceil_div(n, 256), 256, 0, s>>>(src, n, F->ctrl.p, tmp.p);
@@ -966,10 +1033,9 @@ void fast_export_state(FastSolver *F, double *x, double *y, double *dd, double *
         d2h(out, tmp.p, n, s);
         PF_CUDA(cudaStreamSynchronize(s));
     };
-    PF_CUDA(cudaStreamSynchronize(s));
-    scaled(F->dd.p, I.C, dd);
+    scaled(F->dd[dcur].p, I.C, dd);
     scaled(F->dc.p, I.E, dc);
-    scaled(F->dn.p, I.P, dn);
+    scaled(F->dn[dcur].p, I.P, dn);
 }
 
 void fast_stats(FastSolver *F, int64_t *launches, int64_t *tiles, int64_t *grid, int64_t *bytes) {
@@ -977,12 +1043,12 @@ void fast_stats(FastSolver *F, int64_t *launches, int64_t *tiles, int64_t *grid,
     if (launches) *launches = F->launches;
     if (tiles) *tiles = F->L->ntiles;
     if (grid) *grid = F->G;
-    // compulsory HBM bytes per iteration of this kernel's data layout:
-    //  per slot: dcon r/w in A (16) + r in B (8) + slot_eid A,B (4) + pos A,B (4)
-    //  per path: x_k (A,B 16) + x_{k-1} (A 8) + x_{k+1} write (8) + dn r/w A + r B (24) + pair_ptr A,B (8)
-    //  per commodity: dd r/w A + r B (24) + demand A,B (16) + com_path_ptr A,B (8)
-    //  per CTA: edge partials written and read back (2 x 2 x 8 B per edge)
-    if (bytes) *bytes = 32 * F->L->nslots + 64 * I.P + 48 * I.C + (int64_t)F->G * I.E * 32;
+    // compulsory HBM bytes per iteration of this layout (one fused pass):
+    //  per slot: dual_consensus read + write (16) + slot_eid (2) + pos (2)
+    //  per path: x_k read + x_{k+1} write (16) + dual_nonneg read + write (16) + pair_ptr (4)
+    //  per commodity: dual_demand read + write (16) + demand (8) + com_path_ptr (4)
+    //  per CTA: edge partials T and L written and read back (4 x 8 B per edge)
+    if (bytes) *bytes = 20 * F->L->nslots + 36 * I.P + 28 * I.C + (int64_t)F->G * I.E * 32;
 }
 
 }  // namespace pf
