@@ -46,7 +46,7 @@ namespace pf {
 constexpr int NT = 256;        // threads per CTA (3 CTAs per SM)
 constexpr int TP = 1024;       // max pairs (slots) per tile
 constexpr int ITEMS = TP / NT; // slots per thread in the segmented scan
-constexpr int TPATH = 256;     // max paths per tile
+constexpr int TPATH = 256;     // max paths per tile (u8 local path index)
 constexpr int TCOM = 128;      // max commodities per tile
 constexpr int SLOT_ALIGN = 64; // tile slot start alignment
 constexpr int RGRP = 32;       // edges per reduction group (one lane per edge)
@@ -62,6 +62,7 @@ struct TileLayout {
     DevBuf<TileDesc> desc;      // per tile
     DevBuf<uint16_t> slot_eid;  // [nslots] edge id per slot (sorted within a tile)
     DevBuf<uint16_t> pos;       // [nslots] slot of the tile's l-th pair (path-major), at sb + l
+    DevBuf<uint8_t> spath;      // [nslots] tile-local path index of each slot
     DevBuf<uint16_t> pair_slot; // [NP] tile-local slot of pair t (export only)
     DevBuf<int32_t> pair_tile;  // [NP] tile of pair t (export only)
     std::vector<TileDesc> h_desc;
@@ -80,6 +81,7 @@ struct Params {
     int32_t ntiles, G, nslices, pad;
     const TileDesc *desc;
     const uint16_t *slot_eid, *pos;
+    const uint8_t *spath;
     double *dcon[2], *dn[2], *dd[2], *x[2];
     double *dc, *adj;
     double *partT, *partL;  // [G][E]
@@ -103,6 +105,7 @@ struct Stage {
     double xk[TPATH], xo[TPATH], dn[TPATH];
     double D[TCOM], dd[TCOM];
     uint16_t eid[TP], pos[TP];
+    uint8_t spath[TP];        // tile-local path of each slot
     int32_t poff[TPATH + 4];  // raw pair_ptr[p0 .. p1]
     int32_t cpp[TCOM + 4];    // raw com_path_ptr[c0 .. c1]
 };
@@ -110,7 +113,8 @@ struct Stage {
 struct Work {
     double y[TP];
     double pK[TPATH], pw[TPATH], xn[TPATH];
-    uint16_t pidx[TP];
+    double ct[TCOM];
+    uint8_t pcom[TPATH];
     double wv1[NT / 32], wv2[NT / 32];
     int32_t wflag[NT / 32];
     double red[NT / 32];
@@ -178,6 +182,7 @@ __device__ __forceinline__ void stage_tile(const Params &P, const TileDesc &d, S
         cp16(&st.eid[8 * i], &P.slot_eid[d.sb + 8 * i]);
         cp16(&st.pos[8 * i], &P.pos[d.sb + 8 * i]);
     }
+    for (int i = tid; i < (np + 15) / 16; i += NT) cp16(&st.spath[16 * i], &P.spath[d.sb + 16 * i]);
     for (int i = tid; i < npath; i += NT) {
         cp8(&st.xk[i], &io.xk[d.p0 + i]);
         if (MODE == MODE_RB) cp8(&st.xo[i], &io.xo[d.p0 + i]);
@@ -465,6 +470,8 @@ __device__ __noinline__ void edge_phase(const Params &P, double f) {
 // MODE_M : B(k+1) [y, K/w, roots, x_{k+1}] fused with A(k+2) [duals_{k+2}, T/L]
 // MODE_RB: A(k+2) only, recomputing y_{k+1} from x_k, dcon_{k+1}, adj_{k+1}
 // MODE_A1: A(1) with y_0 = x_0[pair_path] (controller.py:118)
+// Every phase is parallel over slots or paths; only the sum-root runs one thread
+// per commodity.
 template <int MODE>
 __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, const PassIO &io, Smem &S, double &r_x,
                                              double &r_dd, double &r_dcon, double &r_dn) {
@@ -474,22 +481,31 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     const int tid = threadIdx.x;
     const int np = d.np, npath = d.p1 - d.p0, nc = d.c1 - d.c0;
     const double f = io.f;
-    // paths: y per pair (kernels.py:98-100), slot->path map, K/w (kernels.py:110-119)
-    for (int i = tid; i < npath; i += NT) {
-        const double x = st.xk[i];
-        const double xy = MODE == MODE_RB ? st.xo[i] : x;
-        const int lo = st.poff[i] - d.t0, hi = st.poff[i + 1] - d.t0;
-        double acc = 0.0;
-        for (int l = lo; l < hi; ++l) {
-            const int sl = st.pos[l];
-            W.pidx[sl] = (uint16_t)i;
-            const double dk = st.dcon[sl];
-            const double y = MODE == MODE_A1 ? x : max0(xy + dk - S.adj[st.eid[sl]]);
-            W.y[sl] = y;
-            if (MODE == MODE_M) acc += y - dk;
-        }
-        if (MODE == MODE_M) {
-            const double dn = st.dn[i];
+    // (1) slots: y (kernels.py:98-100) and y - dcon (kernels.py:114); path -> commodity map
+    for (int sl = tid; sl < np; sl += NT) {
+        const int i = st.spath[sl];
+        const double dk = st.dcon[sl];
+        double y;
+        if (MODE == MODE_A1)
+            y = st.xk[i];
+        else
+            y = max0((MODE == MODE_RB ? st.xo[i] : st.xk[i]) + dk - S.adj[st.eid[sl]]);
+        W.y[sl] = y;
+    }
+    if (MODE == MODE_M)
+        for (int j = tid; j < nc; j += NT)
+            for (int i = st.cpp[j] - d.p0; i < st.cpp[j + 1] - d.p0; ++i) W.pcom[i] = (uint8_t)j;
+    __syncthreads();
+    if (MODE == MODE_M) {
+        // (2) paths: K_p in path order, frozen non-negativity activity (kernels.py:110-119)
+        for (int i = tid; i < npath; i += NT) {
+            const int lo = st.poff[i] - d.t0, hi = st.poff[i + 1] - d.t0;
+            double acc = 0.0;
+            for (int l = lo; l < hi; ++l) {
+                const int sl = st.pos[l];
+                acc += W.y[sl] - st.dcon[sl];
+            }
+            const double x = st.xk[i], dn = st.dn[i];
             const double h = (double)(hi - lo);
             if (x < dn) {
                 W.pK[i] = acc + dn;
@@ -499,15 +515,12 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
                 W.pw[i] = 1.0 / h;
             }
         }
-    }
-    __syncthreads();
-    // commodities: roots and rates (B), then dual_demand / dual_nonneg (A)
-    for (int j = tid; j < nc; j += NT) {
-        const int lo = st.cpp[j] - d.p0, hi = st.cpp[j + 1] - d.p0;
-        const double D = st.D[j], ddk = st.dd[j];
-        if (MODE == MODE_M) {
+        __syncthreads();
+        // (3) commodities: W, Q (kernels.py:122-131), sum root (kernels.py:176-189), rate term (:289-294)
+        for (int j = tid; j < nc; j += NT) {
+            const int lo = st.cpp[j] - d.p0, hi = st.cpp[j + 1] - d.p0;
             const int cc = d.c0 + j;
-            double ws = 0.0, qw = 0.0;  // kernels.py:122-131
+            double ws = 0.0, qw = 0.0;
             for (int i = lo; i < hi; ++i) {
                 ws += W.pw[i];
                 qw += W.pw[i] * W.pK[i];
@@ -516,22 +529,48 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
             if (!(isfinite(ws) && isfinite(qw))) {
                 atomicMin(&P.err[0], cc);
             } else {
-                const double Sc = commodity_root(ws, qw, D - ddk, c.beta, c.alpha);  // kernels.py:176-189
+                const double D = st.D[j], ddk = st.dd[j];
+                const double Sc = commodity_root(ws, qw, D - ddk, c.beta, c.alpha);
                 if (!isfinite(Sc)) atomicMin(&P.err[1], cc);
                 if (P.root_sums) P.root_sums[cc] = Sc;
-                ct = commodity_term(Sc, D, ddk, c.beta, c.alpha);  // kernels.py:289-294
+                ct = commodity_term(Sc, D, ddk, c.beta, c.alpha);
             }
-            for (int i = lo; i < hi; ++i) {
-                const double xv = W.pw[i] * (W.pK[i] + ct);  // kernels.py:195
-                W.xn[i] = xv;
-                io.x_out[d.p0 + i] = xv;
-                const double df = xv - st.xk[i];
-                r_x += df * df;
-            }
-        } else {
-            for (int i = lo; i < hi; ++i) W.xn[i] = st.xk[i];
+            W.ct[j] = ct;
         }
-        // A: S_c in model.py:297-302 order, dual_demand (kernels.py:211)
+        __syncthreads();
+    }
+    // (4) paths: new rate (kernels.py:195) and dual_nonneg (kernels.py:215)
+    for (int i = tid; i < npath; i += NT) {
+        double xv;
+        if (MODE == MODE_M) {
+            xv = W.pw[i] * (W.pK[i] + W.ct[W.pcom[i]]);
+            io.x_out[d.p0 + i] = xv;
+            const double df = xv - st.xk[i];
+            r_x += df * df;
+        } else {
+            xv = st.xk[i];
+        }
+        W.xn[i] = xv;
+        const double o = st.dn[i] * f;
+        const double n = npmax0(o - xv);
+        io.dn_out[d.p0 + i] = n;
+        const double dg = n - o;
+        r_dn += dg * dg;
+    }
+    __syncthreads();
+    // (5) slots: dual_consensus (kernels.py:72), T value x + dcon' (kernels.py:91);
+    //     commodities: S_c in model.py:297-302 order and dual_demand (kernels.py:211)
+    for (int sl = tid; sl < np; sl += NT) {
+        const double dks = st.dcon[sl] * f;
+        const double xn = W.xn[st.spath[sl]];
+        const double dnew = max0(dks + xn - W.y[sl]);
+        io.dcon_out[d.sb + sl] = dnew;
+        const double df = dnew - dks;
+        r_dcon += df * df;
+        st.dcon[sl] = xn + dnew;
+    }
+    for (int j = tid; j < nc; j += NT) {
+        const int lo = st.cpp[j] - d.p0, hi = st.cpp[j + 1] - d.p0;
         double total = 0.0;
         for (int i = lo; i < hi;) {
             const int k2 = i + 32 < hi ? i + 32 : hi;
@@ -540,31 +579,11 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
             total += part;
             i = k2;
         }
-        const double dold = ddk * f;
-        const double dnew = npmax0(dold + (total - D));
+        const double dold = st.dd[j] * f;
+        const double dnew = npmax0(dold + (total - st.D[j]));
         io.dd_out[d.c0 + j] = dnew;
         const double df = dnew - dold;
         r_dd += df * df;
-        // A: dual_nonneg (kernels.py:215)
-        for (int i = lo; i < hi; ++i) {
-            const double o = st.dn[i] * f;
-            const double n = npmax0(o - W.xn[i]);
-            io.dn_out[d.p0 + i] = n;
-            const double dg = n - o;
-            r_dn += dg * dg;
-        }
-    }
-    __syncthreads();
-    // slots: dual_consensus (kernels.py:72) and the T value x + dcon' (kernels.py:91)
-    for (int sl = tid; sl < np; sl += NT) {
-        const int i = W.pidx[sl];
-        const double dks = st.dcon[sl] * f;
-        const double xn = W.xn[i];
-        const double dnew = max0(dks + xn - W.y[sl]);
-        io.dcon_out[d.sb + sl] = dnew;
-        const double df = dnew - dks;
-        r_dcon += df * df;
-        st.dcon[sl] = xn + dnew;
     }
     __syncthreads();
     if (MODE == MODE_RB)
@@ -681,6 +700,9 @@ __global__ void __launch_bounds__(NT, 3) k_fused(const __grid_constant__ Params 
         __syncthreads();
     }
     for (;;) {
+        // the pending edge phase belongs to the next iteration: run it only when
+        // continuing, so a stopped / paused state keeps adj_k for export
+        if (c.stopped || c.status || c.iteration >= c.target || c.iteration >= P.max_iterations) break;
         if (c.need_edge) {
             edge_phase(P, c.f);
             grid.sync();
@@ -691,7 +713,6 @@ __global__ void __launch_bounds__(NT, 3) k_fused(const __grid_constant__ Params 
             }
             __syncthreads();
         }
-        if (c.stopped || c.status || c.iteration >= c.target || c.iteration >= P.max_iterations) break;
         pass_tiles<MODE_M>(P, c, S);
         grid.sync();
         __syncthreads();
@@ -785,6 +806,7 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
     L->ntiles = (int32_t)tiles.size();
     L->nslots = slot;
     std::vector<uint16_t> pair_slot(I.NP), slot_eid(slot ? slot : 1, (uint16_t)0), pos(slot ? slot : 1, (uint16_t)0);
+    std::vector<uint8_t> spath(slot ? slot : 1, (uint8_t)0);
     std::vector<int32_t> pair_tile(I.NP);
 #pragma omp parallel for schedule(dynamic, 16)
     for (int64_t ti = 0; ti < (int64_t)tiles.size(); ++ti) {
@@ -793,22 +815,28 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         for (int32_t l = 0; l < T.np; ++l) ord[l] = l;
         std::stable_sort(ord.begin(), ord.end(),
                          [&](int32_t a, int32_t b) { return pedge[T.t0 + a] < pedge[T.t0 + b]; });
+        std::vector<uint8_t> lpath(T.np);
+        for (int32_t p = T.p0; p < T.p1; ++p)
+            for (int32_t t = pptr[p]; t < pptr[p + 1]; ++t) lpath[t - T.t0] = (uint8_t)(p - T.p0);
         for (int32_t sl = 0; sl < T.np; ++sl) {
             int32_t l = ord[sl];
             pair_slot[T.t0 + l] = (uint16_t)sl;
             pair_tile[T.t0 + l] = (int32_t)ti;
             slot_eid[T.sb + sl] = (uint16_t)pedge[T.t0 + l];
             pos[T.sb + l] = (uint16_t)sl;
+            spath[T.sb + sl] = lpath[l];
         }
     }
     L->desc.alloc(tiles.size() ? tiles.size() : 1);
     L->slot_eid.alloc(slot ? slot : 1);
     L->pos.alloc(slot ? slot : 1);
+    L->spath.alloc(slot ? slot : 1);
     L->pair_slot.alloc(I.NP ? I.NP : 1);
     L->pair_tile.alloc(I.NP ? I.NP : 1);
     h2d(L->desc.p, tiles.data(), tiles.size(), s);
     h2d(L->slot_eid.p, slot_eid.data(), slot, s);
     h2d(L->pos.p, pos.data(), slot, s);
+    h2d(L->spath.p, spath.data(), slot, s);
     h2d(L->pair_slot.p, pair_slot.data(), I.NP, s);
     h2d(L->pair_tile.p, pair_tile.data(), I.NP, s);
     PF_CUDA(cudaStreamSynchronize(s));
@@ -888,6 +916,7 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     P.desc = F->L->desc.p;
     P.slot_eid = F->L->slot_eid.p;
     P.pos = F->L->pos.p;
+    P.spath = F->L->spath.p;
     for (int b = 0; b < 2; ++b) {
         P.dcon[b] = F->dcon[b].p;
         P.dn[b] = F->dn[b].p;
@@ -1044,11 +1073,11 @@ void fast_stats(FastSolver *F, int64_t *launches, int64_t *tiles, int64_t *grid,
     if (tiles) *tiles = F->L->ntiles;
     if (grid) *grid = F->G;
     // compulsory HBM bytes per iteration of this layout (one fused pass):
-    //  per slot: dual_consensus read + write (16) + slot_eid (2) + pos (2)
+    //  per slot: dual_consensus read + write (16) + slot_eid (2) + pos (2) + spath (1)
     //  per path: x_k read + x_{k+1} write (16) + dual_nonneg read + write (16) + pair_ptr (4)
     //  per commodity: dual_demand read + write (16) + demand (8) + com_path_ptr (4)
     //  per CTA: edge partials T and L written and read back (4 x 8 B per edge)
-    if (bytes) *bytes = 20 * F->L->nslots + 36 * I.P + 28 * I.C + (int64_t)F->G * I.E * 32;
+    if (bytes) *bytes = 21 * F->L->nslots + 36 * I.P + 28 * I.C + (int64_t)F->G * I.E * 32;
 }
 
 }  // namespace pf
