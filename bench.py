@@ -43,6 +43,8 @@ CONFIGS = {
     "cfg1": (40, 4, 1.5, "GEANT-sized: random_topology(40), all-pairs gravity, k=4"),
     "cfg1_v0.3": (40, 4, 0.3, "GEANT-sized, V=0.3*cap (reference stop rule fires)"),
     "cfg2": (500, 8, 1.5, "synthetic 500-node WAN, all-pairs gravity, k=8 (~18.3M demand-path pairs)"),
+    "cfg2_v0.3": (500, 8, 0.3, "500-node WAN, V=0.3*cap, k=8"),
+    "target_k4_v0.3": (500, 4, 0.3, "north-star target scale: 500-node all-pairs, k=4 (~1M paths), V=0.3*cap"),
 }
 
 
