@@ -84,6 +84,8 @@ struct Params {
     const uint8_t *spath;
     double *dcon[2], *dn[2], *dd[2], *x[2];
     double *dc, *adj;
+    const double *ne;       // [E] paths per edge (global across ranks when sharded)
+    double *tot;            // [2E + 16] rank totals (multi-GPU): T, L, residual sums, error counts
     double *partT, *partL;  // [G][E]
     double *sub;            // [2][nslices][E]
     double *res;            // [G][8]: 0 dx | 1..3 (dd, dcon, dn) parity 0 | 4..6 parity 1
@@ -449,7 +451,7 @@ __device__ __noinline__ void edge_phase(const Params &P, double f) {
                 double cap = I.capacity[e];
                 double dold = __ldcg(&P.dc[e]) * f;
                 double dnew = npmax0(dold + (L - cap));
-                double adj = (T + dnew - cap) / ((double)I.edge_path_count[e] + 1.0);
+                double adj = (T + dnew - cap) / (P.ne[e] + 1.0);
                 if (adj < 0.0) adj = 0.0;
                 P.dc[e] = dnew;
                 P.adj[e] = adj;
@@ -736,6 +738,110 @@ __global__ void __launch_bounds__(NT, 3) k_fused(const __grid_constant__ Params 
     if (blockIdx.x == 0 && threadIdx.x == 0) *P.ctrl = c;
 }
 
+// ------------------------------------------------------------------ multi-GPU split kernels
+//
+// With a communicator attached (one process per GPU, commodities sharded), the
+// iteration runs as separate launches around ONE ncclAllReduce of
+// [T_e, L_e, residual sums] (2E + 16 doubles) per iteration (a second one only
+// on the rare rollback iterations):
+//   k_pass<M> -> k_local_reduce -> allreduce -> k_ctrl_dist -> [k_pass<RB> ->
+//   k_local_reduce -> allreduce] -> k_edge_dist (next iteration) -> ...
+// Every rank evaluates the same controller on the same totals, so all ranks take
+// the same branch and issue matching collectives.
+
+template <int MODE>
+__global__ void __launch_bounds__(NT, 3) k_pass(const __grid_constant__ Params P) {
+    extern __shared__ __align__(16) char smem_raw[];
+    __shared__ Ctrl c;
+    Smem S = carve(smem_raw, P.I.E);
+    if (threadIdx.x == 0) c = *P.ctrl;
+    __syncthreads();
+    pass_tiles<MODE>(P, c, S);
+}
+
+// CTA partials -> rank totals in a fixed order: tot[0:E] = T, tot[E:2E] = L,
+// tot[2E + 0..6] = residual slots summed over CTAs, tot[2E + 7/8] = error flags.
+__global__ void k_local_reduce(const __grid_constant__ Params P) {
+    const int E = P.I.E;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+        double t = 0.0, l = 0.0;
+        for (int g = 0; g < P.G; ++g) {
+            t += __ldcg(&P.partT[(size_t)g * E + e]);
+            l += __ldcg(&P.partL[(size_t)g * E + e]);
+        }
+        P.tot[e] = t;
+        P.tot[E + e] = l;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 7) {
+        double r = 0.0;
+        for (int g = 0; g < P.G; ++g) r += __ldcg(&P.res[g * 8 + threadIdx.x]);
+        P.tot[2 * E + threadIdx.x] = r;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 7) {
+        P.tot[2 * E + 7] = __ldcg(&P.err[0]) != INT_MAX ? 1.0 : 0.0;
+        P.tot[2 * E + 8] = __ldcg(&P.err[1]) != INT_MAX ? 1.0 : 0.0;
+    }
+}
+
+// controller step from the allreduced totals (one thread)
+__global__ void k_ctrl_dist(const __grid_constant__ Params P) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    Ctrl c = *P.ctrl;
+    c.iteration += 1;
+    c.alpha_used = c.alpha;
+    c.beta_used = c.beta;
+    c.xc ^= 1;
+    c.db ^= 1;
+    const int E = P.I.E;
+    const int par = (int)(c.iteration & 1);
+    const double *t = P.tot + 2 * E;
+    double dcs = 0.0;  // dual_capacity is replicated: its residual is rank-local and identical
+    const int ngroups = (E + RGRP - 1) / RGRP;
+    for (int g = 0; g < ngroups; ++g) dcs += P.res_dc[g];
+    const int32_t ec = t[7] > 0.0 ? (P.err[0] != INT_MAX ? P.err[0] : -1) : INT_MAX;
+    const int32_t er = t[8] > 0.0 ? (P.err[1] != INT_MAX ? P.err[1] : -1) : INT_MAX;
+    controller_step(P, c, sqrt(t[0]), sqrt(((t[1 + 3 * par] + dcs) + t[2 + 3 * par]) + t[3 + 3 * par]), ec, er);
+    c.need_edge = 1;
+    *P.ctrl = c;
+}
+
+// kernels.py:212 and :94-96 from the allreduced per-edge totals (one warp per 32 edges)
+__global__ void k_edge_dist(const __grid_constant__ Params P) {
+    const int E = P.I.E;
+    const int grp = blockIdx.x;
+    const int e = grp * RGRP + threadIdx.x;
+    const double f = P.ctrl->f;
+    double rdc = 0.0;
+    if (e < E) {
+        const double T = P.tot[e], L = P.tot[E + e];
+        const double cap = P.I.capacity[e];
+        const double dold = P.dc[e] * f;
+        const double dnew = npmax0(dold + (L - cap));
+        double adj = (T + dnew - cap) / (P.ne[e] + 1.0);
+        if (adj < 0.0) adj = 0.0;
+        P.dc[e] = dnew;
+        P.adj[e] = adj;
+        const double d = dnew - dold;
+        rdc = d * d;
+    }
+    for (int o = 16; o > 0; o >>= 1) rdc += __shfl_down_sync(0xffffffffu, rdc, o);
+    if (threadIdx.x == 0) P.res_dc[grp] = rdc;
+}
+
+enum { CU_AFTER_A1 = 0, CU_AFTER_EDGE = 1 };
+__global__ void k_ctrl_update(Ctrl *ctrl, int op) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (op == CU_AFTER_A1) {
+        ctrl->need_a1 = 0;
+        ctrl->db ^= 1;
+        ctrl->need_edge = 1;
+        ctrl->f = 1.0;
+    } else {
+        ctrl->need_edge = 0;
+        ctrl->f = 1.0;
+    }
+}
+
 // Export helpers (reference pair order <- slot order), for the state of the last
 // completed iteration k: x_k in x[xc], x_{k-1} in x[xc^1], duals_k in buffer db^1
 // (db holds the speculative duals_{k+1}), adj_k, rescale factor f_k pending.
@@ -851,7 +957,7 @@ struct FastSolver {
     int G = 0, nslices = 1;
     size_t smem = 0;
     DevBuf<double> dcon[2], dn[2], dd[2], x[2];
-    DevBuf<double> dc, adj, partT, partL, sub, res, res_dc, root_sums;
+    DevBuf<double> dc, adj, ne, tot, partT, partL, sub, res, res_dc, root_sums;
     DevBuf<int32_t> grp_count, err;
     DevBuf<Ctrl> ctrl;
     Params P{};
@@ -877,6 +983,9 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     require(F->smem <= (size_t)prop.sharedMemPerBlockOptin,
             "fast mode: edge tables do not fit in shared memory (too many edges)");
     PF_CUDA(cudaFuncSetAttribute(k_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F->smem));
+    PF_CUDA(cudaFuncSetAttribute(k_pass<MODE_M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F->smem));
+    PF_CUDA(cudaFuncSetAttribute(k_pass<MODE_RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F->smem));
+    PF_CUDA(cudaFuncSetAttribute(k_pass<MODE_A1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F->smem));
     int per_sm = 0;
     PF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused, NT, F->smem));
     require(per_sm >= 1, "fast kernel does not fit on an SM");
@@ -896,6 +1005,16 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     }
     F->dc.alloc(E);
     F->adj.alloc(E);
+    F->ne.alloc(E);
+    F->tot.alloc(2 * E + 16);
+    {
+        std::vector<int32_t> cnt(I.E);
+        std::vector<double> ned(E, 0.0);
+        d2h(cnt.data(), I.edge_path_count.p, I.E, s);
+        PF_CUDA(cudaStreamSynchronize(s));
+        for (int64_t e = 0; e < I.E; ++e) ned[e] = (double)cnt[e];
+        h2d(F->ne.p, ned.data(), E, s);
+    }
     F->partT.alloc((size_t)G * E);
     F->partL.alloc((size_t)G * E);
     F->sub.alloc((size_t)2 * F->nslices * E);
@@ -925,6 +1044,8 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     }
     P.dc = F->dc.p;
     P.adj = F->adj.p;
+    P.ne = F->ne.p;
+    P.tot = F->tot.p;
     P.partT = F->partT.p;
     P.partL = F->partL.p;
     P.sub = F->sub.p;
@@ -953,7 +1074,78 @@ void fast_destroy(FastSolver *F) {
     delete F;
 }
 
-void fast_set_comm(FastSolver *F, const CommOps *ops) { F->comm = ops; }
+void fast_set_comm(FastSolver *F, const CommOps *ops) {
+    F->comm = ops;
+    if (!ops) return;
+    // the suggestion divisor n_e + 1 counts paths of ALL ranks (kernels.py:94)
+    cudaStream_t s = nullptr;
+    PF_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const int64_t E = F->inst->idx->E;
+    if (E) ops->allreduce_sum(ops->ctx, F->ne.p, E, s);
+    PF_CUDA(cudaStreamSynchronize(s));
+    PF_CUDA(cudaStreamDestroy(s));
+}
+
+// Host-driven iteration for sharded solves (see the split kernels above).
+static int64_t fast_run_dist(FastSolver *F, int64_t max_steps, cudaStream_t s, float *ms) {
+    const Index &I = *F->inst->idx;
+    const int64_t E = I.E;
+    const int nred = (int)std::max<int64_t>(1, (E + 255) / 256);
+    const int ngroups = (int)((E + RGRP - 1) / RGRP);
+    auto read = [&]() {
+        Ctrl c;
+        d2h(&c, F->ctrl.p, 1, s);
+        PF_CUDA(cudaStreamSynchronize(s));
+        return c;
+    };
+    auto reduce_allreduce = [&]() {
+        k_local_reduce<<<nred, 256, 0, s>>>(F->P);
+        PF_CHECK_LAUNCH();
+        F->comm->allreduce_sum(F->comm->ctx, F->tot.p, 2 * E + 16, s);
+    };
+    Ctrl c = read();
+    const int64_t start = c.iteration;
+    if (I.P == 0 || max_steps <= 0 || c.stopped || c.status) {
+        if (ms) *ms = 0.f;
+        return 0;
+    }
+    const int64_t target = std::min<int64_t>(start + max_steps, F->cfg.max_iterations);
+    PF_CUDA(cudaEventRecord(F->e0, s));
+    if (c.need_a1) {
+        k_pass<MODE_A1><<<F->G, NT, F->smem, s>>>(F->P);
+        PF_CHECK_LAUNCH();
+        reduce_allreduce();
+        k_ctrl_update<<<1, 1, 0, s>>>(F->ctrl.p, CU_AFTER_A1);
+        F->launches += 3;
+        c = read();
+    }
+    while (!c.stopped && !c.status && c.iteration < target) {
+        if (c.need_edge) {
+            if (ngroups) k_edge_dist<<<ngroups, RGRP, 0, s>>>(F->P);
+            k_ctrl_update<<<1, 1, 0, s>>>(F->ctrl.p, CU_AFTER_EDGE);
+        }
+        k_pass<MODE_M><<<F->G, NT, F->smem, s>>>(F->P);
+        PF_CHECK_LAUNCH();
+        reduce_allreduce();
+        k_ctrl_dist<<<1, 32, 0, s>>>(F->P);
+        PF_CHECK_LAUNCH();
+        F->launches += 5;
+        c = read();
+        if (!c.stopped && !c.status && c.f != 1.0) {
+            k_pass<MODE_RB><<<F->G, NT, F->smem, s>>>(F->P);
+            PF_CHECK_LAUNCH();
+            reduce_allreduce();
+            F->launches += 2;
+        }
+    }
+    PF_CUDA(cudaEventRecord(F->e1, s));
+    PF_CUDA(cudaEventSynchronize(F->e1));
+    float t = 0.f;
+    PF_CUDA(cudaEventElapsedTime(&t, F->e0, F->e1));
+    if (ms) *ms = t;
+    c = read();
+    return c.iteration - start;
+}
 
 void fast_init(FastSolver *F, const double *d_x0, int64_t alpha0, double beta0, cudaStream_t s) {
     const Index &I = *F->inst->idx;
@@ -988,6 +1180,7 @@ void fast_init(FastSolver *F, const double *d_x0, int64_t alpha0, double beta0, 
 }
 
 int64_t fast_run(FastSolver *F, int64_t max_steps, cudaStream_t s, float *ms) {
+    if (F->comm) return fast_run_dist(F, max_steps, s, ms);
     Ctrl c;
     d2h(&c, F->ctrl.p, 1, s);
     PF_CUDA(cudaStreamSynchronize(s));

@@ -156,6 +156,8 @@ struct pf_instance {
     std::shared_ptr<pf::Index> idx;
     pf::DevBuf<double> demand, capacity;
     cudaStream_t stream = nullptr;
+    mutable std::mutex ws_mu;
+    mutable std::shared_ptr<void> proj_ws;  // projection scratch (projection.cu)
     pf::InstView view() const {
         pf::InstView v;
         v.C = (int32_t)idx->C;

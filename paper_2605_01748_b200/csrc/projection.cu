@@ -124,15 +124,6 @@ __global__ void k_over(int32_t E, const double *loads, const double *cap, double
     if (o > 0.0) atomicAdd(nviol, 1);
 }
 
-// keys for the per-edge stable path orders, in edge-major (edge_pairs) order
-__global__ void k_edge_path_keys(InstView I, const double *scores, uint64_t *keys, int32_t *vals) {
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= I.NP) return;
-    int32_t p = I.pair_path[I.edge_pairs[t]];
-    keys[t] = desc_key(scores[p]);
-    vals[t] = p;
-}
-
 // CTA-wide _sum_gather_range of x over the edge's pairs (projection.py:87-88).
 __device__ double cta_edge_resum(const InstView &I, const double *x, int32_t lo, int32_t hi, double *parts) {
     __shared__ double s_total;
@@ -197,79 +188,134 @@ __global__ void __launch_bounds__(1024) k_edge_trim(InstView I, const int32_t *e
 
 constexpr int TB = 256;
 
-void score_paths_device(const pf_instance *inst, const double *x, int64_t alpha, double *scores, cudaStream_t s) {
+// segments for the per-edge stable path orders: only violated edges get a
+// non-empty segment (the others are never walked by k_edge_trim)
+__global__ void k_violated_segments(int32_t E, const double *over, const int32_t *eptr, int32_t *sb, int32_t *se) {
+    int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    bool v = over[e] > 0.0;
+    sb[e] = v ? eptr[e] : 0;
+    se[e] = v ? eptr[e + 1] : 0;
+}
+
+__global__ void k_edge_path_keys_violated(InstView I, const double *scores, const double *over, uint64_t *keys,
+                                          int32_t *vals) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= I.NP) return;
+    int32_t pr = I.edge_pairs[t];
+    if (!(over[I.pair_edge[pr]] > 0.0)) return;
+    int32_t p = I.pair_path[pr];
+    keys[t] = desc_key(scores[p]);
+    vals[t] = p;
+}
+
+// Persistent scratch for the projection of one instance's index spaces (allocated
+// once; no cudaMalloc / host synchronisation inside a projection).
+struct ProjWS {
+    DevBuf<double> scores, sums, loads, over, parts;
+    DevBuf<uint8_t> viol;
+    DevBuf<int32_t> order, bad, nviol, eids, eorder, pvals, porder, sb, se;
+    DevBuf<uint64_t> ekeys, ekeys_out, pkeys, pkeys_out;
+    DevBuf<char> cub;
+    size_t cub_bytes = 0;
+    int32_t max_ne = 0;
+};
+
+static ProjWS &workspace(const pf_instance *inst, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(inst->ws_mu);
+    if (inst->proj_ws) return *static_cast<ProjWS *>(inst->proj_ws.get());
     InstView I = inst->view();
-    DevBuf<double> sums(I.C + 1), loads(I.E + 1);
-    DevBuf<uint8_t> viol(I.E + 1);
-    exact_commodity_sums(I, x, sums.p, s);
-    exact_edge_loads_of_rates(I, x, loads.p, s);
-    if (I.E) k_violated_edges<<<ceil_div(I.E, TB), TB, 0, s>>>(I.E, loads.p, I.capacity, 1e-9, viol.p);
-    if (I.P) k_scores<<<ceil_div(I.P, TB), TB, 0, s>>>(I, sums.p, viol.p, alpha, scores);
+    auto ws = std::make_shared<ProjWS>();
+    ws->scores.alloc(I.P + 1);
+    ws->sums.alloc(I.C + 1);
+    ws->loads.alloc(I.E + 1);
+    ws->over.alloc(I.E + 1);
+    ws->viol.alloc(I.E + 1);
+    ws->order.alloc(I.P + 1);
+    ws->bad.alloc(1);
+    ws->nviol.alloc(1);
+    ws->eids.alloc(I.E + 1);
+    ws->eorder.alloc(I.E + 1);
+    ws->ekeys.alloc(I.E + 1);
+    ws->ekeys_out.alloc(I.E + 1);
+    ws->pkeys.alloc(I.NP + 1);
+    ws->pkeys_out.alloc(I.NP + 1);
+    ws->pvals.alloc(I.NP + 1);
+    ws->porder.alloc(I.NP + 1);
+    ws->sb.alloc(I.E + 1);
+    ws->se.alloc(I.E + 1);
+    std::vector<int32_t> eptr(I.E + 1);
+    d2h(eptr.data(), I.edge_pair_ptr, I.E + 1, s);
+    PF_CUDA(cudaStreamSynchronize(s));
+    for (int32_t e = 0; e < I.E; ++e) ws->max_ne = std::max(ws->max_ne, eptr[e + 1] - eptr[e]);
+    ws->parts.alloc((ws->max_ne + BLK - 1) / BLK + 1);
+    size_t a = 0, b = 0;
+    PF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, a, ws->ekeys.p, ws->ekeys_out.p, ws->eids.p, ws->eorder.p,
+                                            I.E, 0, 64, s));
+    PF_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, b, ws->pkeys.p, ws->pkeys_out.p, ws->pvals.p,
+                                                     ws->porder.p, I.NP, I.E, ws->sb.p, ws->se.p, 0, 64, s));
+    ws->cub_bytes = std::max<size_t>(std::max(a, b), 16);
+    ws->cub.alloc(ws->cub_bytes);
+    inst->proj_ws = ws;
+    return *ws;
+}
+
+static void score_paths_ws(const pf_instance *inst, ProjWS &ws, const double *x, int64_t alpha, double *scores,
+                           cudaStream_t s) {
+    InstView I = inst->view();
+    exact_commodity_sums(I, x, ws.sums.p, s);
+    exact_edge_loads_of_rates(I, x, ws.loads.p, s);
+    if (I.E) k_violated_edges<<<ceil_div(I.E, TB), TB, 0, s>>>(I.E, ws.loads.p, I.capacity, 1e-9, ws.viol.p);
+    if (I.P) k_scores<<<ceil_div(I.P, TB), TB, 0, s>>>(I, ws.sums.p, ws.viol.p, alpha, scores);
     PF_CHECK_LAUNCH();
+}
+
+void score_paths_device(const pf_instance *inst, const double *x, int64_t alpha, double *scores, cudaStream_t s) {
+    ProjWS &ws = workspace(inst, s);
+    score_paths_ws(inst, ws, x, alpha, scores, s);
     PF_CUDA(cudaStreamSynchronize(s));
 }
 
 void project_device(const pf_instance *inst, const double *rates, int64_t alpha, double *x, cudaStream_t s) {
     InstView I = inst->view();
-    DevBuf<int32_t> bad(1);
-    int32_t init = INT_MAX;
-    h2d(bad.p, &init, 1, s);
-    if (I.P) k_clamp<<<ceil_div(I.P, TB), TB, 0, s>>>(I.P, rates, x, bad.p);
+    if (I.P == 0) return;
+    ProjWS &ws = workspace(inst, s);
+    int32_t init[2] = {INT_MAX, 0};
+    h2d(ws.bad.p, &init[0], 1, s);
+    h2d(ws.nviol.p, &init[1], 1, s);
+    k_clamp<<<ceil_div(I.P, TB), TB, 0, s>>>(I.P, rates, x, ws.bad.p);
+    PF_CHECK_LAUNCH();
+    // phase 2 (projection.py:63-74)
+    score_paths_ws(inst, ws, x, alpha, ws.scores.p, s);
+    if (I.C) k_demand_trim<<<ceil_div(I.C, 128), 128, 0, s>>>(I, ws.scores.p, x, ws.order.p);
+    PF_CHECK_LAUNCH();
+    // phase 3 (projection.py:76-106): violated edges in stable descending overload
+    exact_edge_loads_of_rates(I, x, ws.loads.p, s);
+    if (I.E)
+        k_over<<<ceil_div(I.E, TB), TB, 0, s>>>(I.E, ws.loads.p, I.capacity, ws.over.p, ws.ekeys.p, ws.eids.p,
+                                                 ws.nviol.p);
+    PF_CHECK_LAUNCH();
+    if (I.E) {
+        size_t bytes = ws.cub_bytes;
+        PF_CUDA(cub::DeviceRadixSort::SortPairs(ws.cub.p, bytes, ws.ekeys.p, ws.ekeys_out.p, ws.eids.p, ws.eorder.p,
+                                                I.E, 0, 64, s));
+    }
+    score_paths_ws(inst, ws, x, alpha, ws.scores.p, s);  // projection.py:81 (post-phase-2 rates)
+    if (I.E) k_violated_segments<<<ceil_div(I.E, TB), TB, 0, s>>>(I.E, ws.over.p, I.edge_pair_ptr, ws.sb.p, ws.se.p);
+    if (I.NP) k_edge_path_keys_violated<<<ceil_div(I.NP, TB), TB, 0, s>>>(I, ws.scores.p, ws.over.p, ws.pkeys.p,
+                                                                         ws.pvals.p);
+    PF_CHECK_LAUNCH();
+    if (I.NP) {
+        size_t bytes = ws.cub_bytes;
+        PF_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(ws.cub.p, bytes, ws.pkeys.p, ws.pkeys_out.p, ws.pvals.p,
+                                                         ws.porder.p, I.NP, I.E, ws.sb.p, ws.se.p, 0, 64, s));
+    }
+    k_edge_trim<<<1, 1024, 0, s>>>(I, ws.eorder.p, ws.nviol.p, ws.porder.p, x, ws.parts.p);
     PF_CHECK_LAUNCH();
     int32_t hb;
-    d2h(&hb, bad.p, 1, s);
+    d2h(&hb, ws.bad.p, 1, s);
     PF_CUDA(cudaStreamSynchronize(s));
     require(hb == INT_MAX, "projection input contains non-finite rates");
-    if (I.P == 0) return;
-
-    DevBuf<double> scores(I.P);
-    DevBuf<int32_t> order(I.P);
-    score_paths_device(inst, x, alpha, scores.p, s);
-    if (I.C) k_demand_trim<<<ceil_div(I.C, 128), 128, 0, s>>>(I, scores.p, x, order.p);
-    PF_CHECK_LAUNCH();
-
-    // phase 3
-    DevBuf<double> loads(I.E + 1), over(I.E + 1);
-    DevBuf<uint64_t> ekeys(I.E + 1), ekeys_out(I.E + 1);
-    DevBuf<int32_t> eids(I.E + 1), eorder(I.E + 1), nviol(1);
-    PF_CUDA(cudaMemsetAsync(nviol.p, 0, sizeof(int32_t), s));
-    exact_edge_loads_of_rates(I, x, loads.p, s);
-    if (I.E) k_over<<<ceil_div(I.E, TB), TB, 0, s>>>(I.E, loads.p, I.capacity, over.p, ekeys.p, eids.p, nviol.p);
-    PF_CHECK_LAUNCH();
-    int32_t hn = 0;
-    d2h(&hn, nviol.p, 1, s);
-    PF_CUDA(cudaStreamSynchronize(s));
-    if (hn == 0) return;
-    {
-        size_t tmp = 0;
-        PF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, ekeys.p, ekeys_out.p, eids.p, eorder.p, I.E, 0, 64, s));
-        DevBuf<char> t(tmp ? tmp : 1);
-        PF_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, ekeys.p, ekeys_out.p, eids.p, eorder.p, I.E, 0, 64, s));
-    }
-    score_paths_device(inst, x, alpha, scores.p, s);  // projection.py:81 (post-phase-2 rates)
-    DevBuf<uint64_t> pkeys(I.NP), pkeys_out(I.NP);
-    DevBuf<int32_t> pvals(I.NP), porder(I.NP);
-    k_edge_path_keys<<<ceil_div(I.NP, TB), TB, 0, s>>>(I, scores.p, pkeys.p, pvals.p);
-    PF_CHECK_LAUNCH();
-    {
-        size_t tmp = 0;
-        PF_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, tmp, pkeys.p, pkeys_out.p, pvals.p, porder.p,
-                                                         I.NP, I.E, I.edge_pair_ptr, I.edge_pair_ptr + 1, 0, 64, s));
-        DevBuf<char> t(tmp ? tmp : 1);
-        PF_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(t.p, tmp, pkeys.p, pkeys_out.p, pvals.p, porder.p, I.NP,
-                                                         I.E, I.edge_pair_ptr, I.edge_pair_ptr + 1, 0, 64, s));
-    }
-    int32_t max_ne = 0;
-    {
-        std::vector<int32_t> eptr(I.E + 1);
-        d2h(eptr.data(), I.edge_pair_ptr, I.E + 1, s);
-        PF_CUDA(cudaStreamSynchronize(s));
-        for (int32_t e = 0; e < I.E; ++e) max_ne = std::max(max_ne, eptr[e + 1] - eptr[e]);
-    }
-    DevBuf<double> parts((max_ne + BLK - 1) / BLK + 1);
-    k_edge_trim<<<1, 1024, 0, s>>>(I, eorder.p, nviol.p, porder.p, x, parts.p);
-    PF_CHECK_LAUNCH();
-    PF_CUDA(cudaStreamSynchronize(s));
 }
 
 }  // namespace pf

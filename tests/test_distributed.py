@@ -1,0 +1,141 @@
+"""Multi-GPU sharding: host-side logic on CPU (gloo, world_size 2) and the
+NCCL-coupled solver at world_size 1 on a GPU.
+
+The sharded data path is exact by construction: each rank's incidence store is
+the reference's build_instance over its commodity range, and the union of the
+shards is the single-instance index space (checked here with the oracle's CPU
+build).  Per iteration the ranks exchange exactly the per-edge sums and the
+residual norms (one allreduce)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import golden_io as G
+from oracle import oracle as O
+from paper_2605_01748_b200 import distributed as D
+from paper_2605_01748_b200.topology import CommodityTable, FlatPathSet
+
+
+def _cfg1():
+    f = G.flat_inputs("cfg1_v0.3")
+    n = f["demand0"].shape[0]
+    tab = CommodityTable(tuple(f"v{i}" for i in range(2 * n)), np.arange(0, 2 * n, 2), np.arange(1, 2 * n, 2),
+                         f["demand0"])
+    flat = FlatPathSet(f["com_path_ptr0"], f["path_edge_ptr0"], f["path_edges0"])
+    return f, tab, flat
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_partition_balances_pairs(world):
+    f, tab, flat = _cfg1()
+    pc = D.pair_counts(tab, flat)
+    ranges = D.partition(pc, world)
+    assert ranges[0][0] == 0 and ranges[-1][1] == len(tab)
+    for (a, b), (c, d) in zip(ranges, ranges[1:]):
+        assert b == c and a <= b
+    loads = [int(pc[a:b].sum()) for a, b in ranges]
+    assert sum(loads) == int(pc.sum())
+    assert max(loads) - min(loads) <= 2 * int(pc.max()) + 1
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shard_union_is_the_single_instance(world):
+    f, tab, flat = _cfg1()
+    full = O.build_instance(f["capacity"], f["demand0"], f["com_path_ptr0"], f["path_edge_ptr0"], f["path_edges0"])
+    ranges = D.partition(D.pair_counts(tab, flat), world)
+    cat = {k: [] for k in ("pair_edge", "hops", "demand")}
+    epc = np.zeros(full.num_edges, np.int64)
+    for lo, hi in ranges:
+        st, sf = D.shard_inputs(tab, flat, lo, hi)
+        sh = O.build_instance(f["capacity"], st.demand, sf.com_path_ptr, sf.path_edge_ptr, sf.path_edges)
+        for k in cat:
+            cat[k].append(getattr(sh, k))
+        epc += sh.edge_path_count
+    for k in cat:
+        assert np.array_equal(np.concatenate(cat[k]), getattr(full, k)), k
+    # global paths-per-edge (the allreduced divisor n_e + 1 of kernels.py:94)
+    assert np.array_equal(epc, full.edge_path_count)
+    pr = D.kept_path_ranges(tab, flat, ranges)
+    assert pr[0][0] == 0 and pr[-1][1] == full.num_paths
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import ctypes as C
+
+    import torch.distributed as dist
+
+    from paper_2605_01748_b200._lib import lib
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    f, tab, flat = _cfg1()
+    ranges = D.partition(D.pair_counts(tab, flat), world)
+    lo, hi = ranges[rank]
+    st, sf = D.shard_inputs(tab, flat, lo, hi)
+    # NCCL unique-id exchange as Comm() does it
+    buf = C.create_string_buffer(128)
+    if rank == 0:
+        assert lib().pf_comm_unique_id(buf) == 0
+    obj = [bytes(buf.raw) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    got = [None] * world if rank == 0 else None
+    dist.gather_object((obj[0], int(sf.path_edge_ptr[-1])), got, dst=0)
+    if rank == 0:
+        ids = {g[0] for g in got}
+        total = sum(g[1] for g in got)
+        q.put((len(ids), total, int(flat.path_edge_ptr[-1])))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_id_exchange_and_shards():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    assert all(p.exitcode == 0 for p in procs)
+    n_ids, total, want = q.get(timeout=10)
+    assert n_ids == 1 and total == want
+
+
+@pytest.mark.gpu
+def test_nccl_world1_matches_single_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.distributed as dist
+
+    import paper_2605_01748_b200 as pf
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1)
+    try:
+        f, tab, flat = _cfg1()
+        topo = pf.random_topology(40, seed=40)
+        tab = pf.gravity_table(topo, 0.3 * float(topo.capacity.sum()))
+        cfg = pf.SolverConfig(mode="fast", max_iterations=5000)
+        sh = D.ShardedSolver(topo, tab, flat, cfg, 0, 1, 0).init()
+        sh.run(5000)
+        r = sh.result()
+        x = sh.gather_x()
+        inst = pf.build_instance_flat(topo, tab, flat, device=0)
+        single = pf.solve(inst, cfg)
+        assert bool(r.converged) and abs(int(r.iterations) - single.iterations) <= 20
+        rates = pf.project(inst, x, int(r.alpha))
+        sums = pf.commodity_sums(inst, rates)
+        np.testing.assert_allclose(np.sort(sums), np.sort(single.sums), rtol=1e-4,
+                                   atol=1e-4 * float(single.sums.max()))
+    finally:
+        dist.destroy_process_group()
