@@ -2,37 +2,51 @@
 // steps) as ONE persistent, grid-synchronised kernel per run of iterations.
 //
 // Layout (TileLayout, built once per instance):
-//   Commodities are cut into TILES of <= TP consecutive pairs (commodity-major,
-//   the reference's own pair order).  Inside a tile the pairs are stored in
-//   SLOTS sorted by edge id (stable), so every edge's pairs form one contiguous
-//   run per tile.  Per slot: `slot_eid` (u16); per tile-local pair (path-major,
-//   stored at the tile's slot base): `pos` (u16 slot of that pair).  Tiles start
-//   on a 64-slot boundary.  The only per-pair STATE is dual_consensus (fp64, slot
-//   order, double buffered); y is never stored.
+//   Commodities are packed into GROUPS of consecutive commodities holding at
+//   most 32 paths (one lane per path), and groups into TILES of NW groups (one
+//   warp per group) and at most `tps` demand-path pairs.  Dynamic per-pair state
+//   (dual_consensus, double buffered) is stored in the reference's pair order
+//   (path-major) with every tile starting on a 16-slot boundary, so a tile is
+//   one contiguous, 128-byte aligned range.  The static per-tile metadata
+//   (edge id per pair, tile-local path per pair, the pair permutation that sorts
+//   the tile's pairs by edge, path / commodity / group offsets) is one
+//   contiguous 16-byte aligned block.  y is never stored.
+//
+// Per tile: one elected thread issues TMA bulk copies (cp.async.bulk) of the
+// tile's dual_consensus, metadata, rates, dual_nonneg, demand and dual_demand
+// into a double-buffered shared-memory stage completing on an mbarrier, one
+// tile ahead of the compute.  Each warp then runs its commodity group:
+//   pairs (lanes over pairs):   y                               kernels.py:98-100
+//   paths (lane = path):        K_p, frozen activity test, w    kernels.py:110-119
+//   commodity (lane segments):  W, Q by segmented shuffles, sum
+//                               root, rate term, x_{k+1}        kernels.py:122-195
+//   pairs:                      dual_consensus, T = x + dcon'   kernels.py:72, :91
+// and the CTA reduces the tile's per-edge T and L = sum y with a warp-level
+// segmented scan over the edge-sorted permutation into CTA-private shared
+// accumulators (one run per edge per tile, so no write conflicts).
 //
 // One pass per iteration.  Iteration k+1 of the reference is
 //   A(k+1): duals_{k+1} from (x_k, y_k, duals_k * f_k)        kernels.py:206-216
 //   E(k+1): dual_capacity_{k+1}, adjustment_{k+1} per edge    kernels.py:88-96, 212
 //   B(k+1): y_{k+1}, coefficients, sum roots, x_{k+1}         kernels.py:235-296
 // and the pass M(k+1) fuses B(k+1) with A(k+2): y_{k+1} and x_{k+1} never leave
-// shared memory before they are consumed by the next dual update, so each pair
-// costs one fp64 read + one fp64 write of dual_consensus per iteration (~20 B
-// with its two u16 indices).  A(k+2) needs the rescale factor f_{k+1} of the
-// controller step that follows B(k+1) (controller.py:251-266); the pass
-// speculates f = 1 (certain during the post-change cooldown and when adapt is
-// off) and a ROLLBACK pass recomputes A(k+2) from the still-intact duals_{k+1}
-// buffers on the rare iterations where beta changes.
+// shared memory before they are consumed by the next dual update.  A(k+2) needs
+// the rescale factor f_{k+1} of the controller step that follows B(k+1)
+// (controller.py:251-266); the pass speculates f = 1 (certain during the
+// post-change cooldown and when adapt is off) and a ROLLBACK pass recomputes
+// A(k+2) from the still-intact duals_{k+1} buffers on the rare iterations where
+// beta changes.
 //
 // Per iteration: M pass -> grid barrier -> controller (every CTA evaluates the
 // same scalar logic from the residual partials) [-> rollback pass -> barrier]
-// -> edge phase -> barrier.  Edge sums are reduced deterministically: a block
-// segmented scan over each tile's edge runs into CTA-private shared-memory
-// accumulators, then CTA partials in a fixed order.  The association differs
-// from the reference's sequential per-edge sums, so fast mode is
-// tolerance-matched (PF_MODE_EXACT is the bitwise path).
+// -> edge phase -> barrier.  Every reduction has a fixed association, so fast
+// mode is deterministic run to run; the association differs from the
+// reference's sequential per-edge sums, so it is tolerance-matched
+// (PF_MODE_EXACT is the bitwise path).
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <array>
 #include <climits>
 #include <cmath>
 #include <cstring>
@@ -43,30 +57,96 @@ namespace cg = cooperative_groups;
 
 namespace pf {
 
-constexpr int NT = 256;        // threads per CTA (3 CTAs per SM)
-constexpr int TP = 1024;       // max pairs (slots) per tile
-constexpr int ITEMS = TP / NT; // slots per thread in the segmented scan
-constexpr int TPATH = 256;     // max paths per tile (u8 local path index)
-constexpr int TCOM = 128;      // max commodities per tile
-constexpr int SLOT_ALIGN = 64; // tile slot start alignment
-constexpr int RGRP = 32;       // edges per reduction group (one lane per edge)
-static_assert(ITEMS * NT == TP, "tile = ITEMS slots per thread");
+constexpr int NW = 4;             // warps per CTA = commodity groups per tile
+constexpr int NT = 32 * NW;       // threads per CTA
+constexpr int GPATH = 32;         // max paths per group (one lane per path)
+constexpr int TPATH = NW * GPATH; // max paths per tile
+constexpr int TCOM = TPATH;       // max commodities per tile
+constexpr int TPS_MIN = 1536;     // default max pairs per tile
+constexpr int SLOT_ALIGN = 16;    // tile start alignment in the per-pair arrays (128 B)
+constexpr int RGRP = 32;          // edges per reduction group (one lane per edge)
+constexpr unsigned FULL = 0xffffffffu;
 
 struct TileDesc {
-    int32_t c0, c1, p0, p1, t0, np, sb, pad;
+    int32_t c0, c1, p0, p1, t0, np, sb, mb16;  // mb16: metadata offset / 16
 };
 
+__host__ __device__ __forceinline__ int r16(int b) { return (b + 15) & ~15; }
+__host__ __device__ __forceinline__ int even(int n) { return (n + 1) & ~1; }
+
+// Byte offsets of the sections of one tile's metadata block.
+struct MetaOff {
+    int eid, perm, spath, poff, pcom, cpp, gpath, bytes;
+};
+__host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc) {
+    MetaOff m;
+    int o = 0;
+    m.eid = o;  // u16 [np] edge id of each pair (path-major)
+    o += r16(2 * np);
+    m.perm = o;  // u16 [np] tile-local pair of each edge-sorted slot
+    o += r16(2 * np);
+    m.spath = o;  // u8 [np] tile-local path of each pair
+    o += r16(np);
+    m.poff = o;  // u16 [npath + 1] tile-local pair offset of each path
+    o += r16(2 * (npath + 1));
+    m.pcom = o;  // u8 [npath] tile-local commodity of each path
+    o += r16(npath);
+    m.cpp = o;  // u16 [nc + 1] tile-local path offset of each commodity
+    o += r16(2 * (nc + 1));
+    m.gpath = o;  // u16 [NW + 1] tile-local path offset of each group
+    o += r16(2 * (NW + 1));
+    m.bytes = o;
+    return m;
+}
+
+// Dynamic shared memory: two stages + work arrays + the per-edge tables.
+struct SmemPlan {
+    int stage, s_dcon, s_meta, s_xk, s_xo, s_dn, s_D, s_dd;  // offsets inside a stage
+    int y, tv, xn, adj, accT, accL, total;                  // offsets from the base
+};
+__host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E) {
+    SmemPlan s;
+    int o = 0;
+    s.s_dcon = o;
+    o += 8 * tps;
+    s.s_meta = o;
+    o += meta_off(tps, TPATH, TCOM).bytes;
+    s.s_xk = o;
+    o += 8 * (TPATH + 2);
+    s.s_xo = o;
+    o += 8 * (TPATH + 2);
+    s.s_dn = o;
+    o += 8 * (TPATH + 2);
+    s.s_D = o;
+    o += 8 * (TCOM + 2);
+    s.s_dd = o;
+    o += 8 * (TCOM + 2);
+    s.stage = r16(o);
+    o = 2 * s.stage;
+    s.y = o;
+    o += 8 * tps;
+    s.tv = o;
+    o += 8 * tps;
+    s.xn = o;
+    o += 8 * TPATH;
+    s.adj = o;
+    o += r16(8 * E);
+    s.accT = o;
+    o += r16(8 * E);
+    s.accL = o;
+    o += r16(8 * E);
+    s.total = o;
+    return s;
+}
+
 struct TileLayout {
-    int32_t ntiles = 0;
-    int64_t nslots = 0;
+    int32_t ntiles = 0, tps = TPS_MIN;
+    int64_t nslots = 0, meta_bytes = 0;
     DevBuf<TileDesc> desc;      // per tile
-    DevBuf<uint16_t> slot_eid;  // [nslots] edge id per slot (sorted within a tile)
-    DevBuf<uint16_t> pos;       // [nslots] slot of the tile's l-th pair (path-major), at sb + l
-    DevBuf<uint8_t> spath;      // [nslots] tile-local path index of each slot
-    DevBuf<uint16_t> pair_slot; // [NP] tile-local slot of pair t (export only)
+    DevBuf<uint8_t> meta;       // per-tile metadata blocks
     DevBuf<int32_t> pair_tile;  // [NP] tile of pair t (export only)
     std::vector<TileDesc> h_desc;
-    int32_t max_pairs = 0, max_paths = 0;
+    int64_t bytes_per_pass = 0;  // compulsory HBM bytes of one M pass over the tiles
 };
 
 struct Ctrl {
@@ -78,10 +158,10 @@ struct Ctrl {
 
 struct Params {
     InstView I;
-    int32_t ntiles, G, nslices, pad;
+    int32_t ntiles, G, nslices, tps;
     const TileDesc *desc;
-    const uint16_t *slot_eid, *pos;
-    const uint8_t *spath;
+    const uint8_t *meta;
+    const double *D;  // [C + 2] demand (padded copy for 16-byte bulk copies)
     double *dcon[2], *dn[2], *dd[2], *x[2];
     double *dc, *adj;
     const double *ne;       // [E] paths per edge (global across ranks when sharded)
@@ -99,70 +179,38 @@ struct Params {
     int32_t adapt;
 };
 
-// ------------------------------------------------------------------ shared memory
+// ------------------------------------------------------------------ TMA / mbarrier
 
-struct Stage {
-    TileDesc d;
-    double dcon[TP];  // duals_k dual_consensus; reused for the T values
-    double xk[TPATH], xo[TPATH], dn[TPATH];
-    double D[TCOM], dd[TCOM];
-    uint16_t eid[TP], pos[TP];
-    uint8_t spath[TP];        // tile-local path of each slot
-    int32_t poff[TPATH + 4];  // raw pair_ptr[p0 .. p1]
-    int32_t cpp[TCOM + 4];    // raw com_path_ptr[c0 .. c1]
-};
+__device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-struct Work {
-    double y[TP];
-    double pK[TPATH], pw[TPATH], xn[TPATH];
-    double ct[TCOM];
-    uint8_t pcom[TPATH];
-    double wv1[NT / 32], wv2[NT / 32];
-    int32_t wflag[NT / 32];
-    double red[NT / 32];
-};
-
-struct Smem {
-    Stage *st;
-    Work *w;
-    double *accT, *accL, *adj;
-};
-
-__device__ __forceinline__ Smem carve(char *base, int E) {
-    Smem s;
-    char *p = base;
-    s.st = (Stage *)p;
-    p += sizeof(Stage);
-    s.w = (Work *)p;
-    p += sizeof(Work);
-    s.accT = (double *)p;
-    p += sizeof(double) * E;
-    s.accL = (double *)p;
-    p += sizeof(double) * E;
-    s.adj = (double *)p;
-    return s;
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(count) : "memory");
 }
-
-static size_t smem_bytes(int E) { return sizeof(Stage) + sizeof(Work) + 3 * sizeof(double) * (size_t)E; }
-
-// ------------------------------------------------------------------ cp.async staging
-
-__device__ __forceinline__ void cp16(void *smem, const void *g) {
-    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g));
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void cp8(void *smem, const void *g) {
-    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(g));
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE;\n"
+        "bra WAIT;\n"
+        "DONE:\n"
+        "}\n" ::"r"(su32(b)),
+        "r"(parity)
+        : "memory");
 }
-__device__ __forceinline__ void cp4(void *smem, const void *g) {
-    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(g));
+// 1-D bulk copy global -> shared, completing `bytes` on the mbarrier.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     su32(dst)),
+                 "l"(src), "r"(bytes), "r"(su32(b))
+                 : "memory");
 }
-__device__ __forceinline__ void cp_commit_wait_all() {
-    asm volatile("cp.async.commit_group;\n" ::);
-    asm volatile("cp.async.wait_group 0;\n" ::);
-}
+// order this thread's generic-proxy accesses before later async-proxy (TMA) ones
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;\n" ::: "memory"); }
 
 enum { MODE_M = 0, MODE_RB = 1, MODE_A1 = 2 };
 
@@ -174,149 +222,73 @@ struct PassIO {
     int par;  // residual parity of the A-part iteration
 };
 
-// Issue the copies of one tile's inputs, then wait (other CTAs on the SM overlap).
+// Stage pointers of one buffer.
+struct StageView {
+    const double *dcon;
+    const uint8_t *meta;
+    const double *xk, *xo, *dn, *D, *dd;  // already shifted to the tile's first path / commodity
+};
+
+__device__ __forceinline__ StageView stage_view(char *base, const SmemPlan &sp, int b, const TileDesc &d) {
+    char *s = base + b * sp.stage;
+    StageView v;
+    v.dcon = (double *)(s + sp.s_dcon);
+    v.meta = (const uint8_t *)(s + sp.s_meta);
+    v.xk = (const double *)(s + sp.s_xk) + (d.p0 & 1);
+    v.xo = (const double *)(s + sp.s_xo) + (d.p0 & 1);
+    v.dn = (const double *)(s + sp.s_dn) + (d.p0 & 1);
+    v.D = (const double *)(s + sp.s_D) + (d.c0 & 1);
+    v.dd = (const double *)(s + sp.s_dd) + (d.c0 & 1);
+    return v;
+}
+
+// One elected thread: bulk copies of a tile's inputs into stage b.
 template <int MODE>
-__device__ __forceinline__ void stage_tile(const Params &P, const TileDesc &d, Stage &st, const PassIO &io) {
-    const int tid = threadIdx.x;
-    const int np = d.np, npath = d.p1 - d.p0, nc = d.c1 - d.c0;
-    for (int i = tid; i < (np + 1) / 2; i += NT) cp16(&st.dcon[2 * i], &io.dcon_in[d.sb + 2 * i]);
-    for (int i = tid; i < (np + 7) / 8; i += NT) {
-        cp16(&st.eid[8 * i], &P.slot_eid[d.sb + 8 * i]);
-        cp16(&st.pos[8 * i], &P.pos[d.sb + 8 * i]);
-    }
-    for (int i = tid; i < (np + 15) / 16; i += NT) cp16(&st.spath[16 * i], &P.spath[d.sb + 16 * i]);
-    for (int i = tid; i < npath; i += NT) {
-        cp8(&st.xk[i], &io.xk[d.p0 + i]);
-        if (MODE == MODE_RB) cp8(&st.xo[i], &io.xo[d.p0 + i]);
-        cp8(&st.dn[i], &io.dn_in[d.p0 + i]);
-    }
-    for (int i = tid; i <= npath; i += NT) cp4(&st.poff[i], &P.I.pair_ptr[d.p0 + i]);
-    for (int i = tid; i <= nc; i += NT) cp4(&st.cpp[i], &P.I.com_path_ptr[d.c0 + i]);
-    for (int i = tid; i < nc; i += NT) {
-        cp8(&st.D[i], &P.I.demand[d.c0 + i]);
-        cp8(&st.dd[i], &io.dd_in[d.c0 + i]);
-    }
-    cp_commit_wait_all();
+__device__ __forceinline__ void issue_tile(const Params &P, const PassIO &io, const TileDesc &d, char *base,
+                                           const SmemPlan &sp, int b, uint64_t *bar) {
+    char *s = base + b * sp.stage;
+    const int npath = d.p1 - d.p0, nc = d.c1 - d.c0;
+    const MetaOff m = meta_off(d.np, npath, nc);
+    const int pa = d.p0 & ~1, npa = even(d.p1 - pa);
+    const int ca = d.c0 & ~1, nca = even(d.c1 - ca);
+    const uint32_t b_dcon = 8u * even(d.np), b_p = 8u * npa, b_c = 8u * nca;
+    uint32_t total = b_dcon + (uint32_t)m.bytes + 2 * b_p + 2 * b_c;
+    if (MODE == MODE_RB) total += b_p;
+    mbar_expect_tx(bar, total);
+    bulk_g2s(s + sp.s_dcon, io.dcon_in + d.sb, b_dcon, bar);
+    bulk_g2s(s + sp.s_meta, P.meta + (size_t)d.mb16 * 16, (uint32_t)m.bytes, bar);
+    bulk_g2s(s + sp.s_xk, io.xk + pa, b_p, bar);
+    bulk_g2s(s + sp.s_dn, io.dn_in + pa, b_p, bar);
+    if (MODE == MODE_RB) bulk_g2s(s + sp.s_xo, io.xo + pa, b_p, bar);
+    bulk_g2s(s + sp.s_D, P.D + ca, b_c, bar);
+    bulk_g2s(s + sp.s_dd, io.dd_in + ca, b_c, bar);
 }
 
 // Block reduction of one double in a fixed tree order (deterministic).
 __device__ double block_sum(double v, double *red) {
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(FULL, v, o);
     int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     __syncthreads();
     if (l == 0) red[w] = v;
     __syncthreads();
     double r = 0.0;
     if (w == 0) {
-        r = l < NT / 32 ? red[l] : 0.0;
-        for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
+        r = l < NW ? red[l] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(FULL, r, o);
     }
     __syncthreads();
     return r;  // valid in thread 0
 }
 
-// Segmented-sum operator on (head flag, value pair): (f1,a1) (+) (f2,a2).
-__device__ __forceinline__ void seg_op2(int f1, double a1, double b1, int &f2, double &a2, double &b2) {
-    if (!f2) {
-        a2 = a1 + a2;
-        b2 = b1 + b2;
-    }
-    f2 |= f1;
-}
-
-// Block-wide segmented inclusive scan over the tile's slots (ITEMS consecutive
-// slots per thread) keyed by edge id, for two value streams at once.  The value
-// at the last slot of each edge run is that run's total; the thread owning it
-// adds it to acc[eid] (one run per edge per tile: no write conflicts).  Fixed
-// operator tree, so the result is deterministic.
-template <bool TWO>
-__device__ void seg_reduce_runs(const double *v1, const double *v2, const uint16_t *eid, int np, double *acc1,
-                                double *acc2, Work &W) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int base = ITEMS * tid;
-    int key[ITEMS + 1];
-    double a[ITEMS], b[ITEMS];
-    int h[ITEMS];
+// Inclusive sum over the lane segment [first, lane] (Hillis-Steele, fixed tree),
+// then broadcast the segment total from lane `last`.
+__device__ __forceinline__ double seg_total(double v, int lane, int first, int last) {
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        int sl = base + i;
-        bool ok = sl < np;
-        key[i] = ok ? (int)eid[sl] : -1 - i;
-        a[i] = ok ? v1[sl] : 0.0;
-        b[i] = (TWO && ok) ? v2[sl] : 0.0;
-    }
-    key[ITEMS] = base + ITEMS < np ? (int)eid[base + ITEMS] : -100;
-    const int kprev = (base > 0 && base - 1 < np) ? (int)eid[base - 1] : -200;
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) h[i] = (i == 0 ? key[0] != kprev : key[i] != key[i - 1]);
-    int f = h[0];
-    double x = a[0], z = b[0];
-#pragma unroll
-    for (int i = 1; i < ITEMS; ++i) {
-        int fi = h[i];
-        double xi = a[i], zi = b[i];
-        seg_op2(f, x, z, fi, xi, zi);
-        f = fi;
-        x = xi;
-        z = zi;
-    }
     for (int o = 1; o < 32; o <<= 1) {
-        int fo = __shfl_up_sync(0xffffffffu, f, o);
-        double xo = __shfl_up_sync(0xffffffffu, x, o);
-        double zo = TWO ? __shfl_up_sync(0xffffffffu, z, o) : 0.0;
-        if (lane >= o) seg_op2(fo, xo, zo, f, x, z);
+        double t = __shfl_up_sync(FULL, v, o);
+        if (lane - o >= first) v += t;
     }
-    if (lane == 31) {
-        W.wflag[warp] = f;
-        W.wv1[warp] = x;
-        W.wv2[warp] = z;
-    }
-    int fe = __shfl_up_sync(0xffffffffu, f, 1);
-    double xe = __shfl_up_sync(0xffffffffu, x, 1);
-    double ze = TWO ? __shfl_up_sync(0xffffffffu, z, 1) : 0.0;
-    if (lane == 0) {
-        fe = 0;
-        xe = 0.0;
-        ze = 0.0;
-    }
-    __syncthreads();
-    if (warp == 0) {
-        const bool in = lane < NT / 32;
-        int wf = in ? W.wflag[lane] : 0;
-        double wx = in ? W.wv1[lane] : 0.0, wz = in ? W.wv2[lane] : 0.0;
-        for (int o = 1; o < NT / 32; o <<= 1) {
-            int fo = __shfl_up_sync(0xffffffffu, wf, o);
-            double xo = __shfl_up_sync(0xffffffffu, wx, o);
-            double zo = __shfl_up_sync(0xffffffffu, wz, o);
-            if (lane >= o) seg_op2(fo, xo, zo, wf, wx, wz);
-        }
-        int pf_ = __shfl_up_sync(0xffffffffu, wf, 1);
-        double px = __shfl_up_sync(0xffffffffu, wx, 1);
-        double pz = __shfl_up_sync(0xffffffffu, wz, 1);
-        if (in) {
-            W.wflag[lane] = lane ? pf_ : 0;
-            W.wv1[lane] = lane ? px : 0.0;
-            W.wv2[lane] = lane ? pz : 0.0;
-        }
-    }
-    __syncthreads();
-    int fp = fe;
-    double xr = xe, zr = ze;
-    seg_op2(W.wflag[warp], W.wv1[warp], W.wv2[warp], fp, xr, zr);  // exclusive prefix of this thread
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        int fi = h[i];
-        double xi = a[i], zi = b[i];
-        seg_op2(fp, xr, zr, fi, xi, zi);
-        fp = fi;
-        xr = xi;
-        zr = zi;
-        if (base + i < np && key[i + 1] != key[i]) {
-            acc1[key[i]] += xi;
-            if (TWO) acc2[key[i]] += zi;
-        }
-    }
-    __syncthreads();
+    return __shfl_sync(FULL, v, last);
 }
 
 // ------------------------------------------------------------------ controller
@@ -401,8 +373,8 @@ __device__ void controller_eval(const Params &P, Ctrl &c) {
         int ngroups = (P.I.E + RGRP - 1) / RGRP;
         for (int g = threadIdx.x; g < ngroups; g += 32) dcs += __ldcg(&P.res_dc[g]);
         for (int j = 0; j < 4; ++j)
-            for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_down_sync(0xffffffffu, acc[j], o);
-        for (int o = 16; o > 0; o >>= 1) dcs += __shfl_down_sync(0xffffffffu, dcs, o);
+            for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_down_sync(FULL, acc[j], o);
+        for (int o = 16; o > 0; o >>= 1) dcs += __shfl_down_sync(FULL, dcs, o);
         if (threadIdx.x == 0)
             controller_step(P, c, sqrt(acc[0]), sqrt(((acc[1] + dcs) + acc[2]) + acc[3]), __ldcg(&P.err[0]),
                             __ldcg(&P.err[1]));
@@ -422,7 +394,7 @@ __device__ __noinline__ void edge_phase(const Params &P, double f) {
     int ngroups = (I.E + RGRP - 1) / RGRP;
     int nitems = ngroups * P.nslices;
     int per = (P.G + P.nslices - 1) / P.nslices;
-    for (int item = g * (NT / 32) + warp; item < nitems; item += P.G * (NT / 32)) {
+    for (int item = g * NW + warp; item < nitems; item += P.G * NW) {
         int grp = item / P.nslices, sl = item % P.nslices;
         int e = grp * RGRP + lane;
         int g0 = sl * per, g1 = g0 + per < P.G ? g0 + per : P.G;
@@ -439,7 +411,7 @@ __device__ __noinline__ void edge_phase(const Params &P, double f) {
         __syncwarp();
         int ticket = 0;
         if (lane == 0) ticket = atomicAdd(&P.grp_count[grp], 1);
-        ticket = __shfl_sync(0xffffffffu, ticket, 0);
+        ticket = __shfl_sync(FULL, ticket, 0);
         if (ticket == P.nslices - 1) {
             __threadfence();
             double T = 0.0, L = 0.0, rdc = 0.0;
@@ -458,7 +430,7 @@ __device__ __noinline__ void edge_phase(const Params &P, double f) {
                 double d = dnew - dold;
                 rdc = d * d;
             }
-            for (int o = 16; o > 0; o >>= 1) rdc += __shfl_down_sync(0xffffffffu, rdc, o);
+            for (int o = 16; o > 0; o >>= 1) rdc += __shfl_down_sync(FULL, rdc, o);
             if (lane == 0) {
                 P.res_dc[grp] = rdc;
                 P.grp_count[grp] = 0;
@@ -469,129 +441,247 @@ __device__ __noinline__ void edge_phase(const Params &P, double f) {
 
 // ------------------------------------------------------------------ tile compute
 
+struct Tail {
+    double T, L;
+    int32_t open;  // the warp's whole range continues a run begun in an earlier warp
+    int32_t pad;
+};
+
+struct Acc {
+    double *adj, *accT, *accL, *y, *tv, *xn;
+};
+
 // MODE_M : B(k+1) [y, K/w, roots, x_{k+1}] fused with A(k+2) [duals_{k+2}, T/L]
 // MODE_RB: A(k+2) only, recomputing y_{k+1} from x_k, dcon_{k+1}, adj_{k+1}
 // MODE_A1: A(1) with y_0 = x_0[pair_path] (controller.py:118)
-// Every phase is parallel over slots or paths; only the sum-root runs one thread
-// per commodity.
 template <int MODE>
-__device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, const PassIO &io, Smem &S, double &r_x,
+__device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, const PassIO &io, const TileDesc &d,
+                                             const StageView &st, const Acc &A, Tail *tails, double &r_x,
                                              double &r_dd, double &r_dcon, double &r_dn) {
-    Stage &st = *S.st;
-    Work &W = *S.w;
-    const TileDesc &d = st.d;
-    const int tid = threadIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int np = d.np, npath = d.p1 - d.p0, nc = d.c1 - d.c0;
+    const MetaOff m = meta_off(np, npath, nc);
+    const uint16_t *eid = (const uint16_t *)(st.meta + m.eid);
+    const uint16_t *perm = (const uint16_t *)(st.meta + m.perm);
+    const uint8_t *spath = st.meta + m.spath;
+    const uint16_t *poff = (const uint16_t *)(st.meta + m.poff);
+    const uint8_t *pcom = st.meta + m.pcom;
+    const uint16_t *cpp = (const uint16_t *)(st.meta + m.cpp);
+    const uint16_t *gpath = (const uint16_t *)(st.meta + m.gpath);
+    const double *dcon = st.dcon;
+    double *ys = A.y;
     const double f = io.f;
-    // (1) slots: y (kernels.py:98-100) and y - dcon (kernels.py:114); path -> commodity map
-    for (int sl = tid; sl < np; sl += NT) {
-        const int i = st.spath[sl];
-        const double dk = st.dcon[sl];
+
+    // ---- this warp's commodity group
+    const int gp0 = gpath[w], gp1 = gpath[w + 1];
+    const int l0 = poff[gp0], l1 = poff[gp1];
+    // (1) pairs: y (kernels.py:98-100)
+    for (int l = l0 + lane; l < l1; l += 32) {
+        const int i = spath[l];
         double y;
         if (MODE == MODE_A1)
             y = st.xk[i];
         else
-            y = max0((MODE == MODE_RB ? st.xo[i] : st.xk[i]) + dk - S.adj[st.eid[sl]]);
-        W.y[sl] = y;
+            y = max0((MODE == MODE_RB ? st.xo[i] : st.xk[i]) + dcon[l] - A.adj[eid[l]]);
+        ys[l] = y;
     }
-    if (MODE == MODE_M)
-        for (int j = tid; j < nc; j += NT)
-            for (int i = st.cpp[j] - d.p0; i < st.cpp[j + 1] - d.p0; ++i) W.pcom[i] = (uint8_t)j;
-    __syncthreads();
-    if (MODE == MODE_M) {
-        // (2) paths: K_p in path order, frozen non-negativity activity (kernels.py:110-119)
-        for (int i = tid; i < npath; i += NT) {
-            const int lo = st.poff[i] - d.t0, hi = st.poff[i + 1] - d.t0;
-            double acc = 0.0;
-            for (int l = lo; l < hi; ++l) {
-                const int sl = st.pos[l];
-                acc += W.y[sl] - st.dcon[sl];
-            }
-            const double x = st.xk[i], dn = st.dn[i];
-            const double h = (double)(hi - lo);
-            if (x < dn) {
-                W.pK[i] = acc + dn;
-                W.pw[i] = 1.0 / (h + 1.0);
-            } else {
-                W.pK[i] = acc;
-                W.pw[i] = 1.0 / h;
-            }
+    __syncwarp();
+    // (2) paths (lane = path) and commodities (lane segments)
+    {
+        const int p = gp0 + lane;
+        const bool valid = p < gp1;
+        int j = 0, first = lane, last = lane;
+        if (valid) {
+            j = pcom[p];
+            first = cpp[j] - gp0;
+            last = cpp[j + 1] - 1 - gp0;
         }
-        __syncthreads();
-        // (3) commodities: W, Q (kernels.py:122-131), sum root (kernels.py:176-189), rate term (:289-294)
-        for (int j = tid; j < nc; j += NT) {
-            const int lo = st.cpp[j] - d.p0, hi = st.cpp[j + 1] - d.p0;
-            const int cc = d.c0 + j;
-            double ws = 0.0, qw = 0.0;
-            for (int i = lo; i < hi; ++i) {
-                ws += W.pw[i];
-                qw += W.pw[i] * W.pK[i];
-            }
-            double ct = NAN;
-            if (!(isfinite(ws) && isfinite(qw))) {
-                atomicMin(&P.err[0], cc);
-            } else {
-                const double D = st.D[j], ddk = st.dd[j];
-                const double Sc = commodity_root(ws, qw, D - ddk, c.beta, c.alpha);
-                if (!isfinite(Sc)) atomicMin(&P.err[1], cc);
-                if (P.root_sums) P.root_sums[cc] = Sc;
-                ct = commodity_term(Sc, D, ddk, c.beta, c.alpha);
-            }
-            W.ct[j] = ct;
-        }
-        __syncthreads();
-    }
-    // (4) paths: new rate (kernels.py:195) and dual_nonneg (kernels.py:215)
-    for (int i = tid; i < npath; i += NT) {
-        double xv;
+        const bool head = valid && lane == first;
+        const int cc = d.c0 + j;
+        const double xk = valid ? st.xk[p] : 0.0;
+        double xv = xk;
         if (MODE == MODE_M) {
-            xv = W.pw[i] * (W.pK[i] + W.ct[W.pcom[i]]);
-            io.x_out[d.p0 + i] = xv;
-            const double df = xv - st.xk[i];
-            r_x += df * df;
-        } else {
-            xv = st.xk[i];
+            double K = 0.0, wgt = 0.0;
+            if (valid) {
+                const int lo = poff[p], hi = poff[p + 1];
+                for (int l = lo; l < hi; ++l) K += ys[l] - dcon[l];
+                const double dnv = st.dn[p];
+                const double h = (double)(hi - lo);
+                if (xk < dnv) {  // frozen non-negativity activity (kernels.py:114-119)
+                    K += dnv;
+                    wgt = 1.0 / (h + 1.0);
+                } else {
+                    wgt = 1.0 / h;
+                }
+            }
+            const double Wc = seg_total(wgt, lane, first, last);
+            const double Qc = seg_total(wgt * K, lane, first, last);
+            double ct = NAN;
+            if (valid) {
+                if (!(isfinite(Wc) && isfinite(Qc))) {
+                    if (head) atomicMin(&P.err[0], cc);
+                } else {
+                    const double D = st.D[j], ddk = st.dd[j];
+                    const double Sc = commodity_root(Wc, Qc, D - ddk, c.beta, c.alpha);
+                    if (head) {
+                        if (!isfinite(Sc)) atomicMin(&P.err[1], cc);
+                        if (P.root_sums) P.root_sums[cc] = Sc;
+                    }
+                    ct = commodity_term(Sc, D, ddk, c.beta, c.alpha);
+                }
+                xv = wgt * (K + ct);
+                io.x_out[d.p0 + p] = xv;
+                const double df = xv - xk;
+                r_x += df * df;
+            }
         }
-        W.xn[i] = xv;
-        const double o = st.dn[i] * f;
-        const double n = npmax0(o - xv);
-        io.dn_out[d.p0 + i] = n;
-        const double dg = n - o;
-        r_dn += dg * dg;
+        if (valid) {
+            A.xn[p] = xv;
+            const double o = st.dn[p] * f;
+            const double n = npmax0(o - xv);
+            io.dn_out[d.p0 + p] = n;
+            const double dg = n - o;
+            r_dn += dg * dg;
+        }
+        // S_c (model.py:297-302) and dual_demand (kernels.py:211)
+        const double Sx = seg_total(valid ? xv : 0.0, lane, first, last);
+        if (head) {
+            const double dold = st.dd[j] * f;
+            const double dnew = npmax0(dold + (Sx - st.D[j]));
+            io.dd_out[cc] = dnew;
+            const double df = dnew - dold;
+            r_dd += df * df;
+        }
     }
-    __syncthreads();
-    // (5) slots: dual_consensus (kernels.py:72), T value x + dcon' (kernels.py:91);
-    //     commodities: S_c in model.py:297-302 order and dual_demand (kernels.py:211)
-    for (int sl = tid; sl < np; sl += NT) {
-        const double dks = st.dcon[sl] * f;
-        const double xn = W.xn[st.spath[sl]];
-        const double dnew = max0(dks + xn - W.y[sl]);
-        io.dcon_out[d.sb + sl] = dnew;
+    __syncwarp();
+    // (3) pairs: dual_consensus (kernels.py:72), T value x + dcon' (kernels.py:91)
+    for (int l = l0 + lane; l < l1; l += 32) {
+        const double dks = dcon[l] * f;
+        const double xn = A.xn[spath[l]];
+        const double dnew = max0(dks + xn - ys[l]);
+        io.dcon_out[d.sb + l] = dnew;
         const double df = dnew - dks;
         r_dcon += df * df;
-        st.dcon[sl] = xn + dnew;
-    }
-    for (int j = tid; j < nc; j += NT) {
-        const int lo = st.cpp[j] - d.p0, hi = st.cpp[j + 1] - d.p0;
-        double total = 0.0;
-        for (int i = lo; i < hi;) {
-            const int k2 = i + 32 < hi ? i + 32 : hi;
-            double part = 0.0;
-            for (int t = i; t < k2; ++t) part += W.xn[t];
-            total += part;
-            i = k2;
-        }
-        const double dold = st.dd[j] * f;
-        const double dnew = npmax0(dold + (total - st.D[j]));
-        io.dd_out[d.c0 + j] = dnew;
-        const double df = dnew - dold;
-        r_dd += df * df;
+        A.tv[l] = xn + dnew;
     }
     __syncthreads();
-    if (MODE == MODE_RB)
-        seg_reduce_runs<false>(st.dcon, nullptr, st.eid, np, S.accT, nullptr, W);
-    else
-        seg_reduce_runs<true>(st.dcon, W.y, st.eid, np, S.accT, S.accL, W);
+
+    // (4) per-edge T and L of the tile over the edge-sorted permutation.  Warp w
+    // owns sorted slots [s0, s1), lane `lane` the consecutive items [a, b): a
+    // sequential segmented sum per lane, one warp scan of the lane aggregates,
+    // then a second sequential pass that adds each run total to the CTA
+    // accumulators (a run never repeats an edge within a tile: no conflicts).
+    // A run begun in an earlier warp is completed after the barrier from the
+    // warps' tails.
+    const int q = ((np + NW - 1) / NW + 31) & ~31;
+    const int s0 = min(w * q, np), s1 = min(s0 + q, np);
+    const int IT = (s1 - s0 + 31) >> 5;
+    const int a = min(s0 + lane * IT, s1), b = min(a + IT, s1);
+    const int kbefore = a > 0 ? (int)eid[perm[a - 1]] : -1;
+    const double *tv = A.tv;
+    // one sequential pass per lane: runs that start and end inside the lane are
+    // added at once; the lane's prefix (continuing a run begun before item a)
+    // and its last run are settled after the warp scan.
+    int pk = kbefore;
+    bool pre = true;  // still in the prefix
+    bool pn = false;  // the prefix is non-empty
+    double cT = 0.0, cL = 0.0, pT = 0.0, pL = 0.0;
+    int pkey = -1;
+    for (int s = a; s < b; ++s) {
+        const int pl = perm[s];
+        const int k = eid[pl];
+        if (k != pk) {  // run head at s
+            if (pre) {
+                pre = false;
+                pn = s > a;
+                pT = cT;
+                pL = cL;
+                pkey = pk;
+            } else {
+                A.accT[pk] += cT;
+                if (MODE != MODE_RB) A.accL[pk] += cL;
+            }
+            cT = 0.0;
+            cL = 0.0;
+        }
+        cT += tv[pl];
+        if (MODE != MODE_RB) cL += ys[pl];
+        pk = k;
+    }
+    const bool hh = !pre;  // the lane holds a run head
+    if (pre) {
+        pn = a < b;
+        pT = cT;
+        pL = cL;
+        pkey = pk;
+    }
+    // warp scan of (head, open-run aggregate): carry into each lane = the sum of
+    // the run that is open at the lane's first item, over the earlier lanes
+    const unsigned hm = __ballot_sync(FULL, hh);
+    double gT = hh ? cT : pT, gL = hh ? cL : pL;
+    {
+        const unsigned upto = hm & (0xffffffffu >> (31 - lane));
+        const int f = upto ? 31 - __clz(upto) : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_up_sync(FULL, gT, o);
+            const double u = (MODE != MODE_RB) ? __shfl_up_sync(FULL, gL, o) : 0.0;
+            if (lane - o >= f) {
+                gT += t;
+                gL += u;
+            }
+        }
+    }
+    double CT = __shfl_up_sync(FULL, gT, 1), CL = (MODE != MODE_RB) ? __shfl_up_sync(FULL, gL, 1) : 0.0;
+    if (lane == 0) {
+        CT = 0.0;
+        CL = 0.0;
+    }
+    const bool copen = (hm & ((1u << lane) - 1u)) == 0u;  // the carried run began before this warp's range
+    bool fix = false;
+    int fkey = 0;
+    double fT = 0.0, fL = 0.0;
+    if (a < b) {
+        const int knext = b < np ? (int)eid[perm[b]] : -3;
+        // prefix run: items [a, first head) continue the carried run
+        if (pn) {
+            const double tT = CT + pT, tL = CL + pL;
+            const bool ends = hh || knext != pkey;  // with a head in the lane the prefix ends before it
+            if (ends) {
+                if (copen) {
+                    fix = true;
+                    fkey = pkey;
+                    fT = tT;
+                    fL = tL;
+                } else {
+                    A.accT[pkey] += tT;
+                    if (MODE != MODE_RB) A.accL[pkey] += tL;
+                }
+            } else if (b == s1) {
+                tails[w] = Tail{tT, tL, copen ? 1 : 0, 0};
+            }
+        }
+        // last run of a lane with a head: started inside the lane
+        if (hh) {
+            if (knext != pk) {
+                A.accT[pk] += cT;
+                if (MODE != MODE_RB) A.accL[pk] += cL;
+            } else if (b == s1) {
+                tails[w] = Tail{cT, cL, 0, 0};
+            }
+        }
+    }
+    __syncthreads();
+    if (fix) {  // the warp's first run began in an earlier warp: add the carried tails
+        double cT = 0.0, cL = 0.0;
+        for (int ww = w - 1; ww >= 0; --ww) {
+            cT += tails[ww].T;
+            cL += tails[ww].L;
+            if (!tails[ww].open) break;
+        }
+        A.accT[fkey] += cT + fT;
+        if (MODE != MODE_RB) A.accL[fkey] += cL + fL;
+    }
 }
 
 template <int MODE>
@@ -637,61 +727,108 @@ __device__ PassIO pass_io(const Params &P, const Ctrl &c) {
     return io;
 }
 
-// One pass over this CTA's tiles.  Odd iterations walk the tiles in reverse so a
-// pass first re-reads what the previous pass wrote last (L2 reuse).
+// Per-CTA persistent shared state.
+struct CtaShared {
+    uint64_t bar[2];
+    TileDesc sd[2];
+    PassIO io;
+    Tail tails[NW];
+    double red[NW];
+};
+
+// One pass over this CTA's tiles (static assignment tile = g + k*G, so every
+// tile's state is only ever touched by one CTA).  Odd iterations walk the tiles
+// in reverse so a pass first re-reads what the previous pass wrote last (L2
+// reuse).  `seq` counts the tiles this CTA has staged (stage = seq & 1, mbarrier
+// parity = (seq >> 1) & 1), persistent across passes.
 template <int MODE>
-__device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, Smem &S) {
-    const int g = blockIdx.x;
+__device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *base, CtaShared &cs, uint32_t &seq) {
+    const int g = blockIdx.x, tid = threadIdx.x;
     const int E = P.I.E;
-    __shared__ PassIO io;  // kept in shared memory: frees ~20 registers per thread
-    if (threadIdx.x == 0) io = pass_io<MODE>(P, c);
-    for (int e = threadIdx.x; e < E; e += NT) {
-        S.accT[e] = 0.0;
-        S.accL[e] = 0.0;
-        S.adj[e] = MODE == MODE_A1 ? 0.0 : __ldcg(&P.adj[e]);
-    }
+    const SmemPlan sp = smem_plan(P.tps, E);
+    Acc A;
+    A.adj = (double *)(base + sp.adj);
+    A.accT = (double *)(base + sp.accT);
+    A.accL = (double *)(base + sp.accL);
+    A.y = (double *)(base + sp.y);
+    A.tv = (double *)(base + sp.tv);
+    A.xn = (double *)(base + sp.xn);
     const int my = g < P.ntiles ? (P.ntiles - 1 - g) / P.G + 1 : 0;
     const bool rev = (c.iteration & 1) != 0;
-    double r_x = 0.0, r_dd = 0.0, r_dcon = 0.0, r_dn = 0.0;
-    for (int k = 0; k < my; ++k) {
-        const int tile = g + (rev ? my - 1 - k : k) * P.G;
-        const TileDesc d = P.desc[tile];
-        __syncthreads();  // previous tile finished with the stage buffer
-        if (threadIdx.x == 0) S.st->d = d;
-        stage_tile<MODE>(P, d, *S.st, io);
-        __syncthreads();
-        tile_compute<MODE>(P, c, io, S, r_x, r_dd, r_dcon, r_dn);
+    auto tile_of = [&](int k) { return g + (rev ? my - 1 - k : k) * P.G; };
+    if (tid == 0) {
+        cs.io = pass_io<MODE>(P, c);
+        fence_proxy_async();  // this pass's inputs were written by generic stores after a grid barrier
+        if (my > 0) {
+            const int b = seq & 1;
+            cs.sd[b] = P.desc[tile_of(0)];
+            issue_tile<MODE>(P, cs.io, cs.sd[b], base, sp, b, &cs.bar[b]);
+        }
+    }
+    for (int e = tid; e < E; e += NT) {
+        A.accT[e] = 0.0;
+        A.accL[e] = 0.0;
+        A.adj[e] = MODE == MODE_A1 ? 0.0 : __ldcg(&P.adj[e]);
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < E; e += NT) {
-        P.partT[(size_t)g * E + e] = S.accT[e];
-        if (MODE != MODE_RB) P.partL[(size_t)g * E + e] = S.accL[e];
+    const PassIO &io = cs.io;
+    double r_x = 0.0, r_dd = 0.0, r_dcon = 0.0, r_dn = 0.0;
+    for (int k = 0; k < my; ++k, ++seq) {
+        const int b = seq & 1;
+        if (tid == 0 && k + 1 < my) {  // prefetch the next tile into the other stage
+            const int nb = b ^ 1;
+            cs.sd[nb] = P.desc[tile_of(k + 1)];
+            issue_tile<MODE>(P, io, cs.sd[nb], base, sp, nb, &cs.bar[nb]);
+        }
+        mbar_wait(&cs.bar[b], (seq >> 1) & 1);
+        const TileDesc d = cs.sd[b];
+        const StageView st = stage_view(base, sp, b, d);
+        tile_compute<MODE>(P, c, io, d, st, A, cs.tails, r_x, r_dd, r_dcon, r_dn);
+        __syncthreads();  // stage b is only read by generic accesses; free for the TMA of tile k + 2
+    }
+    for (int e = tid; e < E; e += NT) {
+        P.partT[(size_t)g * E + e] = A.accT[e];
+        if (MODE != MODE_RB) P.partL[(size_t)g * E + e] = A.accL[e];
     }
     double *r = P.res + g * 8;
     double t;
     if (MODE == MODE_M) {
-        t = block_sum(r_x, S.w->red);
-        if (threadIdx.x == 0) r[0] = t;
+        t = block_sum(r_x, cs.red);
+        if (tid == 0) r[0] = t;
     }
-    t = block_sum(r_dd, S.w->red);
-    if (threadIdx.x == 0) r[1 + 3 * io.par] = t;
-    t = block_sum(r_dcon, S.w->red);
-    if (threadIdx.x == 0) r[2 + 3 * io.par] = t;
-    t = block_sum(r_dn, S.w->red);
-    if (threadIdx.x == 0) r[3 + 3 * io.par] = t;
+    t = block_sum(r_dd, cs.red);
+    if (tid == 0) r[1 + 3 * io.par] = t;
+    t = block_sum(r_dcon, cs.red);
+    if (tid == 0) r[2 + 3 * io.par] = t;
+    t = block_sum(r_dn, cs.red);
+    if (tid == 0) r[3 + 3 * io.par] = t;
+    // the generic-proxy stores of this pass (dual_consensus, rates, ...) are read
+    // by TMA in the next pass
+    fence_proxy_async();
+}
+
+__device__ __forceinline__ void cta_init(CtaShared &cs) {
+    if (threadIdx.x == 0) {
+        mbar_init(&cs.bar[0], 1);
+        mbar_init(&cs.bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
 }
 
 // ------------------------------------------------------------------ kernels
 
-__global__ void __launch_bounds__(NT, 3) k_fused(const __grid_constant__ Params P) {
-    extern __shared__ __align__(16) char smem_raw[];
+__global__ void __launch_bounds__(NT) k_fused(const __grid_constant__ Params P) {
+    extern __shared__ __align__(128) char smem_raw[];
     __shared__ Ctrl c;
-    Smem S = carve(smem_raw, P.I.E);
+    __shared__ CtaShared cs;
     cg::grid_group grid = cg::this_grid();
+    cta_init(cs);
+    uint32_t seq = 0;
     if (threadIdx.x == 0) c = *P.ctrl;
     __syncthreads();
     if (c.need_a1) {
-        pass_tiles<MODE_A1>(P, c, S);
+        pass_tiles<MODE_A1>(P, c, smem_raw, cs, seq);
         grid.sync();
         if (threadIdx.x == 0) {
             c.need_a1 = 0;
@@ -715,7 +852,7 @@ __global__ void __launch_bounds__(NT, 3) k_fused(const __grid_constant__ Params 
             }
             __syncthreads();
         }
-        pass_tiles<MODE_M>(P, c, S);
+        pass_tiles<MODE_M>(P, c, smem_raw, cs, seq);
         grid.sync();
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -728,7 +865,7 @@ __global__ void __launch_bounds__(NT, 3) k_fused(const __grid_constant__ Params 
         __syncthreads();
         controller_eval(P, c);
         if (!c.stopped && !c.status && c.f != 1.0) {
-            pass_tiles<MODE_RB>(P, c, S);
+            pass_tiles<MODE_RB>(P, c, smem_raw, cs, seq);
             grid.sync();
         }
         __syncthreads();
@@ -750,13 +887,15 @@ __global__ void __launch_bounds__(NT, 3) k_fused(const __grid_constant__ Params 
 // the same branch and issue matching collectives.
 
 template <int MODE>
-__global__ void __launch_bounds__(NT, 3) k_pass(const __grid_constant__ Params P) {
-    extern __shared__ __align__(16) char smem_raw[];
+__global__ void __launch_bounds__(NT) k_pass(const __grid_constant__ Params P) {
+    extern __shared__ __align__(128) char smem_raw[];
     __shared__ Ctrl c;
-    Smem S = carve(smem_raw, P.I.E);
+    __shared__ CtaShared cs;
+    cta_init(cs);
+    uint32_t seq = 0;
     if (threadIdx.x == 0) c = *P.ctrl;
     __syncthreads();
-    pass_tiles<MODE>(P, c, S);
+    pass_tiles<MODE>(P, c, smem_raw, cs, seq);
 }
 
 // CTA partials -> rank totals in a fixed order: tot[0:E] = T, tot[E:2E] = L,
@@ -824,7 +963,7 @@ __global__ void k_edge_dist(const __grid_constant__ Params P) {
         const double d = dnew - dold;
         rdc = d * d;
     }
-    for (int o = 16; o > 0; o >>= 1) rdc += __shfl_down_sync(0xffffffffu, rdc, o);
+    for (int o = 16; o > 0; o >>= 1) rdc += __shfl_down_sync(FULL, rdc, o);
     if (threadIdx.x == 0) P.res_dc[grp] = rdc;
 }
 
@@ -842,16 +981,16 @@ __global__ void k_ctrl_update(Ctrl *ctrl, int op) {
     }
 }
 
-// Export helpers (reference pair order <- slot order), for the state of the last
-// completed iteration k: x_k in x[xc], x_{k-1} in x[xc^1], duals_k in buffer db^1
-// (db holds the speculative duals_{k+1}), adj_k, rescale factor f_k pending.
-__global__ void k_export_pairs(const __grid_constant__ Params P, const int32_t *pair_tile,
-                               const uint16_t *pair_slot, double *y_out, double *dcon_out) {
+// Export helpers (reference pair order), for the state of the last completed
+// iteration k: x_k in x[xc], x_{k-1} in x[xc^1], duals_k in buffer db^1 (db
+// holds the speculative duals_{k+1}), adj_k, rescale factor f_k pending.
+__global__ void k_export_pairs(const __grid_constant__ Params P, const int32_t *pair_tile, double *y_out,
+                               double *dcon_out) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= P.I.NP) return;
     const Ctrl c = *P.ctrl;
     const TileDesc d = P.desc[pair_tile[t]];
-    const int sl = d.sb + pair_slot[t];
+    const int sl = d.sb + (t - d.t0);
     const int p = P.I.pair_path[t];
     if (c.iteration == 0) {
         if (y_out) y_out[t] = P.x[c.xc][p];
@@ -859,7 +998,7 @@ __global__ void k_export_pairs(const __grid_constant__ Params P, const int32_t *
         return;
     }
     const double dk = P.dcon[c.db ^ 1][sl];
-    if (y_out) y_out[t] = max0(P.x[c.xc ^ 1][p] + dk - P.adj[P.slot_eid[sl]]);
+    if (y_out) y_out[t] = max0(P.x[c.xc ^ 1][p] + dk - P.adj[P.I.pair_edge[t]]);
     if (dcon_out) dcon_out[t] = dk * c.f;
 }
 
@@ -870,6 +1009,8 @@ __global__ void k_scaled_copy(const double *a, int64_t n, const Ctrl *ctrl, doub
 
 // ------------------------------------------------------------------ host side
 
+// Pack commodities into groups (<= GPATH paths, one warp) and groups into tiles
+// (<= NW groups, <= tps pairs), then write each tile's metadata block.
 static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStream_t s) {
     const Index &I = *inst->idx;
     std::vector<int32_t> cpp(I.C + 1), pptr(I.P + 1), pedge(I.NP);
@@ -879,71 +1020,117 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
     PF_CUDA(cudaStreamSynchronize(s));
     require(I.E <= 65535, "fast mode supports up to 65535 edges (u16 edge ids)");
     auto L = std::make_shared<TileLayout>();
-    std::vector<TileDesc> tiles;
-    int64_t slot = 0;
-    int32_t c = 0;
-    while (c < I.C) {
-        int32_t c0 = c;
-        int32_t p0 = cpp[c0];
-        int32_t t0 = pptr[p0];
+    int64_t max_com_pairs = 0;
+    for (int64_t c = 0; c < I.C; ++c) {
+        require(cpp[c + 1] - cpp[c] <= GPATH, "fast mode supports at most " + std::to_string(GPATH) +
+                                                  " paths per commodity (commodity " + std::to_string(c) + ")");
+        max_com_pairs = std::max<int64_t>(max_com_pairs, pptr[cpp[c + 1]] - pptr[cpp[c]]);
+    }
+    const int64_t tps = std::max<int64_t>(TPS_MIN, (max_com_pairs + 63) / 64 * 64);
+    require(tps <= 16384, "a commodity has too many demand-path pairs for a fast-mode tile");
+    L->tps = (int32_t)tps;
+    // groups
+    std::vector<int32_t> gstart;  // first commodity of each group
+    {
+        int32_t c = 0;
         while (c < I.C) {
-            int32_t np_ = pptr[cpp[c + 1]] - t0;
-            int32_t npath = cpp[c + 1] - p0;
-            if (c > c0 && (np_ > TP || npath > TPATH || c + 1 - c0 > TCOM)) break;
-            require(np_ <= TP && npath <= TPATH,
-                    "commodity " + std::to_string(c) + " has more pairs/paths than a fast-mode tile holds");
-            ++c;
+            gstart.push_back(c);
+            const int32_t c0 = c;
+            while (c < I.C) {
+                const int64_t npath = cpp[c + 1] - cpp[c0];
+                const int64_t npair = pptr[cpp[c + 1]] - pptr[cpp[c0]];
+                if (c > c0 && (npath > GPATH || npair > tps)) break;
+                ++c;
+            }
         }
-        TileDesc d;
-        d.c0 = c0;
-        d.c1 = c;
-        d.p0 = p0;
-        d.p1 = cpp[c];
-        d.t0 = t0;
-        d.np = pptr[cpp[c]] - t0;
-        d.sb = (int32_t)slot;
-        d.pad = 0;
-        tiles.push_back(d);
-        L->max_pairs = std::max(L->max_pairs, d.np);
-        L->max_paths = std::max(L->max_paths, d.p1 - d.p0);
-        slot += (d.np + SLOT_ALIGN - 1) / SLOT_ALIGN * SLOT_ALIGN;
-        require(slot < INT_MAX, "too many slots");
+        gstart.push_back((int32_t)I.C);
+    }
+    // tiles
+    std::vector<TileDesc> tiles;
+    std::vector<std::array<int32_t, NW + 1>> tgroups;  // group commodity boundaries per tile
+    int64_t slot = 0, mb = 0;
+    {
+        const int64_t ng = (int64_t)gstart.size() - 1;
+        int64_t gi = 0;
+        while (gi < ng) {
+            const int32_t c0 = gstart[gi];
+            int64_t gj = gi;
+            while (gj < ng && gj - gi < NW) {
+                const int64_t npair = pptr[cpp[gstart[gj + 1]]] - pptr[cpp[c0]];
+                if (gj > gi && npair > tps) break;
+                ++gj;
+            }
+            std::array<int32_t, NW + 1> gb;
+            for (int k = 0; k <= NW; ++k) gb[k] = gstart[std::min<int64_t>(gi + k, gj)];
+            const int32_t c1 = gstart[gj];
+            TileDesc d;
+            d.c0 = c0;
+            d.c1 = c1;
+            d.p0 = cpp[c0];
+            d.p1 = cpp[c1];
+            d.t0 = pptr[d.p0];
+            d.np = pptr[d.p1] - d.t0;
+            d.sb = (int32_t)slot;
+            require(mb / 16 < INT_MAX, "fast-mode metadata exceeds 32 GB");
+            d.mb16 = (int32_t)(mb / 16);
+            tiles.push_back(d);
+            tgroups.push_back(gb);
+            slot += (d.np + SLOT_ALIGN - 1) / SLOT_ALIGN * SLOT_ALIGN;
+            mb += meta_off(d.np, d.p1 - d.p0, d.c1 - d.c0).bytes;
+            require(slot < INT_MAX, "too many demand-path pairs for fast mode");
+            gi = gj;
+        }
     }
     L->ntiles = (int32_t)tiles.size();
     L->nslots = slot;
-    std::vector<uint16_t> pair_slot(I.NP), slot_eid(slot ? slot : 1, (uint16_t)0), pos(slot ? slot : 1, (uint16_t)0);
-    std::vector<uint8_t> spath(slot ? slot : 1, (uint8_t)0);
+    L->meta_bytes = mb;
+    std::vector<uint8_t> meta(mb ? mb : 16, 0);
     std::vector<int32_t> pair_tile(I.NP);
 #pragma omp parallel for schedule(dynamic, 16)
     for (int64_t ti = 0; ti < (int64_t)tiles.size(); ++ti) {
         const TileDesc &T = tiles[ti];
-        std::vector<int32_t> ord(T.np);
-        for (int32_t l = 0; l < T.np; ++l) ord[l] = l;
-        std::stable_sort(ord.begin(), ord.end(),
-                         [&](int32_t a, int32_t b) { return pedge[T.t0 + a] < pedge[T.t0 + b]; });
-        std::vector<uint8_t> lpath(T.np);
-        for (int32_t p = T.p0; p < T.p1; ++p)
-            for (int32_t t = pptr[p]; t < pptr[p + 1]; ++t) lpath[t - T.t0] = (uint8_t)(p - T.p0);
-        for (int32_t sl = 0; sl < T.np; ++sl) {
-            int32_t l = ord[sl];
-            pair_slot[T.t0 + l] = (uint16_t)sl;
+        const int np = T.np, npath = T.p1 - T.p0, nc = T.c1 - T.c0;
+        const MetaOff m = meta_off(np, npath, nc);
+        uint8_t *blk = meta.data() + (int64_t)T.mb16 * 16;
+        uint16_t *eid = (uint16_t *)(blk + m.eid);
+        uint16_t *perm = (uint16_t *)(blk + m.perm);
+        uint8_t *spath = blk + m.spath;
+        uint16_t *poff = (uint16_t *)(blk + m.poff);
+        uint8_t *pcom = blk + m.pcom;
+        uint16_t *lcpp = (uint16_t *)(blk + m.cpp);
+        uint16_t *gpath = (uint16_t *)(blk + m.gpath);
+        for (int l = 0; l < np; ++l) {
+            eid[l] = (uint16_t)pedge[T.t0 + l];
+            perm[l] = (uint16_t)l;
             pair_tile[T.t0 + l] = (int32_t)ti;
-            slot_eid[T.sb + sl] = (uint16_t)pedge[T.t0 + l];
-            pos[T.sb + l] = (uint16_t)sl;
-            spath[T.sb + sl] = lpath[l];
         }
+        std::stable_sort(perm, perm + np, [&](uint16_t a, uint16_t b) { return eid[a] < eid[b]; });
+        for (int i = 0; i < npath; ++i) {
+            poff[i] = (uint16_t)(pptr[T.p0 + i] - T.t0);
+            for (int32_t t = pptr[T.p0 + i]; t < pptr[T.p0 + i + 1]; ++t) spath[t - T.t0] = (uint8_t)i;
+        }
+        poff[npath] = (uint16_t)np;
+        for (int j = 0; j < nc; ++j) {
+            lcpp[j] = (uint16_t)(cpp[T.c0 + j] - T.p0);
+            for (int32_t p = cpp[T.c0 + j]; p < cpp[T.c0 + j + 1]; ++p) pcom[p - T.p0] = (uint8_t)j;
+        }
+        lcpp[nc] = (uint16_t)npath;
+        for (int k = 0; k <= NW; ++k) gpath[k] = (uint16_t)(cpp[tgroups[ti][k]] - T.p0);
     }
+    // compulsory HBM bytes of one M pass: what the bulk copies read plus what the pass writes
+    int64_t bytes = 0;
+    for (const TileDesc &d : tiles) {
+        const int npath = d.p1 - d.p0, nc = d.c1 - d.c0;
+        const int npa = even(d.p1 - (d.p0 & ~1)), nca = even(d.c1 - (d.c0 & ~1));
+        bytes += 8LL * even(d.np) + meta_off(d.np, npath, nc).bytes + 16LL * npa + 16LL * nca;  // reads
+        bytes += 8LL * d.np + 16LL * npath + 8LL * nc;                                            // writes
+    }
+    L->bytes_per_pass = bytes;
     L->desc.alloc(tiles.size() ? tiles.size() : 1);
-    L->slot_eid.alloc(slot ? slot : 1);
-    L->pos.alloc(slot ? slot : 1);
-    L->spath.alloc(slot ? slot : 1);
-    L->pair_slot.alloc(I.NP ? I.NP : 1);
+    L->meta.alloc(meta.size());
     L->pair_tile.alloc(I.NP ? I.NP : 1);
     h2d(L->desc.p, tiles.data(), tiles.size(), s);
-    h2d(L->slot_eid.p, slot_eid.data(), slot, s);
-    h2d(L->pos.p, pos.data(), slot, s);
-    h2d(L->spath.p, spath.data(), slot, s);
-    h2d(L->pair_slot.p, pair_slot.data(), I.NP, s);
+    h2d(L->meta.p, meta.data(), meta.size(), s);
     h2d(L->pair_tile.p, pair_tile.data(), I.NP, s);
     PF_CUDA(cudaStreamSynchronize(s));
     L->h_desc = std::move(tiles);
@@ -957,7 +1144,7 @@ struct FastSolver {
     int G = 0, nslices = 1;
     size_t smem = 0;
     DevBuf<double> dcon[2], dn[2], dd[2], x[2];
-    DevBuf<double> dc, adj, ne, tot, partT, partL, sub, res, res_dc, root_sums;
+    DevBuf<double> D, dc, adj, ne, tot, partT, partL, sub, res, res_dc, root_sums;
     DevBuf<int32_t> grp_count, err;
     DevBuf<Ctrl> ctrl;
     Params P{};
@@ -976,11 +1163,12 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
         if (!inst->idx->tiles) inst->idx->tiles = build_tiles(inst, s);
         F->L = inst->idx->tiles;
     }
-    F->smem = smem_bytes((int)I.E);
+    F->smem = (size_t)smem_plan(F->L->tps, (int)I.E).total;
     int dev = inst->device();
     cudaDeviceProp prop;
     PF_CUDA(cudaGetDeviceProperties(&prop, dev));
-    require(F->smem <= (size_t)prop.sharedMemPerBlockOptin,
+    const size_t static_smem = sizeof(Ctrl) + sizeof(CtaShared) + 64;
+    require(F->smem + static_smem <= (size_t)prop.sharedMemPerBlockOptin,
             "fast mode: edge tables do not fit in shared memory (too many edges)");
     PF_CUDA(cudaFuncSetAttribute(k_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F->smem));
     PF_CUDA(cudaFuncSetAttribute(k_pass<MODE_M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F->smem));
@@ -993,16 +1181,19 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     G = std::max(1, std::min(G, F->L->ntiles));
     F->G = G;
     int ngroups = (int)((I.E + RGRP - 1) / RGRP);
-    int warps = G * (NT / 32);
+    int warps = G * NW;
     F->nslices = std::max(1, std::min(G, warps / std::max(ngroups, 1)));
     F->nslices = std::min(F->nslices, 32);
     int64_t E = I.E ? I.E : 1;
     for (int b = 0; b < 2; ++b) {
-        F->dcon[b].alloc(F->L->nslots ? F->L->nslots : 1);
-        F->dn[b].alloc(I.P ? I.P : 1);
-        F->dd[b].alloc(I.C ? I.C : 1);
-        F->x[b].alloc(I.P ? I.P : 1);
+        F->dcon[b].alloc(F->L->nslots + SLOT_ALIGN);
+        F->dn[b].alloc(I.P + 2);
+        F->dd[b].alloc(I.C + 2);
+        F->x[b].alloc(I.P + 2);
     }
+    F->D.alloc(I.C + 2);
+    PF_CUDA(cudaMemsetAsync(F->D.p, 0, F->D.bytes(), s));
+    if (I.C) PF_CUDA(cudaMemcpyAsync(F->D.p, inst->demand.p, sizeof(double) * I.C, cudaMemcpyDeviceToDevice, s));
     F->dc.alloc(E);
     F->adj.alloc(E);
     F->ne.alloc(E);
@@ -1032,10 +1223,10 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     P.ntiles = F->L->ntiles;
     P.G = G;
     P.nslices = F->nslices;
+    P.tps = F->L->tps;
     P.desc = F->L->desc.p;
-    P.slot_eid = F->L->slot_eid.p;
-    P.pos = F->L->pos.p;
-    P.spath = F->L->spath.p;
+    P.meta = F->L->meta.p;
+    P.D = F->D.p;
     for (int b = 0; b < 2; ++b) {
         P.dcon[b] = F->dcon[b].p;
         P.dn[b] = F->dn[b].p;
@@ -1150,7 +1341,8 @@ static int64_t fast_run_dist(FastSolver *F, int64_t max_steps, cudaStream_t s, f
 void fast_init(FastSolver *F, const double *d_x0, int64_t alpha0, double beta0, cudaStream_t s) {
     const Index &I = *F->inst->idx;
     for (int b = 0; b < 2; ++b) {
-        PF_CUDA(cudaMemcpyAsync(F->x[b].p, d_x0, sizeof(double) * I.P, cudaMemcpyDeviceToDevice, s));
+        PF_CUDA(cudaMemsetAsync(F->x[b].p, 0, F->x[b].bytes(), s));
+        if (I.P) PF_CUDA(cudaMemcpyAsync(F->x[b].p, d_x0, sizeof(double) * I.P, cudaMemcpyDeviceToDevice, s));
         PF_CUDA(cudaMemsetAsync(F->dcon[b].p, 0, F->dcon[b].bytes(), s));
         PF_CUDA(cudaMemsetAsync(F->dn[b].p, 0, F->dn[b].bytes(), s));
         PF_CUDA(cudaMemsetAsync(F->dd[b].p, 0, F->dd[b].bytes(), s));
@@ -1240,9 +1432,7 @@ void fast_export_state(FastSolver *F, double *x, double *y, double *dd, double *
     PF_CUDA(cudaStreamSynchronize(s));
     const int dcur = c.iteration == 0 ? c.db : (c.db ^ 1);
     DevBuf<double> dy(I.NP ? I.NP : 1), ddc(I.NP ? I.NP : 1), tmp(std::max<int64_t>({I.C, I.E, I.P, 1}));
-    if (I.NP)
-        k_export_pairs<<<ceil_div(I.NP, 256), 256, 0, s>>>(F->P, F->L->pair_tile.p, F->L->pair_slot.p, dy.p,
-                                                           ddc.p);
+    if (I.NP) k_export_pairs<<<ceil_div(I.NP, 256), 256, 0, s>>>(F->P, F->L->pair_tile.p, dy.p, ddc.p);
     PF_CHECK_LAUNCH();
     if (x) d2h(x, F->x[c.xc].p, I.P, s);
     if (y) d2h(y, dy.p, I.NP, s);
@@ -1265,12 +1455,10 @@ void fast_stats(FastSolver *F, int64_t *launches, int64_t *tiles, int64_t *grid,
     if (launches) *launches = F->launches;
     if (tiles) *tiles = F->L->ntiles;
     if (grid) *grid = F->G;
-    // compulsory HBM bytes per iteration of this layout (one fused pass):
-    //  per slot: dual_consensus read + write (16) + slot_eid (2) + pos (2) + spath (1)
-    //  per path: x_k read + x_{k+1} write (16) + dual_nonneg read + write (16) + pair_ptr (4)
-    //  per commodity: dual_demand read + write (16) + demand (8) + com_path_ptr (4)
-    //  per CTA: edge partials T and L written and read back (4 x 8 B per edge)
-    if (bytes) *bytes = 21 * F->L->nslots + 36 * I.P + 28 * I.C + (int64_t)F->G * I.E * 32;
+    // compulsory HBM bytes per iteration of this layout: one M pass (bulk-copied
+    // inputs + written state) plus the CTA edge partials T and L written and read
+    // back (4 x 8 B per edge per CTA)
+    if (bytes) *bytes = F->L->bytes_per_pass + (int64_t)F->G * I.E * 32;
 }
 
 }  // namespace pf

@@ -248,8 +248,33 @@ void score_paths_device(const pf_instance *inst, const double *d_rates, int64_t 
 
 // ----------------------------------------------------------------- inline device math
 
-__host__ __device__ __forceinline__ double npmax0(double v) { return v < 0.0 ? 0.0 : v; }  // np.maximum(v,0)
-__host__ __device__ __forceinline__ double max0(double v) { return v > 0.0 ? v : 0.0; }    // numba clamp
+// On the device both clamps are one compare + one select (setp/selp); the
+// compiler's own max-pattern lowering adds NaN/-0 fix-ups that these exact
+// semantics do not need.
+__host__ __device__ __forceinline__ double npmax0(double v) {  // np.maximum(v, 0): NaN and -0.0 pass through
+#ifdef __CUDA_ARCH__
+    double r;
+    asm("{\n\t.reg .pred p;\n\tsetp.lt.f64 p, %1, 0d0000000000000000;\n\t"
+        "selp.f64 %0, 0d0000000000000000, %1, p;\n\t}"
+        : "=d"(r)
+        : "d"(v));
+    return r;
+#else
+    return v < 0.0 ? 0.0 : v;
+#endif
+}
+__host__ __device__ __forceinline__ double max0(double v) {  // numba clamp `v if v > 0 else 0`: NaN -> 0
+#ifdef __CUDA_ARCH__
+    double r;
+    asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %1, 0d0000000000000000;\n\t"
+        "selp.f64 %0, %1, 0d0000000000000000, p;\n\t}"
+        : "=d"(r)
+        : "d"(v));
+    return r;
+#else
+    return v > 0.0 ? v : 0.0;
+#endif
+}
 __host__ __device__ __forceinline__ double pymax1(double v) { return v > 1.0 ? v : 1.0; }  // max(1.0, v)
 
 // kernels.py:153-173: safeguarded Newton + bisection for alpha >= 2 (kept out of

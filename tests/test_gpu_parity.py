@@ -367,3 +367,22 @@ def test_edge_cases(mode):
         pf.solve(inst, pf.SolverConfig(mode=mode), warm_start=np.array([1.0, np.nan, 2.0]))
     with pytest.raises(pf.InputError):
         pf.solve(inst, pf.SolverConfig(mode=mode), warm_start=np.array([1.0, 2.0]))
+
+
+@pytest.mark.parametrize("n,k", [(60, 8), (50, 1), (45, 3)])
+def test_fast_iterations_match_exact_generated(n, k):
+    """Larger generated instances (many tiles, full 32-path groups at k=8, 32
+    single-path commodities per group at k=1): iterations 1-3 of the fused
+    kernel agree with the exact-order path to 1e-11."""
+    from b200_helpers import generated
+    topo, tab, ps = generated(n, k, 1.5)
+    inst = pf.build_instance(topo, tab, ps, device=0)
+    ex = pf.Solver(inst, pf.SolverConfig(mode="exact")).init()
+    fa = pf.Solver(inst, pf.SolverConfig(mode="fast")).init()
+    for it in (1, 2, 3):
+        ex.run(1)
+        fa.run(1)
+        a, b = ex.state(), fa.state()
+        assert a.iteration == b.iteration == it
+        for f in ("x", "y", "dual_demand", "dual_capacity", "dual_consensus", "dual_nonneg"):
+            np.testing.assert_allclose(getattr(b, f), getattr(a, f), rtol=1e-10, atol=1e-10, err_msg=f"{it} {f}")
