@@ -26,7 +26,8 @@ def lib():
     if _lib is None:
         with _lock:
             if _lib is None:
-                path = _build.LIB
+                # PF_B200_LIB selects a tuning variant built with build.py --variant
+                path = os.environ.get("PF_B200_LIB") or _build.LIB
                 if not os.path.exists(path):
                     try:
                         _build.build()

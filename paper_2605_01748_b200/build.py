@@ -55,8 +55,12 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OUT_DIR, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, variant: str | None = None, defines=()) -> str:
+    """Build the library.  `variant` + `defines` build a tuning variant into
+    _build/<variant>/ (selected at run time with PF_B200_LIB=<path>)."""
+    out_dir = os.path.join(OUT_DIR, variant) if variant else OUT_DIR
+    lib_path = os.path.join(out_dir, "libpf_b200.so") if variant else LIB
+    os.makedirs(out_dir, exist_ok=True)
     nvcc = _nvcc()
     env = dict(os.environ)
     # The image's $CC may point at a gcc wrapper without libgomp; nvcc uses the system gcc.
@@ -65,27 +69,29 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     hdrs = headers()
     for src in sources():
-        obj = os.path.join(OUT_DIR, os.path.basename(src) + ".o")
+        obj = os.path.join(out_dir, os.path.basename(src) + ".o")
         objs.append(obj)
         if force or _stale(obj, [src, __file__] + hdrs):
-            cmd = [nvcc] + ARCH + NVCC_FLAGS + ["-c", src, "-o", obj]
+            cmd = [nvcc] + ARCH + NVCC_FLAGS + [f"-D{d}" for d in defines] + ["-c", src, "-o", obj]
             if verbose:
                 print(" ".join(cmd), flush=True)
             subprocess.run(cmd, check=True, env=env)
-    if force or _stale(LIB, objs):
-        cmd = [nvcc] + ARCH + ["-shared", "-o", LIB] + objs + ["-lgomp", "-lcudart", "-ldl"]
+    if force or _stale(lib_path, objs):
+        cmd = [nvcc] + ARCH + ["-shared", "-o", lib_path] + objs + ["-lgomp", "-lcudart", "-ldl"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True, env=env)
-    return LIB
+    return lib_path
 
 
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-v", "--verbose", action="store_true")
+    ap.add_argument("--variant", default=None, help="tuning variant name (output _build/<variant>/)")
+    ap.add_argument("-D", dest="defines", action="append", default=[], help="preprocessor define for a variant")
     a = ap.parse_args(argv)
-    print(build(force=a.force, verbose=a.verbose))
+    print(build(force=a.force, verbose=a.verbose, variant=a.variant, defines=a.defines))
 
 
 if __name__ == "__main__":

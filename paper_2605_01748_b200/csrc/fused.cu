@@ -48,6 +48,7 @@
 #include <algorithm>
 #include <array>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 
@@ -57,12 +58,16 @@ namespace cg = cooperative_groups;
 
 namespace pf {
 
-constexpr int NW = 4;             // warps per CTA = commodity groups per tile
+#ifndef PF_NW
+#define PF_NW 8
+#endif
+constexpr int NW = PF_NW;         // warps per CTA = commodity groups per tile
 constexpr int NT = 32 * NW;       // threads per CTA
 constexpr int GPATH = 32;         // max paths per group (one lane per path)
 constexpr int TPATH = NW * GPATH; // max paths per tile
 constexpr int TCOM = TPATH;       // max commodities per tile
-constexpr int TPS_MIN = 1536;     // default max pairs per tile
+static_assert(TPATH <= 256, "tile-local path / commodity indices are u8");
+constexpr int TPS_MIN = 2560;     // default max pairs per tile
 constexpr int SLOT_ALIGN = 16;    // tile start alignment in the per-pair arrays (128 B)
 constexpr int RGRP = 32;          // edges per reduction group (one lane per edge)
 constexpr unsigned FULL = 0xffffffffu;
@@ -102,9 +107,9 @@ __host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc) 
 // Dynamic shared memory: two stages + work arrays + the per-edge tables.
 struct SmemPlan {
     int stage, s_dcon, s_meta, s_xk, s_xo, s_dn, s_D, s_dd;  // offsets inside a stage
-    int y, tv, xn, adj, accT, accL, total;                  // offsets from the base
+    int y, xn, accT, accL, total;                           // offsets from the base
 };
-__host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E) {
+__host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E, int nbuf) {
     SmemPlan s;
     int o = 0;
     s.s_dcon = o;
@@ -122,15 +127,11 @@ __host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E) {
     s.s_dd = o;
     o += 8 * (TCOM + 2);
     s.stage = r16(o);
-    o = 2 * s.stage;
+    o = nbuf * s.stage;
     s.y = o;
-    o += 8 * tps;
-    s.tv = o;
     o += 8 * tps;
     s.xn = o;
     o += 8 * TPATH;
-    s.adj = o;
-    o += r16(8 * E);
     s.accT = o;
     o += r16(8 * E);
     s.accL = o;
@@ -158,7 +159,7 @@ struct Ctrl {
 
 struct Params {
     InstView I;
-    int32_t ntiles, G, nslices, tps;
+    int32_t ntiles, G, nslices, tps, nbuf;
     const TileDesc *desc;
     const uint8_t *meta;
     const double *D;  // [C + 2] demand (padded copy for 16-byte bulk copies)
@@ -208,6 +209,9 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                      su32(dst)),
                  "l"(src), "r"(bytes), "r"(su32(b))
                  : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
 }
 // order this thread's generic-proxy accesses before later async-proxy (TMA) ones
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;\n" ::: "memory"); }
@@ -448,7 +452,8 @@ struct Tail {
 };
 
 struct Acc {
-    double *adj, *accT, *accL, *y, *tv, *xn;
+    const double *adj;  // global (L1-cached: written only by the edge phase, read after a grid barrier)
+    double *accT, *accL, *y, *xn;
 };
 
 // MODE_M : B(k+1) [y, K/w, roots, x_{k+1}] fused with A(k+2) [duals_{k+2}, T/L]
@@ -482,7 +487,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
         if (MODE == MODE_A1)
             y = st.xk[i];
         else
-            y = max0((MODE == MODE_RB ? st.xo[i] : st.xk[i]) + dcon[l] - A.adj[eid[l]]);
+            y = max0((MODE == MODE_RB ? st.xo[i] : st.xk[i]) + dcon[l] - __ldca(&A.adj[eid[l]]));
         ys[l] = y;
     }
     __syncwarp();
@@ -554,22 +559,13 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
         }
     }
     __syncwarp();
-    // (3) pairs: dual_consensus (kernels.py:72), T value x + dcon' (kernels.py:91)
-    for (int l = l0 + lane; l < l1; l += 32) {
-        const double dks = dcon[l] * f;
-        const double xn = A.xn[spath[l]];
-        const double dnew = max0(dks + xn - ys[l]);
-        io.dcon_out[d.sb + l] = dnew;
-        const double df = dnew - dks;
-        r_dcon += df * df;
-        A.tv[l] = xn + dnew;
-    }
     __syncthreads();
 
-    // (4) per-edge T and L of the tile over the edge-sorted permutation.  Warp w
-    // owns sorted slots [s0, s1), lane `lane` the consecutive items [a, b): a
-    // sequential segmented sum per lane, one warp scan of the lane aggregates,
-    // then a second sequential pass that adds each run total to the CTA
+    // (3) pairs in edge-sorted order: dual_consensus (kernels.py:72) and the
+    // per-edge sums T = sum (x + dcon') (kernels.py:91) and L = sum y
+    // (kernels.py:210).  Warp w owns sorted slots [s0, s1), lane `lane` the
+    // consecutive items [a, b): a sequential segmented sum per lane, one warp
+    // scan of the lane aggregates, then the run totals go to the CTA
     // accumulators (a run never repeats an edge within a tile: no conflicts).
     // A run begun in an earlier warp is completed after the barrier from the
     // warps' tails.
@@ -578,7 +574,6 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     const int IT = (s1 - s0 + 31) >> 5;
     const int a = min(s0 + lane * IT, s1), b = min(a + IT, s1);
     const int kbefore = a > 0 ? (int)eid[perm[a - 1]] : -1;
-    const double *tv = A.tv;
     // one sequential pass per lane: runs that start and end inside the lane are
     // added at once; the lane's prefix (continuing a run begun before item a)
     // and its last run are settled after the warp scan.
@@ -604,8 +599,15 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
             cT = 0.0;
             cL = 0.0;
         }
-        cT += tv[pl];
-        if (MODE != MODE_RB) cL += ys[pl];
+        const double xn = A.xn[spath[pl]];
+        const double dks = dcon[pl] * f;
+        const double yv = ys[pl];
+        const double dnew = max0(dks + xn - yv);
+        io.dcon_out[d.sb + pl] = dnew;
+        const double df = dnew - dks;
+        r_dcon += df * df;
+        cT += xn + dnew;
+        if (MODE != MODE_RB) cL += yv;
         pk = k;
     }
     const bool hh = !pre;  // the lane holds a run head
@@ -745,22 +747,22 @@ template <int MODE>
 __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *base, CtaShared &cs, uint32_t &seq) {
     const int g = blockIdx.x, tid = threadIdx.x;
     const int E = P.I.E;
-    const SmemPlan sp = smem_plan(P.tps, E);
+    const SmemPlan sp = smem_plan(P.tps, E, P.nbuf);
     Acc A;
-    A.adj = (double *)(base + sp.adj);
+    A.adj = P.adj;
     A.accT = (double *)(base + sp.accT);
     A.accL = (double *)(base + sp.accL);
     A.y = (double *)(base + sp.y);
-    A.tv = (double *)(base + sp.tv);
     A.xn = (double *)(base + sp.xn);
     const int my = g < P.ntiles ? (P.ntiles - 1 - g) / P.G + 1 : 0;
     const bool rev = (c.iteration & 1) != 0;
     auto tile_of = [&](int k) { return g + (rev ? my - 1 - k : k) * P.G; };
+    const bool dbl = P.nbuf == 2;
     if (tid == 0) {
         cs.io = pass_io<MODE>(P, c);
         fence_proxy_async();  // this pass's inputs were written by generic stores after a grid barrier
         if (my > 0) {
-            const int b = seq & 1;
+            const int b = dbl ? (seq & 1) : 0;
             cs.sd[b] = P.desc[tile_of(0)];
             issue_tile<MODE>(P, cs.io, cs.sd[b], base, sp, b, &cs.bar[b]);
         }
@@ -768,23 +770,37 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
     for (int e = tid; e < E; e += NT) {
         A.accT[e] = 0.0;
         A.accL[e] = 0.0;
-        A.adj[e] = MODE == MODE_A1 ? 0.0 : __ldcg(&P.adj[e]);
     }
+    // adj is read through L1 (ld.global.ca); it was rewritten by the edge phase
+    // before the grid barrier, so drop any stale L1 lines (acquire at gpu scope)
+    asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
     __syncthreads();
     const PassIO &io = cs.io;
     double r_x = 0.0, r_dd = 0.0, r_dcon = 0.0, r_dn = 0.0;
     for (int k = 0; k < my; ++k, ++seq) {
-        const int b = seq & 1;
-        if (tid == 0 && k + 1 < my) {  // prefetch the next tile into the other stage
-            const int nb = b ^ 1;
-            cs.sd[nb] = P.desc[tile_of(k + 1)];
-            issue_tile<MODE>(P, io, cs.sd[nb], base, sp, nb, &cs.bar[nb]);
+        const int b = dbl ? (seq & 1) : 0;
+        const uint32_t par = dbl ? ((seq >> 1) & 1) : (seq & 1);
+        if (tid == 0 && k + 1 < my) {
+            if (dbl) {  // prefetch the next tile into the other stage
+                const int nb = b ^ 1;
+                cs.sd[nb] = P.desc[tile_of(k + 1)];
+                issue_tile<MODE>(P, io, cs.sd[nb], base, sp, nb, &cs.bar[nb]);
+            } else {  // single stage: warm L2 with the next tile's pair data
+                const TileDesc dn_ = P.desc[tile_of(k + 1)];
+                prefetch_l2(io.dcon_in + dn_.sb, 8u * even(dn_.np));
+                prefetch_l2(P.meta + (size_t)dn_.mb16 * 16,
+                            (uint32_t)meta_off(dn_.np, dn_.p1 - dn_.p0, dn_.c1 - dn_.c0).bytes);
+            }
         }
-        mbar_wait(&cs.bar[b], (seq >> 1) & 1);
+        mbar_wait(&cs.bar[b], par);
         const TileDesc d = cs.sd[b];
         const StageView st = stage_view(base, sp, b, d);
         tile_compute<MODE>(P, c, io, d, st, A, cs.tails, r_x, r_dd, r_dcon, r_dn);
-        __syncthreads();  // stage b is only read by generic accesses; free for the TMA of tile k + 2
+        __syncthreads();  // stage b is only read by generic accesses; free for the next TMA into it
+        if (!dbl && tid == 0 && k + 1 < my) {
+            cs.sd[0] = P.desc[tile_of(k + 1)];
+            issue_tile<MODE>(P, io, cs.sd[0], base, sp, 0, &cs.bar[0]);
+        }
     }
     for (int e = tid; e < E; e += NT) {
         P.partT[(size_t)g * E + e] = A.accT[e];
@@ -1026,9 +1042,17 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
                                                   " paths per commodity (commodity " + std::to_string(c) + ")");
         max_com_pairs = std::max<int64_t>(max_com_pairs, pptr[cpp[c + 1]] - pptr[cpp[c]]);
     }
-    const int64_t tps = std::max<int64_t>(TPS_MIN, (max_com_pairs + 63) / 64 * 64);
+    int64_t tps_min = TPS_MIN;
+    if (const char *v = getenv("PF_FAST_TPS")) tps_min = std::max(256, atoi(v)) / 64 * 64;
+    const int64_t tps = std::max<int64_t>(tps_min, (max_com_pairs + 63) / 64 * 64);
     require(tps <= 16384, "a commodity has too many demand-path pairs for a fast-mode tile");
     L->tps = (int32_t)tps;
+    // paths per group: as many as lets NW groups of mean-length paths fill a tile
+    // (k = 8, 9.2 hops: 3 commodities = 24 paths = ~220 pairs per warp)
+    int64_t max_paths = 1;
+    for (int64_t c = 0; c < I.C; ++c) max_paths = std::max<int64_t>(max_paths, cpp[c + 1] - cpp[c]);
+    const double mean_hops = I.P ? (double)I.NP / (double)I.P : 1.0;
+    const int64_t gmax = std::min<int64_t>(GPATH, std::max<int64_t>(max_paths, (int64_t)(tps / (NW * mean_hops * 1.08))));
     // groups
     std::vector<int32_t> gstart;  // first commodity of each group
     {
@@ -1039,7 +1063,7 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
             while (c < I.C) {
                 const int64_t npath = cpp[c + 1] - cpp[c0];
                 const int64_t npair = pptr[cpp[c + 1]] - pptr[cpp[c0]];
-                if (c > c0 && (npath > GPATH || npair > tps)) break;
+                if (c > c0 && (npath > gmax || npair > tps)) break;
                 ++c;
             }
         }
@@ -1141,7 +1165,7 @@ struct FastSolver {
     const pf_instance *inst;
     pf_config cfg;
     std::shared_ptr<TileLayout> L;
-    int G = 0, nslices = 1;
+    int G = 0, nslices = 1, nbuf = 1;
     size_t smem = 0;
     DevBuf<double> dcon[2], dn[2], dd[2], x[2];
     DevBuf<double> D, dc, adj, ne, tot, partT, partL, sub, res, res_dc, root_sums;
@@ -1163,7 +1187,9 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
         if (!inst->idx->tiles) inst->idx->tiles = build_tiles(inst, s);
         F->L = inst->idx->tiles;
     }
-    F->smem = (size_t)smem_plan(F->L->tps, (int)I.E).total;
+    F->nbuf = 1;  // measured: a second stage costs an SM's second CTA, which hides more
+    if (const char *v = getenv("PF_FAST_NBUF")) F->nbuf = std::max(1, std::min(2, atoi(v)));
+    F->smem = (size_t)smem_plan(F->L->tps, (int)I.E, F->nbuf).total;
     int dev = inst->device();
     cudaDeviceProp prop;
     PF_CUDA(cudaGetDeviceProperties(&prop, dev));
@@ -1224,6 +1250,7 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     P.G = G;
     P.nslices = F->nslices;
     P.tps = F->L->tps;
+    P.nbuf = F->nbuf;
     P.desc = F->L->desc.p;
     P.meta = F->L->meta.p;
     P.D = F->D.p;
