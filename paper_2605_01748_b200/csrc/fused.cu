@@ -81,16 +81,18 @@ __host__ __device__ __forceinline__ int even(int n) { return (n + 1) & ~1; }
 
 // Byte offsets of the sections of one tile's metadata block.
 struct MetaOff {
-    int eid, perm, spath, poff, pcom, cpp, gpath, bytes;
+    int eid, spath, skp, sspath, poff, pcom, cpp, gpath, bytes;
 };
 __host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc) {
     MetaOff m;
     int o = 0;
     m.eid = o;  // u16 [np] edge id of each pair (path-major)
     o += r16(2 * np);
-    m.perm = o;  // u16 [np] tile-local pair of each edge-sorted slot
-    o += r16(2 * np);
     m.spath = o;  // u8 [np] tile-local path of each pair
+    o += r16(np);
+    m.skp = o;  // u32 [np] (edge << 16) | tile-local pair, for the edge-sorted slots (stable by pair)
+    o += r16(4 * np);
+    m.sspath = o;  // u8 [np] tile-local path of each edge-sorted slot (= spath[perm[s]])
     o += r16(np);
     m.poff = o;  // u16 [npath + 1] tile-local pair offset of each path
     o += r16(2 * (npath + 1));
@@ -107,7 +109,7 @@ __host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc) 
 // Dynamic shared memory: two stages + work arrays + the per-edge tables.
 struct SmemPlan {
     int stage, s_dcon, s_meta, s_xk, s_xo, s_dn, s_D, s_dd;  // offsets inside a stage
-    int y, xn, accT, accL, total;                           // offsets from the base
+    int y, xn, adj, acc, total;                             // offsets from the base
 };
 __host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E, int nbuf) {
     SmemPlan s;
@@ -132,10 +134,10 @@ __host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E, int nbuf)
     o += 8 * tps;
     s.xn = o;
     o += 8 * TPATH;
-    s.accT = o;
+    s.adj = o;
     o += r16(8 * E);
-    s.accL = o;
-    o += r16(8 * E);
+    s.acc = o;  // double2 {T, L} per edge
+    o += r16(16 * E);
     s.total = o;
     return s;
 }
@@ -161,6 +163,7 @@ struct Params {
     InstView I;
     int32_t ntiles, G, nslices, tps, nbuf;
     const TileDesc *desc;
+    const int32_t *cta_ptr, *cta_tiles;  // CTA g walks tiles cta_tiles[cta_ptr[g] .. cta_ptr[g + 1])
     const uint8_t *meta;
     const double *D;  // [C + 2] demand (padded copy for 16-byte bulk copies)
     double *dcon[2], *dn[2], *dd[2], *x[2];
@@ -178,6 +181,7 @@ struct Params {
     double gamma, residual_ratio, beta_scale, beta_min, beta_max;
     int64_t alpha_target, max_iterations;
     int32_t adapt;
+    int32_t ablate;  // tuning only (PF_FAST_ABLATE): 1 skip y/paths/commodities, 2 skip the edge scan
 };
 
 // ------------------------------------------------------------------ TMA / mbarrier
@@ -302,6 +306,7 @@ __device__ __noinline__ void controller_step(const Params &P, Ctrl &c, double s,
     c.s = s;
     c.r = r;
     c.f = 1.0;
+    if (P.ablate) return;  // timing experiments: results are meaningless, keep iterating
     if (ec != INT_MAX) {
         c.status = PF_ERR_KERNEL_COEF;
         c.bad = ec;
@@ -452,8 +457,22 @@ struct Tail {
 };
 
 struct Acc {
-    const double *adj;  // global (L1-cached: written only by the edge phase, read after a grid barrier)
-    double *accT, *accL, *y, *xn;
+    double *adj, *y, *xn;
+    double2 *acc;  // per edge {T, L}
+};
+
+template <int MODE>
+__device__ __forceinline__ void acc_add(double2 *acc, int e, double T, double L) {
+    double2 v = acc[e];
+    v.x += T;
+    if (MODE != MODE_RB) v.y += L;
+    acc[e] = v;
+}
+
+struct Fix {
+    bool on;
+    int key, w;
+    double T, L;
 };
 
 // MODE_M : B(k+1) [y, K/w, roots, x_{k+1}] fused with A(k+2) [duals_{k+2}, T/L]
@@ -461,13 +480,12 @@ struct Acc {
 // MODE_A1: A(1) with y_0 = x_0[pair_path] (controller.py:118)
 template <int MODE>
 __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, const PassIO &io, const TileDesc &d,
-                                             const StageView &st, const Acc &A, Tail *tails, double &r_x,
+                                             const StageView &st, const Acc &A, Tail *tails, Fix &fx, double &r_x,
                                              double &r_dd, double &r_dcon, double &r_dn) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int np = d.np, npath = d.p1 - d.p0, nc = d.c1 - d.c0;
     const MetaOff m = meta_off(np, npath, nc);
     const uint16_t *eid = (const uint16_t *)(st.meta + m.eid);
-    const uint16_t *perm = (const uint16_t *)(st.meta + m.perm);
     const uint8_t *spath = st.meta + m.spath;
     const uint16_t *poff = (const uint16_t *)(st.meta + m.poff);
     const uint8_t *pcom = st.meta + m.pcom;
@@ -476,19 +494,21 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     const double *dcon = st.dcon;
     double *ys = A.y;
     const double f = io.f;
+    double *const dcon_out = io.dcon_out + d.sb;  // register copies: no reloads from shared memory
+    double *const x_out = io.x_out, *const dn_out = io.dn_out, *const dd_out = io.dd_out;
 
     // ---- this warp's commodity group
     const int gp0 = gpath[w], gp1 = gpath[w + 1];
     const int l0 = poff[gp0], l1 = poff[gp1];
-    // (1) pairs: y (kernels.py:98-100)
-    for (int l = l0 + lane; l < l1; l += 32) {
-        const int i = spath[l];
-        double y;
-        if (MODE == MODE_A1)
-            y = st.xk[i];
-        else
-            y = max0((MODE == MODE_RB ? st.xo[i] : st.xk[i]) + dcon[l] - __ldca(&A.adj[eid[l]]));
-        ys[l] = y;
+    if (!(P.ablate & 1)) {
+    // (1) pairs: y (kernels.py:98-100); the path's rate comes from its lane
+    const double xlane = gp0 + lane < gp1 ? (MODE == MODE_RB ? st.xo[gp0 + lane] : st.xk[gp0 + lane]) : 0.0;
+#pragma unroll 4
+    for (int base = l0; base < l1; base += 32) {
+        const int l = base + lane;
+        const int i = l < l1 ? (int)spath[l] - gp0 : 0;
+        const double xp = __shfl_sync(FULL, xlane, i);
+        if (l < l1) ys[l] = MODE == MODE_A1 ? xp : max0(xp + dcon[l] - A.adj[eid[l]]);
     }
     __syncwarp();
     // (2) paths (lane = path) and commodities (lane segments)
@@ -509,7 +529,14 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
             double K = 0.0, wgt = 0.0;
             if (valid) {
                 const int lo = poff[p], hi = poff[p + 1];
-                for (int l = lo; l < hi; ++l) K += ys[l] - dcon[l];
+                double K1 = 0.0;  // two chains (fixed association)
+                int l = lo;
+                for (; l + 1 < hi; l += 2) {
+                    K += ys[l] - dcon[l];
+                    K1 += ys[l + 1] - dcon[l + 1];
+                }
+                if (l < hi) K += ys[l] - dcon[l];
+                K += K1;
                 const double dnv = st.dn[p];
                 const double h = (double)(hi - lo);
                 if (xk < dnv) {  // frozen non-negativity activity (kernels.py:114-119)
@@ -535,7 +562,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
                     ct = commodity_term(Sc, D, ddk, c.beta, c.alpha);
                 }
                 xv = wgt * (K + ct);
-                io.x_out[d.p0 + p] = xv;
+                x_out[d.p0 + p] = xv;
                 const double df = xv - xk;
                 r_x += df * df;
             }
@@ -544,7 +571,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
             A.xn[p] = xv;
             const double o = st.dn[p] * f;
             const double n = npmax0(o - xv);
-            io.dn_out[d.p0 + p] = n;
+            dn_out[d.p0 + p] = n;
             const double dg = n - o;
             r_dn += dg * dg;
         }
@@ -553,7 +580,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
         if (head) {
             const double dold = st.dd[j] * f;
             const double dnew = npmax0(dold + (Sx - st.D[j]));
-            io.dd_out[cc] = dnew;
+            dd_out[cc] = dnew;
             const double df = dnew - dold;
             r_dd += df * df;
         }
@@ -561,6 +588,8 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     __syncwarp();
     __syncthreads();
 
+    }
+    if (P.ablate & 2) return;
     // (3) pairs in edge-sorted order: dual_consensus (kernels.py:72) and the
     // per-edge sums T = sum (x + dcon') (kernels.py:91) and L = sum y
     // (kernels.py:210).  Warp w owns sorted slots [s0, s1), lane `lane` the
@@ -573,49 +602,53 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     const int s0 = min(w * q, np), s1 = min(s0 + q, np);
     const int IT = (s1 - s0 + 31) >> 5;
     const int a = min(s0 + lane * IT, s1), b = min(a + IT, s1);
-    const int kbefore = a > 0 ? (int)eid[perm[a - 1]] : -1;
-    // one sequential pass per lane: runs that start and end inside the lane are
-    // added at once; the lane's prefix (continuing a run begun before item a)
-    // and its last run are settled after the warp scan.
-    int pk = kbefore;
-    bool pre = true;  // still in the prefix
-    bool pn = false;  // the prefix is non-empty
+    const uint32_t *skp = (const uint32_t *)(st.meta + m.skp);
+    const uint8_t *sspath = st.meta + m.sspath;
+    const int kbefore = a > 0 ? (int)(skp[a - 1] >> 16) : -1;
+    // one sequential pass per lane: the lane's prefix (items continuing the run
+    // open at item a) is summed first; runs that start inside the lane are added
+    // at their end; the prefix and the lane's last run are settled after the
+    // warp scan.
     double cT = 0.0, cL = 0.0, pT = 0.0, pL = 0.0;
-    int pkey = -1;
-    for (int s = a; s < b; ++s) {
-        const int pl = perm[s];
-        const int k = eid[pl];
-        if (k != pk) {  // run head at s
-            if (pre) {
-                pre = false;
-                pn = s > a;
-                pT = cT;
-                pL = cL;
-                pkey = pk;
-            } else {
-                A.accT[pk] += cT;
-                if (MODE != MODE_RB) A.accL[pk] += cL;
-            }
-            cT = 0.0;
-            cL = 0.0;
-        }
-        const double xn = A.xn[spath[pl]];
+    const int pkey = kbefore;
+    int s = a;
+    uint32_t kp = s < b ? skp[s] : 0u;  // (edge << 16) | pair of the current item
+    auto item = [&](uint32_t kpv, int s_, double &T, double &L) {
+        const int pl = (int)(kpv & 0xffffu);
+        const double xn = A.xn[sspath[s_]];
         const double dks = dcon[pl] * f;
         const double yv = ys[pl];
         const double dnew = max0(dks + xn - yv);
-        io.dcon_out[d.sb + pl] = dnew;
+        dcon_out[pl] = dnew;
         const double df = dnew - dks;
         r_dcon += df * df;
-        cT += xn + dnew;
-        if (MODE != MODE_RB) cL += yv;
-        pk = k;
+        T += xn + dnew;
+        if (MODE != MODE_RB) L += yv;
+    };
+    while (s < b && (int)(kp >> 16) == kbefore) {
+        const uint32_t cur = kp;
+        if (s + 1 < b) kp = skp[s + 1];
+        item(cur, s, pT, pL);
+        ++s;
     }
-    const bool hh = !pre;  // the lane holds a run head
-    if (pre) {
-        pn = a < b;
-        pT = cT;
-        pL = cL;
-        pkey = pk;
+    const bool pn = s > a;  // the prefix is non-empty
+    const bool hh = s < b;  // the lane holds a run head
+    int pk = hh ? (int)(kp >> 16) : kbefore;
+    for (; s < b; ++s) {
+        const uint32_t cur = kp;
+        if (s + 1 < b) kp = skp[s + 1];  // next item's key in flight while this one computes
+        const int k = (int)(cur >> 16);
+        if (k != pk) {  // run head at s: the previous run ended inside the lane
+            acc_add<MODE>(A.acc, pk, cT, cL);
+            cT = 0.0;
+            cL = 0.0;
+            pk = k;
+        }
+        item(cur, s, cT, cL);
+    }
+    if (!hh) {  // the whole lane continues one run
+        cT = pT;
+        cL = pL;
     }
     // warp scan of (head, open-run aggregate): carry into each lane = the sum of
     // the run that is open at the lane's first item, over the earlier lanes
@@ -640,24 +673,21 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
         CL = 0.0;
     }
     const bool copen = (hm & ((1u << lane) - 1u)) == 0u;  // the carried run began before this warp's range
-    bool fix = false;
-    int fkey = 0;
-    double fT = 0.0, fL = 0.0;
     if (a < b) {
-        const int knext = b < np ? (int)eid[perm[b]] : -3;
+        const int knext = b < np ? (int)(skp[b] >> 16) : -3;
         // prefix run: items [a, first head) continue the carried run
         if (pn) {
             const double tT = CT + pT, tL = CL + pL;
             const bool ends = hh || knext != pkey;  // with a head in the lane the prefix ends before it
             if (ends) {
-                if (copen) {
-                    fix = true;
-                    fkey = pkey;
-                    fT = tT;
-                    fL = tL;
+                if (copen) {  // completed by the caller after the end-of-tile barrier
+                    fx.on = true;
+                    fx.key = pkey;
+                    fx.T = tT;
+                    fx.L = tL;
+                    fx.w = w;
                 } else {
-                    A.accT[pkey] += tT;
-                    if (MODE != MODE_RB) A.accL[pkey] += tL;
+                    acc_add<MODE>(A.acc, pkey, tT, tL);
                 }
             } else if (b == s1) {
                 tails[w] = Tail{tT, tL, copen ? 1 : 0, 0};
@@ -666,24 +696,27 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
         // last run of a lane with a head: started inside the lane
         if (hh) {
             if (knext != pk) {
-                A.accT[pk] += cT;
-                if (MODE != MODE_RB) A.accL[pk] += cL;
+                acc_add<MODE>(A.acc, pk, cT, cL);
             } else if (b == s1) {
                 tails[w] = Tail{cT, cL, 0, 0};
             }
         }
     }
-    __syncthreads();
-    if (fix) {  // the warp's first run began in an earlier warp: add the carried tails
-        double cT = 0.0, cL = 0.0;
-        for (int ww = w - 1; ww >= 0; --ww) {
-            cT += tails[ww].T;
-            cL += tails[ww].L;
-            if (!tails[ww].open) break;
-        }
-        A.accT[fkey] += cT + fT;
-        if (MODE != MODE_RB) A.accL[fkey] += cL + fL;
+}
+
+// The warp's first run began in an earlier warp of the same tile: add the
+// carried tails (after the end-of-tile barrier, before the next tile's scan).
+template <int MODE>
+__device__ __forceinline__ void apply_fix(Fix &fx, const Tail *tails, const Acc &A) {
+    if (!fx.on) return;
+    double cT = 0.0, cL = 0.0;
+    for (int ww = fx.w - 1; ww >= 0; --ww) {
+        cT += tails[ww].T;
+        cL += tails[ww].L;
+        if (!tails[ww].open) break;
     }
+    acc_add<MODE>(A.acc, fx.key, cT + fx.T, cL + fx.L);
+    fx.on = false;
 }
 
 template <int MODE>
@@ -749,14 +782,13 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
     const int E = P.I.E;
     const SmemPlan sp = smem_plan(P.tps, E, P.nbuf);
     Acc A;
-    A.adj = P.adj;
-    A.accT = (double *)(base + sp.accT);
-    A.accL = (double *)(base + sp.accL);
+    A.adj = (double *)(base + sp.adj);
+    A.acc = (double2 *)(base + sp.acc);
     A.y = (double *)(base + sp.y);
     A.xn = (double *)(base + sp.xn);
-    const int my = g < P.ntiles ? (P.ntiles - 1 - g) / P.G + 1 : 0;
+    const int t0 = P.cta_ptr[g], my = P.cta_ptr[g + 1] - t0;
     const bool rev = (c.iteration & 1) != 0;
-    auto tile_of = [&](int k) { return g + (rev ? my - 1 - k : k) * P.G; };
+    auto tile_of = [&](int k) { return P.cta_tiles[t0 + (rev ? my - 1 - k : k)]; };
     const bool dbl = P.nbuf == 2;
     if (tid == 0) {
         cs.io = pass_io<MODE>(P, c);
@@ -768,15 +800,14 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
         }
     }
     for (int e = tid; e < E; e += NT) {
-        A.accT[e] = 0.0;
-        A.accL[e] = 0.0;
+        A.acc[e] = make_double2(0.0, 0.0);
+        A.adj[e] = MODE == MODE_A1 ? 0.0 : __ldcg(&P.adj[e]);
     }
-    // adj is read through L1 (ld.global.ca); it was rewritten by the edge phase
-    // before the grid barrier, so drop any stale L1 lines (acquire at gpu scope)
-    asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
     __syncthreads();
     const PassIO &io = cs.io;
     double r_x = 0.0, r_dd = 0.0, r_dcon = 0.0, r_dn = 0.0;
+    Fix fx;
+    fx.on = false;
     for (int k = 0; k < my; ++k, ++seq) {
         const int b = dbl ? (seq & 1) : 0;
         const uint32_t par = dbl ? ((seq >> 1) & 1) : (seq & 1);
@@ -795,16 +826,19 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
         mbar_wait(&cs.bar[b], par);
         const TileDesc d = cs.sd[b];
         const StageView st = stage_view(base, sp, b, d);
-        tile_compute<MODE>(P, c, io, d, st, A, cs.tails, r_x, r_dd, r_dcon, r_dn);
+        tile_compute<MODE>(P, c, io, d, st, A, cs.tails, fx, r_x, r_dd, r_dcon, r_dn);
         __syncthreads();  // stage b is only read by generic accesses; free for the next TMA into it
+        apply_fix<MODE>(fx, cs.tails, A);
         if (!dbl && tid == 0 && k + 1 < my) {
             cs.sd[0] = P.desc[tile_of(k + 1)];
             issue_tile<MODE>(P, io, cs.sd[0], base, sp, 0, &cs.bar[0]);
         }
     }
+    __syncthreads();  // last tile's fix-ups
     for (int e = tid; e < E; e += NT) {
-        P.partT[(size_t)g * E + e] = A.accT[e];
-        if (MODE != MODE_RB) P.partL[(size_t)g * E + e] = A.accL[e];
+        const double2 v = A.acc[e];
+        P.partT[(size_t)g * E + e] = v.x;
+        if (MODE != MODE_RB) P.partL[(size_t)g * E + e] = v.y;
     }
     double *r = P.res + g * 8;
     double t;
@@ -834,7 +868,7 @@ __device__ __forceinline__ void cta_init(CtaShared &cs) {
 
 // ------------------------------------------------------------------ kernels
 
-__global__ void __launch_bounds__(NT) k_fused(const __grid_constant__ Params P) {
+__global__ void __launch_bounds__(NT, 2) k_fused(const __grid_constant__ Params P) {
     extern __shared__ __align__(128) char smem_raw[];
     __shared__ Ctrl c;
     __shared__ CtaShared cs;
@@ -903,7 +937,7 @@ __global__ void __launch_bounds__(NT) k_fused(const __grid_constant__ Params P) 
 // the same branch and issue matching collectives.
 
 template <int MODE>
-__global__ void __launch_bounds__(NT) k_pass(const __grid_constant__ Params P) {
+__global__ void __launch_bounds__(NT, 2) k_pass(const __grid_constant__ Params P) {
     extern __shared__ __align__(128) char smem_raw[];
     __shared__ Ctrl c;
     __shared__ CtaShared cs;
@@ -1042,7 +1076,16 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
                                                   " paths per commodity (commodity " + std::to_string(c) + ")");
         max_com_pairs = std::max<int64_t>(max_com_pairs, pptr[cpp[c + 1]] - pptr[cpp[c]]);
     }
+    // largest tile (<= TPS_MIN pairs) that keeps two CTAs per SM with this
+    // instance's per-edge tables; PF_FAST_TPS overrides (tuning)
     int64_t tps_min = TPS_MIN;
+    {
+        int per_sm = 0, reserved = 0;
+        PF_CUDA(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, inst->device()));
+        PF_CUDA(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, inst->device()));
+        const int64_t budget = per_sm / 2 - reserved - 1024;
+        while (tps_min > 1024 && smem_plan((int)tps_min, (int)I.E, 1).total > budget) tps_min -= 256;
+    }
     if (const char *v = getenv("PF_FAST_TPS")) tps_min = std::max(256, atoi(v)) / 64 * 64;
     const int64_t tps = std::max<int64_t>(tps_min, (max_com_pairs + 63) / 64 * 64);
     require(tps <= 16384, "a commodity has too many demand-path pairs for a fast-mode tile");
@@ -1117,7 +1160,7 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         const MetaOff m = meta_off(np, npath, nc);
         uint8_t *blk = meta.data() + (int64_t)T.mb16 * 16;
         uint16_t *eid = (uint16_t *)(blk + m.eid);
-        uint16_t *perm = (uint16_t *)(blk + m.perm);
+        std::vector<uint16_t> perm(np);
         uint8_t *spath = blk + m.spath;
         uint16_t *poff = (uint16_t *)(blk + m.poff);
         uint8_t *pcom = blk + m.pcom;
@@ -1128,12 +1171,18 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
             perm[l] = (uint16_t)l;
             pair_tile[T.t0 + l] = (int32_t)ti;
         }
-        std::stable_sort(perm, perm + np, [&](uint16_t a, uint16_t b) { return eid[a] < eid[b]; });
+        std::stable_sort(perm.begin(), perm.end(), [&](uint16_t a, uint16_t b) { return eid[a] < eid[b]; });
+        uint32_t *skp = (uint32_t *)(blk + m.skp);
+        uint8_t *sspath = blk + m.sspath;
         for (int i = 0; i < npath; ++i) {
             poff[i] = (uint16_t)(pptr[T.p0 + i] - T.t0);
             for (int32_t t = pptr[T.p0 + i]; t < pptr[T.p0 + i + 1]; ++t) spath[t - T.t0] = (uint8_t)i;
         }
         poff[npath] = (uint16_t)np;
+        for (int sl = 0; sl < np; ++sl) {
+            skp[sl] = ((uint32_t)eid[perm[sl]] << 16) | perm[sl];
+            sspath[sl] = spath[perm[sl]];
+        }
         for (int j = 0; j < nc; ++j) {
             lcpp[j] = (uint16_t)(cpp[T.c0 + j] - T.p0);
             for (int32_t p = cpp[T.c0 + j]; p < cpp[T.c0 + j + 1]; ++p) pcom[p - T.p0] = (uint8_t)j;
@@ -1169,7 +1218,7 @@ struct FastSolver {
     size_t smem = 0;
     DevBuf<double> dcon[2], dn[2], dd[2], x[2];
     DevBuf<double> D, dc, adj, ne, tot, partT, partL, sub, res, res_dc, root_sums;
-    DevBuf<int32_t> grp_count, err;
+    DevBuf<int32_t> grp_count, err, cta_ptr, cta_tiles;
     DevBuf<Ctrl> ctrl;
     Params P{};
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -1232,6 +1281,21 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
         for (int64_t e = 0; e < I.E; ++e) ned[e] = (double)cnt[e];
         h2d(F->ne.p, ned.data(), E, s);
     }
+    {  // static tile -> CTA assignment: round robin (tile g + k*G), so at any time
+       // the grid works on one contiguous window of tiles (DRAM / L2 locality;
+       // measured faster than a pair-balanced assignment)
+        const int64_t nt = F->L->ntiles;
+        std::vector<int32_t> ptr(G + 1, 0), flat;
+        flat.reserve(nt);
+        for (int g = 0; g < G; ++g) {
+            for (int64_t t = g; t < nt; t += G) flat.push_back((int32_t)t);
+            ptr[g + 1] = (int32_t)flat.size();
+        }
+        F->cta_ptr.alloc(G + 1);
+        F->cta_tiles.alloc(flat.size() ? flat.size() : 1);
+        h2d(F->cta_ptr.p, ptr.data(), G + 1, s);
+        h2d(F->cta_tiles.p, flat.data(), flat.size(), s);
+    }
     F->partT.alloc((size_t)G * E);
     F->partL.alloc((size_t)G * E);
     F->sub.alloc((size_t)2 * F->nslices * E);
@@ -1252,6 +1316,8 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     P.tps = F->L->tps;
     P.nbuf = F->nbuf;
     P.desc = F->L->desc.p;
+    P.cta_ptr = F->cta_ptr.p;
+    P.cta_tiles = F->cta_tiles.p;
     P.meta = F->L->meta.p;
     P.D = F->D.p;
     for (int b = 0; b < 2; ++b) {
@@ -1281,6 +1347,8 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     P.alpha_target = cfg.alpha_target;
     P.max_iterations = cfg.max_iterations;
     P.adapt = cfg.adapt;
+    P.ablate = 0;
+    if (const char *v = getenv("PF_FAST_ABLATE")) P.ablate = atoi(v);
     PF_CUDA(cudaStreamSynchronize(s));
     return F.release();
 }
