@@ -18,6 +18,8 @@
 #include <cub/cub.cuh>
 
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 
 #include "pf_internal.cuh"
 
@@ -124,64 +126,172 @@ __global__ void k_over(int32_t E, const double *loads, const double *cap, double
     if (o > 0.0) atomicAdd(nviol, 1);
 }
 
-// CTA-wide _sum_gather_range of x over the edge's pairs (projection.py:87-88).
-__device__ double cta_edge_resum(const InstView &I, const double *x, int32_t lo, int32_t hi, double *parts) {
+// CTA-wide _sum_gather_range of x over the edge's pairs (projection.py:87-88):
+// the values are gathered in parallel into shared memory one block at a time,
+// each 32-element chunk is summed sequentially and the chunk partials are added
+// in chunk order by one thread -- the reference's exact association.
+constexpr int RB = 8192;  // gather block (a multiple of the 32-element chunk)
+
+__device__ double cta_edge_resum(const int32_t *epath, const double *x, int32_t lo, int32_t hi, double *buf) {
+    __shared__ double s_parts[RB / BLK];
     __shared__ double s_total;
-    int32_t n = hi - lo;
-    int32_t nch = (n + BLK - 1) / BLK;
-    for (int32_t ch = threadIdx.x; ch < nch; ch += blockDim.x) {
-        int32_t cs = lo + ch * BLK, ce = cs + BLK < hi ? cs + BLK : hi;
-        double part = 0.0;
-        for (int32_t t = cs; t < ce; ++t) part += x[I.pair_path[I.edge_pairs[t]]];
-        parts[ch] = part;
+    if (threadIdx.x == 0) s_total = 0.0;
+    for (int32_t b0 = lo; b0 < hi; b0 += RB) {
+        const int32_t n = hi - b0 < RB ? hi - b0 : RB;
+        // 8 independent gathers in flight per thread
+        for (int32_t j0 = threadIdx.x; j0 < n; j0 += 8 * blockDim.x) {
+            int32_t pi[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int32_t j = j0 + u * blockDim.x;
+                pi[u] = j < n ? epath[b0 + j] : -1;
+            }
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = pi[u] >= 0 ? x[pi[u]] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int32_t j = j0 + u * blockDim.x;
+                if (j < n) buf[j] = v[u];
+            }
+        }
+        __syncthreads();
+        const int32_t nch = (n + BLK - 1) / BLK;
+        for (int32_t ch = threadIdx.x; ch < nch; ch += blockDim.x) {
+            const int32_t cs = ch * BLK, ce = cs + BLK < n ? cs + BLK : n;
+            double part = 0.0;
+            for (int32_t t = cs; t < ce; ++t) part += buf[t];
+            s_parts[ch] = part;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double total = s_total;
+            for (int32_t ch = 0; ch < nch; ++ch) total += s_parts[ch];
+            s_total = total;
+        }
+        __syncthreads();
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double total = 0.0;
-        for (int32_t ch = 0; ch < nch; ++ch) total += parts[ch];
-        s_total = total;
-    }
-    __syncthreads();
-    double r = s_total;
+    const double r = s_total;
     __syncthreads();
     return r;
 }
 
-// projection.py:83-106, one CTA walks the violated edges in order.
+// store a trimmed rate and mark the edges of its path for an exact re-sum
+__device__ __forceinline__ void write_back(const InstView &I, double *x, uint8_t *dirty, int32_t p, double v) {
+    if (x[p] != v) {
+        x[p] = v;
+        for (int32_t t = I.pair_ptr[p]; t < I.pair_ptr[p + 1]; ++t) dirty[I.pair_edge[t]] = 1;
+    }
+}
+
+constexpr int TCH = 4096;  // chunk of ordered candidates (dynamic shared memory: 2 x 48 KB)
+
 __global__ void __launch_bounds__(1024) k_edge_trim(InstView I, const int32_t *edge_order, const int32_t *nviol_p,
-                                                     const int32_t *path_order, double *x, double *parts) {
-    int32_t nviol = *nviol_p;
-    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+                                                     const int32_t *path_order, const int32_t *epath, double *x,
+                                                     const double *over, uint8_t *dirty, int stats) {
+    long long st_pass = 0, st_chain = 0, st_resum = 0, st_edges = 0;
+    extern __shared__ __align__(16) char dsm[];
+    double(*sx)[TCH] = (double(*)[TCH])dsm;                        // [2][TCH], also the re-sum buffer
+    int32_t(*sp)[TCH] = (int32_t(*)[TCH])(dsm + 2 * TCH * sizeof(double));  // [2][TCH]
+    __shared__ double s_ex;
+    __shared__ int32_t s_done;
+    const int32_t nviol = *nviol_p;
+    const int tid = threadIdx.x, nthr = blockDim.x;
     for (int32_t vi = 0; vi < nviol; ++vi) {
-        int32_t e = edge_order[vi];
-        int32_t lo = I.edge_pair_ptr[e], hi = I.edge_pair_ptr[e + 1];
-        double cap = I.capacity[e];
-        double excess = cta_edge_resum(I, x, lo, hi, parts) - cap;
+        const int32_t e = edge_order[vi];
+        const int32_t lo = I.edge_pair_ptr[e], hi = I.edge_pair_ptr[e + 1];
+        const double cap = I.capacity[e];
+        // an edge none of whose paths was trimmed since phase 3 began still has
+        // its exact starting load (same association as the re-sum)
+        double excess;
+        if (dirty[e]) {
+            excess = cta_edge_resum(epath, x, lo, hi, &sx[0][0]) - cap;
+            st_resum += hi - lo;
+        } else {
+            excess = over[e];
+        }
         if (excess <= 0.0) continue;
+        ++st_edges;
+        const int32_t nch = (hi - lo + TCH - 1) / TCH;
         for (int pass = 0; pass < 16; ++pass) {
-            if (warp == 0) {
-                double ex = excess;
-                for (int32_t base = lo; base < hi && ex > 0.0; base += 32) {
-                    int32_t t = base + lane;
-                    int32_t p = t < hi ? path_order[t] : -1;
-                    double xv = p >= 0 ? x[p] : 0.0;
-                    int n = hi - base < 32 ? hi - base : 32;
-                    for (int j = 0; j < n; ++j) {
-                        if (ex <= 0.0) break;
-                        double xj = __shfl_sync(0xffffffffu, xv, j);
-                        double d = xj < ex ? xj : ex;
-                        if (d > 0.0) {
-                            if (lane == j) x[p] = xj - d;
-                            ex -= d;
+            if (tid == 0) {
+                s_ex = excess;
+                s_done = 0;
+            }
+            // chunk 0
+            for (int32_t j = tid; j < TCH && lo + j < hi; j += nthr) {
+                const int32_t p = path_order[lo + j];
+                sp[0][j] = p;
+                sx[0][j] = x[p];
+            }
+            __syncthreads();
+            int32_t t = 0;
+            for (; t < nch; ++t) {
+                const int b = t & 1;
+                const int32_t base = lo + t * TCH;
+                const int32_t n = hi - base < TCH ? hi - base : TCH;
+                if (tid == 0) {  // the exact sequential chain (projection.py:95-102)
+                    // Once excess <= 0 every later step is a no-op (d <= 0), so
+                    // the chain runs unrolled without a per-element exit.
+                    double ex = s_ex;
+                    double *v = sx[b];
+                    int32_t j = 0;
+                    for (; j < n && ex > 0.0; j += 8) {
+                        double xv[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) xv[u] = j + u < n ? v[j + u] : 0.0;
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            // d = min(x, ex); if d > 0: x -= d, ex -= d  (projection.py:97-101):
+                            // x < ex:  d = x,  x - x = +0,  ex - x
+                            // x >= ex: d = ex, x - ex,      ex - ex = +0
+                            const double xu = xv[u];
+                            const bool c = xu < ex;
+                            const double t = ex - xu;
+                            const double nx = c ? (xu > 0.0 ? 0.0 : xu) : (ex > 0.0 ? xu - ex : xu);
+                            ex = c ? (xu > 0.0 ? t : ex) : (ex > 0.0 ? 0.0 : ex);
+                            if (j + u < n) v[j + u] = nx;
+                        }
+                    }
+                    s_ex = ex;
+                    st_chain += j;
+                    if (!(ex > 0.0)) s_done = 1;
+                } else if (tid >= 32) {
+                    const int nb = b ^ 1;
+                    const int ltid = tid - 32, lthr = nthr - 32;
+                    if (t >= 1) {  // write back chunk t-1
+                        const int32_t pbase = base - TCH;
+                        for (int32_t j = ltid; j < TCH && pbase + j < hi; j += lthr)
+                            write_back(I, x, dirty, sp[nb][j], sx[nb][j]);
+                    }
+                    if (t + 1 < nch) {  // gather chunk t+1
+                        const int32_t nbase = base + TCH;
+                        for (int32_t j = ltid; j < TCH && nbase + j < hi; j += lthr) {
+                            const int32_t p = path_order[nbase + j];
+                            sp[nb][j] = p;
+                            sx[nb][j] = x[p];
                         }
                     }
                 }
+                __syncthreads();
+                if (s_done) break;
+            }
+            {  // write back the last chained chunk
+                const int32_t tt = t < nch ? t : nch - 1;
+                const int b = tt & 1;
+                const int32_t base = lo + tt * TCH;
+                for (int32_t j = tid; j < TCH && base + j < hi; j += nthr) write_back(I, x, dirty, sp[b][j], sx[b][j]);
             }
             __syncthreads();
-            excess = cta_edge_resum(I, x, lo, hi, parts) - cap;
+            excess = cta_edge_resum(epath, x, lo, hi, &sx[0][0]) - cap;
+            st_resum += hi - lo;
+            ++st_pass;
             if (excess <= 0.0) break;
         }
     }
+    if (stats && threadIdx.x == 0)
+        printf("[k_edge_trim] violated %d trimmed %lld passes %lld chained %lld resummed %lld\n", nviol, st_edges,
+               st_pass, st_chain, st_resum);
 }
 
 }  // namespace
@@ -209,12 +319,19 @@ __global__ void k_edge_path_keys_violated(InstView I, const double *scores, cons
     vals[t] = p;
 }
 
+__global__ void k_edge_paths(InstView I, int32_t *epath) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < I.NP) epath[t] = I.pair_path[I.edge_pairs[t]];
+}
+
+constexpr int TRIM_SMEM = 2 * TCH * (sizeof(double) + sizeof(int32_t));
+
 // Persistent scratch for the projection of one instance's index spaces (allocated
 // once; no cudaMalloc / host synchronisation inside a projection).
 struct ProjWS {
     DevBuf<double> scores, sums, loads, over, parts;
-    DevBuf<uint8_t> viol;
-    DevBuf<int32_t> order, bad, nviol, eids, eorder, pvals, porder, sb, se;
+    DevBuf<uint8_t> viol, dirty;
+    DevBuf<int32_t> order, bad, nviol, eids, eorder, pvals, porder, sb, se, epath;
     DevBuf<uint64_t> ekeys, ekeys_out, pkeys, pkeys_out;
     DevBuf<char> cub;
     size_t cub_bytes = 0;
@@ -231,6 +348,7 @@ static ProjWS &workspace(const pf_instance *inst, cudaStream_t s) {
     ws->loads.alloc(I.E + 1);
     ws->over.alloc(I.E + 1);
     ws->viol.alloc(I.E + 1);
+    ws->dirty.alloc(I.E + 1);
     ws->order.alloc(I.P + 1);
     ws->bad.alloc(1);
     ws->nviol.alloc(1);
@@ -244,6 +362,9 @@ static ProjWS &workspace(const pf_instance *inst, cudaStream_t s) {
     ws->porder.alloc(I.NP + 1);
     ws->sb.alloc(I.E + 1);
     ws->se.alloc(I.E + 1);
+    ws->epath.alloc(I.NP + 1);  // path of each edge-major pair: pair_path[edge_pairs[t]]
+    if (I.NP) k_edge_paths<<<ceil_div(I.NP, 256), 256, 0, s>>>(I, ws->epath.p);
+    PF_CHECK_LAUNCH();
     std::vector<int32_t> eptr(I.E + 1);
     d2h(eptr.data(), I.edge_pair_ptr, I.E + 1, s);
     PF_CUDA(cudaStreamSynchronize(s));
@@ -256,6 +377,7 @@ static ProjWS &workspace(const pf_instance *inst, cudaStream_t s) {
                                                      ws->porder.p, I.NP, I.E, ws->sb.p, ws->se.p, 0, 64, s));
     ws->cub_bytes = std::max<size_t>(std::max(a, b), 16);
     ws->cub.alloc(ws->cub_bytes);
+    PF_CUDA(cudaFuncSetAttribute(k_edge_trim, cudaFuncAttributeMaxDynamicSharedMemorySize, TRIM_SMEM));
     inst->proj_ws = ws;
     return *ws;
 }
@@ -310,7 +432,10 @@ void project_device(const pf_instance *inst, const double *rates, int64_t alpha,
         PF_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(ws.cub.p, bytes, ws.pkeys.p, ws.pkeys_out.p, ws.pvals.p,
                                                          ws.porder.p, I.NP, I.E, ws.sb.p, ws.se.p, 0, 64, s));
     }
-    k_edge_trim<<<1, 1024, 0, s>>>(I, ws.eorder.p, ws.nviol.p, ws.porder.p, x, ws.parts.p);
+    static const int stats = getenv("PF_PROJ_STATS") ? 1 : 0;
+    PF_CUDA(cudaMemsetAsync(ws.dirty.p, 0, I.E + 1, s));
+    k_edge_trim<<<1, 1024, TRIM_SMEM, s>>>(I, ws.eorder.p, ws.nviol.p, ws.porder.p, ws.epath.p, x, ws.over.p, ws.dirty.p,
+                                   stats);
     PF_CHECK_LAUNCH();
     int32_t hb;
     d2h(&hb, ws.bad.p, 1, s);
