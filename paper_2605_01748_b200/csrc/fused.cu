@@ -143,7 +143,7 @@ __host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E, int nbuf)
 }
 
 struct TileLayout {
-    int32_t ntiles = 0, tps = TPS_MIN;
+    int32_t ntiles = 0, tps = TPS_MIN, kspan = 1;
     int64_t nslots = 0, meta_bytes = 0;
     DevBuf<TileDesc> desc;      // per tile
     DevBuf<uint8_t> meta;       // per-tile metadata blocks
@@ -161,7 +161,7 @@ struct Ctrl {
 
 struct Params {
     InstView I;
-    int32_t ntiles, G, nslices, tps, nbuf;
+    int32_t ntiles, G, nslices, tps, nbuf, kspan;  // kspan: power of two >= max paths per commodity
     const TileDesc *desc;
     const int32_t *cta_ptr, *cta_tiles;  // CTA g walks tiles cta_tiles[cta_ptr[g] .. cta_ptr[g + 1])
     const uint8_t *meta;
@@ -290,13 +290,65 @@ __device__ double block_sum(double v, double *red) {
 
 // Inclusive sum over the lane segment [first, lane] (Hillis-Steele, fixed tree),
 // then broadcast the segment total from lane `last`.
-__device__ __forceinline__ double seg_total(double v, int lane, int first, int last) {
+__device__ __forceinline__ double seg_total(double v, int lane, int first, int last, int span) {
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
+        if (o >= span) break;  // a commodity spans at most `span` lanes
         double t = __shfl_up_sync(FULL, v, o);
         if (lane - o >= first) v += t;
     }
     return __shfl_sync(FULL, v, last);
+}
+__device__ __forceinline__ void seg_total2(double &a, double &b, int lane, int first, int last, int span) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        if (o >= span) break;
+        const double ta = __shfl_up_sync(FULL, a, o);
+        const double tb = __shfl_up_sync(FULL, b, o);
+        if (lane - o >= first) {
+            a += ta;
+            b += tb;
+        }
+    }
+    a = __shfl_sync(FULL, a, last);
+    b = __shfl_sync(FULL, b, last);
+}
+
+// Correctly rounded 1/h for the path weights 1/hops and 1/(hops+1)
+// (kernels.py:115-119): a table of IEEE quotients is bitwise the division.
+constexpr int RCP_MAX = 64;
+__constant__ double c_rcp[RCP_MAX + 1];
+__device__ __forceinline__ double rcp_int(int h) { return h <= RCP_MAX ? c_rcp[h] : 1.0 / (double)h; }
+
+// kernels.py:134-173 with lin = 1: (q + c) / 1.0 is q + c exactly, and the
+// alpha = 1 quotient by 2.0 is an exact scaling; other cases as the reference.
+__device__ __forceinline__ double root_lin1(double c, double q, int64_t alpha) {
+    if (alpha == 0) return q + c;
+    if (alpha == 1) {
+        const double sq = sqrt(q * q + 4.0 * c);
+        if (q >= 0.0) return (q + sq) * 0.5;
+        return (2.0 * c) / (sq - q);
+    }
+    return root_newton(1.0, c, q, alpha);
+}
+// kernels.py:183-189 (commodity_root) using root_lin1 for the first root
+__device__ __forceinline__ double fast_commodity_root(double w, double q, double d_eff, double beta, int64_t alpha) {
+    const double cc = w / beta;
+    double s = root_lin1(cc, q, alpha);
+    if (s > d_eff) s = root_scalar(1.0 + w, cc, q + w * d_eff, alpha);
+    return s;
+}
+// kernels.py:289-294 with 1/beta hoisted for alpha = 0 (the same quotient)
+__device__ __forceinline__ double fast_commodity_term(double S, double D, double dd, double beta, double inv_beta,
+                                                      int64_t alpha) {
+    double gain;
+    if (alpha == 0)
+        gain = inv_beta;
+    else if (alpha == 1)
+        gain = (1.0 / S) / beta;
+    else
+        gain = pow(S, -(double)alpha) / beta;
+    return gain - npmax0(S - (D - dd));
 }
 
 // ------------------------------------------------------------------ controller
@@ -494,7 +546,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     const double *dcon = st.dcon;
     double *ys = A.y;
     const double f = io.f;
-    double *const dcon_out = io.dcon_out + d.sb;  // register copies: no reloads from shared memory
+    const double inv_beta = 1.0 / c.beta;
     double *const x_out = io.x_out, *const dn_out = io.dn_out, *const dd_out = io.dd_out;
 
     // ---- this warp's commodity group
@@ -538,28 +590,27 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
                 if (l < hi) K += ys[l] - dcon[l];
                 K += K1;
                 const double dnv = st.dn[p];
-                const double h = (double)(hi - lo);
                 if (xk < dnv) {  // frozen non-negativity activity (kernels.py:114-119)
                     K += dnv;
-                    wgt = 1.0 / (h + 1.0);
+                    wgt = rcp_int(hi - lo + 1);
                 } else {
-                    wgt = 1.0 / h;
+                    wgt = rcp_int(hi - lo);
                 }
             }
-            const double Wc = seg_total(wgt, lane, first, last);
-            const double Qc = seg_total(wgt * K, lane, first, last);
+            double Wc = wgt, Qc = wgt * K;
+            seg_total2(Wc, Qc, lane, first, last, P.kspan);
             double ct = NAN;
             if (valid) {
                 if (!(isfinite(Wc) && isfinite(Qc))) {
                     if (head) atomicMin(&P.err[0], cc);
                 } else {
                     const double D = st.D[j], ddk = st.dd[j];
-                    const double Sc = commodity_root(Wc, Qc, D - ddk, c.beta, c.alpha);
+                    const double Sc = fast_commodity_root(Wc, Qc, D - ddk, c.beta, c.alpha);
                     if (head) {
                         if (!isfinite(Sc)) atomicMin(&P.err[1], cc);
                         if (P.root_sums) P.root_sums[cc] = Sc;
                     }
-                    ct = commodity_term(Sc, D, ddk, c.beta, c.alpha);
+                    ct = fast_commodity_term(Sc, D, ddk, c.beta, inv_beta, c.alpha);
                 }
                 xv = wgt * (K + ct);
                 x_out[d.p0 + p] = xv;
@@ -576,7 +627,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
             r_dn += dg * dg;
         }
         // S_c (model.py:297-302) and dual_demand (kernels.py:211)
-        const double Sx = seg_total(valid ? xv : 0.0, lane, first, last);
+        const double Sx = seg_total(valid ? xv : 0.0, lane, first, last, P.kspan);
         if (head) {
             const double dold = st.dd[j] * f;
             const double dnew = npmax0(dold + (Sx - st.D[j]));
@@ -619,7 +670,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
         const double dks = dcon[pl] * f;
         const double yv = ys[pl];
         const double dnew = max0(dks + xn - yv);
-        dcon_out[pl] = dnew;
+        ys[pl] = dnew;  // y of this pair is consumed: its slot takes dcon' (copied out coalesced)
         const double df = dnew - dks;
         r_dcon += df * df;
         T += xn + dnew;
@@ -833,6 +884,15 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
             cs.sd[0] = P.desc[tile_of(k + 1)];
             issue_tile<MODE>(P, io, cs.sd[0], base, sp, 0, &cs.bar[0]);
         }
+        {  // dcon' of the tile (left in the y slots by the scan): coalesced 16-byte stores,
+           // overlapping the next tile's bulk copy
+            const double2 *src = (const double2 *)A.y;
+            double2 *dst = (double2 *)(io.dcon_out + d.sb);
+            const int n2 = d.np >> 1;
+            for (int i = tid; i < n2; i += NT) dst[i] = src[i];
+            if ((d.np & 1) && tid == 0) io.dcon_out[d.sb + d.np - 1] = A.y[d.np - 1];
+        }
+        __syncthreads();  // the y slots are free for the next tile
     }
     __syncthreads();  // last tile's fix-ups
     for (int e = tid; e < E; e += NT) {
@@ -1086,6 +1146,13 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         const int64_t budget = per_sm / 2 - reserved - 1024;
         while (tps_min > 1024 && smem_plan((int)tps_min, (int)I.E, 1).total > budget) tps_min -= 256;
     }
+    {  // small instances: smaller tiles so that the tiles fill the grid (per-tile latency
+       // bounds an iteration when every CTA holds one tile)
+        int sms = 148;
+        PF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, inst->device()));
+        const int64_t fill = (I.NP / (2 * (int64_t)sms) + 63) / 64 * 64;
+        tps_min = std::min<int64_t>(tps_min, std::max<int64_t>(256, fill));
+    }
     if (const char *v = getenv("PF_FAST_TPS")) tps_min = std::max(256, atoi(v)) / 64 * 64;
     const int64_t tps = std::max<int64_t>(tps_min, (max_com_pairs + 63) / 64 * 64);
     require(tps <= 16384, "a commodity has too many demand-path pairs for a fast-mode tile");
@@ -1094,6 +1161,7 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
     // (k = 8, 9.2 hops: 3 commodities = 24 paths = ~220 pairs per warp)
     int64_t max_paths = 1;
     for (int64_t c = 0; c < I.C; ++c) max_paths = std::max<int64_t>(max_paths, cpp[c + 1] - cpp[c]);
+    while (L->kspan < max_paths) L->kspan <<= 1;
     const double mean_hops = I.P ? (double)I.NP / (double)I.P : 1.0;
     const int64_t gmax = std::min<int64_t>(GPATH, std::max<int64_t>(max_paths, (int64_t)(tps / (NW * mean_hops * 1.08))));
     // groups
@@ -1315,6 +1383,13 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     P.nslices = F->nslices;
     P.tps = F->L->tps;
     P.nbuf = F->nbuf;
+    P.kspan = F->L->kspan;
+    {
+        double rcp[RCP_MAX + 1];
+        rcp[0] = 0.0;
+        for (int h = 1; h <= RCP_MAX; ++h) rcp[h] = 1.0 / (double)h;  // correctly rounded (IEEE division)
+        PF_CUDA(cudaMemcpyToSymbolAsync(c_rcp, rcp, sizeof(rcp), 0, cudaMemcpyHostToDevice, s));
+    }
     P.desc = F->L->desc.p;
     P.cta_ptr = F->cta_ptr.p;
     P.cta_tiles = F->cta_tiles.p;
