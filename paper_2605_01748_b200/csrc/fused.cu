@@ -1032,8 +1032,11 @@ __global__ void k_local_reduce(const __grid_constant__ Params P) {
     }
 }
 
-// controller step from the allreduced totals (one thread)
-__global__ void k_ctrl_dist(const __grid_constant__ Params P) {
+// controller step from the allreduced totals (one thread).  Inside the
+// per-run CUDA graph it also sets the graph's conditions: run the rollback
+// branch, continue the iteration loop.
+__global__ void k_ctrl_dist(const __grid_constant__ Params P, cudaGraphConditionalHandle h_loop,
+                            cudaGraphConditionalHandle h_rb, int in_graph) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     Ctrl c = *P.ctrl;
     c.iteration += 1;
@@ -1052,6 +1055,11 @@ __global__ void k_ctrl_dist(const __grid_constant__ Params P) {
     controller_step(P, c, sqrt(t[0]), sqrt(((t[1 + 3 * par] + dcs) + t[2 + 3 * par]) + t[3 + 3 * par]), ec, er);
     c.need_edge = 1;
     *P.ctrl = c;
+    if (in_graph) {
+        const bool live = !c.stopped && !c.status;
+        cudaGraphSetConditional(h_rb, live && c.f != 1.0 ? 1u : 0u);
+        cudaGraphSetConditional(h_loop, live && c.iteration < c.target && c.iteration < P.max_iterations ? 1u : 0u);
+    }
 }
 
 // kernels.py:212 and :94-96 from the allreduced per-edge totals (one warp per 32 edges)
@@ -1292,6 +1300,10 @@ struct FastSolver {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     int64_t launches = 0;
     const CommOps *comm = nullptr;
+    // multi-GPU: one CUDA graph per run (WHILE over the iteration body, IF for the rollback)
+    cudaGraph_t dgraph = nullptr;
+    cudaGraphExec_t dexec = nullptr;
+    int dgraph_state = 0;  // 0 untried, 1 built, -1 unavailable (host-driven loop)
 };
 
 FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStream_t s) {
@@ -1430,6 +1442,8 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
 
 void fast_destroy(FastSolver *F) {
     if (!F) return;
+    if (F->dexec) cudaGraphExecDestroy(F->dexec);
+    if (F->dgraph) cudaGraphDestroy(F->dgraph);
     if (F->e0) cudaEventDestroy(F->e0);
     if (F->e1) cudaEventDestroy(F->e1);
     delete F;
@@ -1447,7 +1461,84 @@ void fast_set_comm(FastSolver *F, const CommOps *ops) {
     PF_CUDA(cudaStreamDestroy(s));
 }
 
-// Host-driven iteration for sharded solves (see the split kernels above).
+// The iteration loop of a sharded solve as ONE CUDA graph:
+//   WHILE (continue) {
+//     k_edge_dist -> k_ctrl_update -> k_pass<M> -> k_local_reduce -> ncclAllReduce -> k_ctrl_dist
+//     IF (beta changed) { k_pass<RB> -> k_local_reduce -> ncclAllReduce }
+//   }
+// k_ctrl_dist sets both conditions on the device, so a run of iterations has no
+// host round trip (every rank evaluates the same controller on the same totals,
+// so all ranks take the same branches and issue matching collectives).
+static bool build_dist_graph(FastSolver *F, cudaStream_t s) {
+    const Index &I = *F->inst->idx;
+    const int64_t E = I.E;
+    const int nred = (int)std::max<int64_t>(1, (E + 255) / 256);
+    const int ngroups = (int)((E + RGRP - 1) / RGRP);
+    auto ok = [](cudaError_t e) { return e == cudaSuccess; };
+    cudaGraph_t top = nullptr;
+    if (!ok(cudaGraphCreate(&top, 0))) return false;
+    bool good = false;
+    do {
+        cudaGraphConditionalHandle h_loop, h_rb;
+        if (!ok(cudaGraphConditionalHandleCreate(&h_loop, top, 1, cudaGraphCondAssignDefault))) break;
+        cudaGraphNodeParams wp = {cudaGraphNodeTypeConditional};
+        wp.conditional.handle = h_loop;
+        wp.conditional.type = cudaGraphCondTypeWhile;
+        wp.conditional.size = 1;
+        cudaGraphNode_t wnode;
+        if (!ok(cudaGraphAddNode(&wnode, top, nullptr, 0, &wp))) break;
+        cudaGraph_t body = wp.conditional.phGraph_out[0];
+        if (!ok(cudaGraphConditionalHandleCreate(&h_rb, body, 0, cudaGraphCondAssignDefault))) break;
+        if (!ok(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed))) break;
+        // (k_ctrl_update is not needed inside the loop: the M pass speculates f = 1
+        // itself and k_ctrl_dist rewrites f and need_edge)
+        if (ngroups) k_edge_dist<<<ngroups, RGRP, 0, s>>>(F->P);
+        k_pass<MODE_M><<<F->G, NT, F->smem, s>>>(F->P);
+        k_local_reduce<<<nred, 256, 0, s>>>(F->P);
+        F->comm->allreduce_sum(F->comm->ctx, F->tot.p, 2 * E + 16, s);
+        k_ctrl_dist<<<1, 32, 0, s>>>(F->P, h_loop, h_rb, 1);
+        cudaStreamCaptureStatus cst;
+        cudaGraph_t capg = nullptr;
+        const cudaGraphNode_t *deps = nullptr;
+        size_t ndeps = 0;
+        bool cap_ok = ok(cudaStreamGetCaptureInfo(s, &cst, nullptr, &capg, &deps, &ndeps));
+        cudaGraphNodeParams ip = {cudaGraphNodeTypeConditional};
+        ip.conditional.handle = h_rb;
+        ip.conditional.type = cudaGraphCondTypeIf;
+        ip.conditional.size = 1;
+        cudaGraphNode_t inode = nullptr;
+        if (cap_ok) cap_ok = ok(cudaGraphAddNode(&inode, capg, deps, ndeps, &ip));
+        if (cap_ok) cap_ok = ok(cudaStreamUpdateCaptureDependencies(s, &inode, 1, cudaStreamSetCaptureDependencies));
+        cudaGraph_t tmp = nullptr;
+        if (!ok(cudaStreamEndCapture(s, &tmp)) || !cap_ok) break;
+        cudaGraph_t rbody = ip.conditional.phGraph_out[0];
+        if (!ok(cudaStreamBeginCaptureToGraph(s, rbody, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed))) break;
+        k_pass<MODE_RB><<<F->G, NT, F->smem, s>>>(F->P);
+        k_local_reduce<<<nred, 256, 0, s>>>(F->P);
+        F->comm->allreduce_sum(F->comm->ctx, F->tot.p, 2 * E + 16, s);
+        if (!ok(cudaStreamEndCapture(s, &tmp))) break;
+        if (!ok(cudaGraphInstantiate(&F->dexec, top, 0))) break;
+        good = true;
+    } while (false);
+    if (!good) {
+        cudaGetLastError();  // clear a sticky-free capture / instantiate error
+        cudaStreamCaptureStatus cst;
+        if (cudaStreamIsCapturing(s, &cst) == cudaSuccess && cst != cudaStreamCaptureStatusNone) {
+            cudaGraph_t tmp = nullptr;
+            cudaStreamEndCapture(s, &tmp);
+            if (tmp) cudaGraphDestroy(tmp);
+        }
+        cudaGetLastError();
+        cudaGraphDestroy(top);
+        F->dexec = nullptr;
+        return false;
+    }
+    F->dgraph = top;
+    return true;
+}
+
+// Host-driven iteration for sharded solves (see the split kernels above); the
+// iteration loop itself runs as the per-run CUDA graph when it could be built.
 static int64_t fast_run_dist(FastSolver *F, int64_t max_steps, cudaStream_t s, float *ms) {
     const Index &I = *F->inst->idx;
     const int64_t E = I.E;
@@ -1480,6 +1571,17 @@ static int64_t fast_run_dist(FastSolver *F, int64_t max_steps, cudaStream_t s, f
         F->launches += 3;
         c = read();
     }
+    if (F->dgraph_state == 0) {
+        const bool off = getenv("PF_DIST_NO_GRAPH") != nullptr;
+        F->dgraph_state = !off && build_dist_graph(F, s) ? 1 : -1;
+    }
+    if (F->dgraph_state == 1 && !c.stopped && !c.status && c.iteration < target && c.need_edge) {
+        PF_CUDA(cudaMemcpyAsync((char *)F->ctrl.p + offsetof(Ctrl, target), &target, sizeof(int64_t),
+                                cudaMemcpyHostToDevice, s));
+        PF_CUDA(cudaGraphLaunch(F->dexec, s));
+        F->launches += 1;
+        c = read();
+    }
     while (!c.stopped && !c.status && c.iteration < target) {
         if (c.need_edge) {
             if (ngroups) k_edge_dist<<<ngroups, RGRP, 0, s>>>(F->P);
@@ -1488,7 +1590,7 @@ static int64_t fast_run_dist(FastSolver *F, int64_t max_steps, cudaStream_t s, f
         k_pass<MODE_M><<<F->G, NT, F->smem, s>>>(F->P);
         PF_CHECK_LAUNCH();
         reduce_allreduce();
-        k_ctrl_dist<<<1, 32, 0, s>>>(F->P);
+        k_ctrl_dist<<<1, 32, 0, s>>>(F->P, 0, 0, 0);
         PF_CHECK_LAUNCH();
         F->launches += 5;
         c = read();

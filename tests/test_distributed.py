@@ -139,3 +139,38 @@ def test_nccl_world1_matches_single_gpu():
                                    atol=1e-4 * float(single.sums.max()))
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_nccl_world1_graph_loop_matches_host_loop(monkeypatch):
+    """The sharded iteration loop runs as one CUDA graph (WHILE over the body,
+    IF for the rollback branch, conditions set on the device); it must take the
+    same branches and produce bitwise the same iterates as the host-driven loop
+    over 300 iterations that include beta changes (rollback passes)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.distributed as dist
+
+    import paper_2605_01748_b200 as pf
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1)
+    try:
+        topo = pf.random_topology(40, seed=40)
+        tab = pf.gravity_table(topo, 0.3 * float(topo.capacity.sum()))
+        flat = pf.k_shortest_paths(topo, tab, 4)
+        cfg = pf.SolverConfig(mode="fast", max_iterations=5000, gamma=1e-12)
+        runs = {}
+        for mode in ("graph", "host"):
+            if mode == "host":
+                monkeypatch.setenv("PF_DIST_NO_GRAPH", "1")
+            sh = D.ShardedSolver(topo, tab, flat, cfg, 0, 1, 0).init()
+            sh.run(120)
+            sh.run(180)  # two runs: the graph is relaunched with a new target
+            r = sh.result()
+            runs[mode] = (sh.local_x(), int(r.iterations), float(r.beta), int(sh.solver.kernel_stats()["launches"]))
+        (xg, ig, bg, lg), (xh, ih, bh, lh) = runs["graph"], runs["host"]
+        assert ig == ih == 300 and bg == bh
+        assert np.array_equal(xg, xh)
+        assert lg < 20 < lh  # the graph replaced ~5 launches per iteration
+    finally:
+        dist.destroy_process_group()
