@@ -81,7 +81,7 @@ __host__ __device__ __forceinline__ int even(int n) { return (n + 1) & ~1; }
 
 // Byte offsets of the sections of one tile's metadata block.
 struct MetaOff {
-    int eid, spath, skp, sspath, poff, pcom, cpp, gpath, bytes;
+    int eid, spath, skp, poff, pcom, cpp, gpath, bytes;
 };
 __host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc) {
     MetaOff m;
@@ -92,8 +92,6 @@ __host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc) 
     o += r16(np);
     m.skp = o;  // u32 [np] (edge << 16) | tile-local pair, for the edge-sorted slots (stable by pair)
     o += r16(4 * np);
-    m.sspath = o;  // u8 [np] tile-local path of each edge-sorted slot (= spath[perm[s]])
-    o += r16(np);
     m.poff = o;  // u16 [npath + 1] tile-local pair offset of each path
     o += r16(2 * (npath + 1));
     m.pcom = o;  // u8 [npath] tile-local commodity of each path
@@ -109,7 +107,7 @@ __host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc) 
 // Dynamic shared memory: two stages + work arrays + the per-edge tables.
 struct SmemPlan {
     int stage, s_dcon, s_meta, s_xk, s_xo, s_dn, s_D, s_dd;  // offsets inside a stage
-    int y, xn, adj, acc, total;                             // offsets from the base
+    int y, adj, acc, total;                                 // offsets from the base
 };
 __host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E, int nbuf) {
     SmemPlan s;
@@ -132,8 +130,6 @@ __host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E, int nbuf)
     o = nbuf * s.stage;
     s.y = o;
     o += 8 * tps;
-    s.xn = o;
-    o += 8 * TPATH;
     s.adj = o;
     o += r16(8 * E);
     s.acc = o;  // double2 {T, L} per edge
@@ -219,6 +215,9 @@ __device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes) {
 }
 // order this thread's generic-proxy accesses before later async-proxy (TMA) ones
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_shared() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
 
 enum { MODE_M = 0, MODE_RB = 1, MODE_A1 = 2 };
 
@@ -509,7 +508,7 @@ struct Tail {
 };
 
 struct Acc {
-    double *adj, *y, *xn;
+    double *adj, *y;
     double2 *acc;  // per edge {T, L}
 };
 
@@ -526,6 +525,60 @@ struct Fix {
     int key, w;
     double T, L;
 };
+
+// The per-pair loops as functions with __restrict__ operands: the shared-memory
+// arrays a loop stores to never alias the ones it loads from, so the compiler
+// may overlap the dependent loads of consecutive iterations.
+template <int MODE>
+__device__ __forceinline__ void pairs_y(int l0, int l1, int gp0, int lane, double xlane,
+                                        const uint8_t *__restrict__ spath, const uint16_t *__restrict__ eid,
+                                        const double *__restrict__ dcon, const double *__restrict__ adj,
+                                        double *__restrict__ ys) {
+#pragma unroll 4
+    for (int base = l0; base < l1; base += 32) {
+        const int l = base + lane;
+        const int i = l < l1 ? (int)spath[l] - gp0 : 0;
+        const double xp = __shfl_sync(FULL, xlane, i);
+        if (l < l1) ys[l] = MODE == MODE_A1 ? xp : max0(xp + dcon[l] - adj[eid[l]]);
+    }
+}
+
+// dual_consensus' (kernels.py:72) stored coalesced to global; T = x' + dcon'
+// (kernels.py:91) into tv
+__device__ __forceinline__ double pairs_dcon(int l0, int l1, int gp0, int lane, double xlane, double f,
+                                             const uint8_t *__restrict__ spath, const double *__restrict__ dcon,
+                                             const double *__restrict__ ys, double *__restrict__ dco,
+                                             double *__restrict__ tv) {
+    double r = 0.0;
+#pragma unroll 4
+    for (int base = l0; base < l1; base += 32) {
+        const int l = base + lane;
+        const int i = l < l1 ? (int)spath[l] - gp0 : 0;
+        const double xn = __shfl_sync(FULL, xlane, i);
+        if (l < l1) {
+            const double dks = dcon[l] * f;
+            const double dnew = max0(dks + xn - ys[l]);
+            dco[l] = dnew;
+            const double df = dnew - dks;
+            r += df * df;
+            tv[l] = xn + dnew;
+        }
+    }
+    return r;
+}
+
+// K_p over the path's pairs (two chains, fixed association)
+__device__ __forceinline__ double path_k(int lo, int hi, const double *__restrict__ ys,
+                                         const double *__restrict__ dcon) {
+    double K = 0.0, K1 = 0.0;
+    int l = lo;
+    for (; l + 1 < hi; l += 2) {
+        K += ys[l] - dcon[l];
+        K1 += ys[l + 1] - dcon[l + 1];
+    }
+    if (l < hi) K += ys[l] - dcon[l];
+    return K + K1;
+}
 
 // MODE_M : B(k+1) [y, K/w, roots, x_{k+1}] fused with A(k+2) [duals_{k+2}, T/L]
 // MODE_RB: A(k+2) only, recomputing y_{k+1} from x_k, dcon_{k+1}, adj_{k+1}
@@ -555,15 +608,10 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     if (!(P.ablate & 1)) {
     // (1) pairs: y (kernels.py:98-100); the path's rate comes from its lane
     const double xlane = gp0 + lane < gp1 ? (MODE == MODE_RB ? st.xo[gp0 + lane] : st.xk[gp0 + lane]) : 0.0;
-#pragma unroll 4
-    for (int base = l0; base < l1; base += 32) {
-        const int l = base + lane;
-        const int i = l < l1 ? (int)spath[l] - gp0 : 0;
-        const double xp = __shfl_sync(FULL, xlane, i);
-        if (l < l1) ys[l] = MODE == MODE_A1 ? xp : max0(xp + dcon[l] - A.adj[eid[l]]);
-    }
+    pairs_y<MODE>(l0, l1, gp0, lane, xlane, spath, eid, dcon, A.adj, ys);
     __syncwarp();
     // (2) paths (lane = path) and commodities (lane segments)
+    double xnew_lane = 0.0;  // x' of this lane's path
     {
         const int p = gp0 + lane;
         const bool valid = p < gp1;
@@ -577,18 +625,11 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
         const int cc = d.c0 + j;
         const double xk = valid ? st.xk[p] : 0.0;
         double xv = xk;
-        if (MODE == MODE_M) {
+        if (MODE == MODE_M && !(P.ablate & 16)) {
             double K = 0.0, wgt = 0.0;
             if (valid) {
                 const int lo = poff[p], hi = poff[p + 1];
-                double K1 = 0.0;  // two chains (fixed association)
-                int l = lo;
-                for (; l + 1 < hi; l += 2) {
-                    K += ys[l] - dcon[l];
-                    K1 += ys[l + 1] - dcon[l + 1];
-                }
-                if (l < hi) K += ys[l] - dcon[l];
-                K += K1;
+                K = path_k(lo, hi, ys, dcon);
                 const double dnv = st.dn[p];
                 if (xk < dnv) {  // frozen non-negativity activity (kernels.py:114-119)
                     K += dnv;
@@ -619,7 +660,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
             }
         }
         if (valid) {
-            A.xn[p] = xv;
+            xnew_lane = xv;
             const double o = st.dn[p] * f;
             const double n = npmax0(o - xv);
             dn_out[d.p0 + p] = n;
@@ -637,13 +678,19 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
         }
     }
     __syncwarp();
+    // (3) pairs in path order: dual_consensus' (kernels.py:72) stored coalesced;
+    // T = x' + dcon' (kernels.py:91) replaces the consumed dcon in the stage
+    // (tv aliases dcon on purpose: every iteration reads dcon[l] before it
+    // writes tv[l], for the same l only)
+    r_dcon += pairs_dcon(l0, l1, gp0, lane, xnew_lane, f, spath, dcon, ys, io.dcon_out + d.sb,
+                         const_cast<double *>(dcon));
+    fence_proxy_async_shared();  // these generic writes precede the TMA that refills the stage
     __syncthreads();
 
     }
     if (P.ablate & 2) return;
-    // (3) pairs in edge-sorted order: dual_consensus (kernels.py:72) and the
-    // per-edge sums T = sum (x + dcon') (kernels.py:91) and L = sum y
-    // (kernels.py:210).  Warp w owns sorted slots [s0, s1), lane `lane` the
+    // (4) pairs in edge-sorted order: the per-edge sums T = sum (x' + dcon')
+    // (kernels.py:91) and L = sum y (kernels.py:210).  Warp w owns sorted slots [s0, s1), lane `lane` the
     // consecutive items [a, b): a sequential segmented sum per lane, one warp
     // scan of the lane aggregates, then the run totals go to the CTA
     // accumulators (a run never repeats an edge within a tile: no conflicts).
@@ -654,7 +701,6 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     const int IT = (s1 - s0 + 31) >> 5;
     const int a = min(s0 + lane * IT, s1), b = min(a + IT, s1);
     const uint32_t *skp = (const uint32_t *)(st.meta + m.skp);
-    const uint8_t *sspath = st.meta + m.sspath;
     const int kbefore = a > 0 ? (int)(skp[a - 1] >> 16) : -1;
     // one sequential pass per lane: the lane's prefix (items continuing the run
     // open at item a) is summed first; runs that start inside the lane are added
@@ -666,15 +712,8 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     uint32_t kp = s < b ? skp[s] : 0u;  // (edge << 16) | pair of the current item
     auto item = [&](uint32_t kpv, int s_, double &T, double &L) {
         const int pl = (int)(kpv & 0xffffu);
-        const double xn = A.xn[sspath[s_]];
-        const double dks = dcon[pl] * f;
-        const double yv = ys[pl];
-        const double dnew = max0(dks + xn - yv);
-        ys[pl] = dnew;  // y of this pair is consumed: its slot takes dcon' (copied out coalesced)
-        const double df = dnew - dks;
-        r_dcon += df * df;
-        T += xn + dnew;
-        if (MODE != MODE_RB) L += yv;
+        T += dcon[pl];  // x' + dcon' (written by step 3)
+        if (MODE != MODE_RB) L += ys[pl];
     };
     while (s < b && (int)(kp >> 16) == kbefore) {
         const uint32_t cur = kp;
@@ -836,7 +875,6 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
     A.adj = (double *)(base + sp.adj);
     A.acc = (double2 *)(base + sp.acc);
     A.y = (double *)(base + sp.y);
-    A.xn = (double *)(base + sp.xn);
     const int t0 = P.cta_ptr[g], my = P.cta_ptr[g + 1] - t0;
     const bool rev = (c.iteration & 1) != 0;
     auto tile_of = [&](int k) { return P.cta_tiles[t0 + (rev ? my - 1 - k : k)]; };
@@ -878,21 +916,12 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
         const TileDesc d = cs.sd[b];
         const StageView st = stage_view(base, sp, b, d);
         tile_compute<MODE>(P, c, io, d, st, A, cs.tails, fx, r_x, r_dd, r_dcon, r_dn);
-        __syncthreads();  // stage b is only read by generic accesses; free for the next TMA into it
+        __syncthreads();  // the stage is free for the next TMA (its generic writes were proxy-fenced)
         apply_fix<MODE>(fx, cs.tails, A);
         if (!dbl && tid == 0 && k + 1 < my) {
             cs.sd[0] = P.desc[tile_of(k + 1)];
             issue_tile<MODE>(P, io, cs.sd[0], base, sp, 0, &cs.bar[0]);
         }
-        {  // dcon' of the tile (left in the y slots by the scan): coalesced 16-byte stores,
-           // overlapping the next tile's bulk copy
-            const double2 *src = (const double2 *)A.y;
-            double2 *dst = (double2 *)(io.dcon_out + d.sb);
-            const int n2 = d.np >> 1;
-            for (int i = tid; i < n2; i += NT) dst[i] = src[i];
-            if ((d.np & 1) && tid == 0) io.dcon_out[d.sb + d.np - 1] = A.y[d.np - 1];
-        }
-        __syncthreads();  // the y slots are free for the next tile
     }
     __syncthreads();  // last tile's fix-ups
     for (int e = tid; e < E; e += NT) {
@@ -1249,7 +1278,6 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         }
         std::stable_sort(perm.begin(), perm.end(), [&](uint16_t a, uint16_t b) { return eid[a] < eid[b]; });
         uint32_t *skp = (uint32_t *)(blk + m.skp);
-        uint8_t *sspath = blk + m.sspath;
         for (int i = 0; i < npath; ++i) {
             poff[i] = (uint16_t)(pptr[T.p0 + i] - T.t0);
             for (int32_t t = pptr[T.p0 + i]; t < pptr[T.p0 + i + 1]; ++t) spath[t - T.t0] = (uint8_t)i;
@@ -1257,7 +1285,6 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         poff[npath] = (uint16_t)np;
         for (int sl = 0; sl < np; ++sl) {
             skp[sl] = ((uint32_t)eid[perm[sl]] << 16) | perm[sl];
-            sspath[sl] = spath[perm[sl]];
         }
         for (int j = 0; j < nc; ++j) {
             lcpp[j] = (uint16_t)(cpp[T.c0 + j] - T.p0);
