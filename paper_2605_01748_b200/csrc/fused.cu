@@ -109,7 +109,7 @@ struct SmemPlan {
     int stage, s_dcon, s_meta, s_xk, s_xo, s_dn, s_D, s_dd;  // offsets inside a stage
     int y, adj, acc, total;                                 // offsets from the base
 };
-__host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E, int nbuf) {
+__host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E, int nbuf, bool adj_smem = true) {
     SmemPlan s;
     int o = 0;
     s.s_dcon = o;
@@ -130,8 +130,8 @@ __host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E, int nbuf)
     o = nbuf * s.stage;
     s.y = o;
     o += 8 * tps;
-    s.adj = o;
-    o += r16(8 * E);
+    s.adj = o;  // per-edge adjustment table (absent for large E: read through L1)
+    if (adj_smem) o += r16(8 * E);
     s.acc = o;  // double2 {T, L} per edge
     o += r16(16 * E);
     s.total = o;
@@ -140,6 +140,7 @@ __host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E, int nbuf)
 
 struct TileLayout {
     int32_t ntiles = 0, tps = TPS_MIN, kspan = 1;
+    bool adj_smem = true;  // false for large E: one CTA per SM, the adjustment table read through L1
     int64_t nslots = 0, meta_bytes = 0;
     DevBuf<TileDesc> desc;      // per tile
     DevBuf<uint8_t> meta;       // per-tile metadata blocks
@@ -158,6 +159,7 @@ struct Ctrl {
 struct Params {
     InstView I;
     int32_t ntiles, G, nslices, tps, nbuf, kspan;  // kspan: power of two >= max paths per commodity
+    int32_t adj_smem;                               // adjustment table in shared memory (else L1)
     const TileDesc *desc;
     const int32_t *cta_ptr, *cta_tiles;  // CTA g walks tiles cta_tiles[cta_ptr[g] .. cta_ptr[g + 1])
     const uint8_t *meta;
@@ -533,13 +535,13 @@ template <int MODE>
 __device__ __forceinline__ void pairs_y(int l0, int l1, int gp0, int lane, double xlane,
                                         const uint8_t *__restrict__ spath, const uint16_t *__restrict__ eid,
                                         const double *__restrict__ dcon, const double *__restrict__ adj,
-                                        double *__restrict__ ys) {
+                                        bool adj_l1, double *__restrict__ ys) {
 #pragma unroll 4
     for (int base = l0; base < l1; base += 32) {
         const int l = base + lane;
         const int i = l < l1 ? (int)spath[l] - gp0 : 0;
         const double xp = __shfl_sync(FULL, xlane, i);
-        if (l < l1) ys[l] = MODE == MODE_A1 ? xp : max0(xp + dcon[l] - adj[eid[l]]);
+        if (l < l1) ys[l] = MODE == MODE_A1 ? xp : max0(xp + dcon[l] - (adj_l1 ? __ldca(&adj[eid[l]]) : adj[eid[l]]));
     }
 }
 
@@ -608,7 +610,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     if (!(P.ablate & 1)) {
     // (1) pairs: y (kernels.py:98-100); the path's rate comes from its lane
     const double xlane = gp0 + lane < gp1 ? (MODE == MODE_RB ? st.xo[gp0 + lane] : st.xk[gp0 + lane]) : 0.0;
-    pairs_y<MODE>(l0, l1, gp0, lane, xlane, spath, eid, dcon, A.adj, ys);
+    pairs_y<MODE>(l0, l1, gp0, lane, xlane, spath, eid, dcon, A.adj, !P.adj_smem, ys);
     __syncwarp();
     // (2) paths (lane = path) and commodities (lane segments)
     double xnew_lane = 0.0;  // x' of this lane's path
@@ -870,9 +872,9 @@ template <int MODE>
 __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *base, CtaShared &cs, uint32_t &seq) {
     const int g = blockIdx.x, tid = threadIdx.x;
     const int E = P.I.E;
-    const SmemPlan sp = smem_plan(P.tps, E, P.nbuf);
+    const SmemPlan sp = smem_plan(P.tps, E, P.nbuf, P.adj_smem);
     Acc A;
-    A.adj = (double *)(base + sp.adj);
+    A.adj = P.adj_smem ? (double *)(base + sp.adj) : P.adj;
     A.acc = (double2 *)(base + sp.acc);
     A.y = (double *)(base + sp.y);
     const int t0 = P.cta_ptr[g], my = P.cta_ptr[g + 1] - t0;
@@ -890,8 +892,12 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
     }
     for (int e = tid; e < E; e += NT) {
         A.acc[e] = make_double2(0.0, 0.0);
-        A.adj[e] = MODE == MODE_A1 ? 0.0 : __ldcg(&P.adj[e]);
+        if (P.adj_smem) A.adj[e] = MODE == MODE_A1 ? 0.0 : __ldcg(&P.adj[e]);
     }
+    // without the shared table adj is read through L1 (ld.global.ca); it was
+    // rewritten by the edge phase before the grid barrier: acquire at gpu scope
+    // so no stale L1 line survives
+    if (!P.adj_smem) asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
     __syncthreads();
     const PassIO &io = cs.io;
     double r_x = 0.0, r_dd = 0.0, r_dcon = 0.0, r_dn = 0.0;
@@ -1181,7 +1187,15 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         PF_CUDA(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, inst->device()));
         PF_CUDA(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, inst->device()));
         const int64_t budget = per_sm / 2 - reserved - 1024;
-        while (tps_min > 1024 && smem_plan((int)tps_min, (int)I.E, 1).total > budget) tps_min -= 256;
+        if (smem_plan(1024, (int)I.E, 1).total > budget || getenv("PF_FAST_LARGE_E")) {
+            // large E: the per-edge tables rule out two CTAs per SM; run one CTA per
+            // SM with large tiles and the adjustment table read through L1
+            L->adj_smem = false;
+            const int64_t budget1 = per_sm - reserved - 1024;
+            while (tps_min > 512 && smem_plan((int)tps_min, (int)I.E, 1, false).total > budget1) tps_min -= 256;
+        } else {
+            while (tps_min > 1024 && smem_plan((int)tps_min, (int)I.E, 1).total > budget) tps_min -= 256;
+        }
     }
     {  // small instances: smaller tiles so that the tiles fill the grid (per-tile latency
        // bounds an iteration when every CTA holds one tile)
@@ -1345,7 +1359,7 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     }
     F->nbuf = 1;  // measured: a second stage costs an SM's second CTA, which hides more
     if (const char *v = getenv("PF_FAST_NBUF")) F->nbuf = std::max(1, std::min(2, atoi(v)));
-    F->smem = (size_t)smem_plan(F->L->tps, (int)I.E, F->nbuf).total;
+    F->smem = (size_t)smem_plan(F->L->tps, (int)I.E, F->nbuf, F->L->adj_smem).total;
     int dev = inst->device();
     cudaDeviceProp prop;
     PF_CUDA(cudaGetDeviceProperties(&prop, dev));
@@ -1423,6 +1437,7 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     P.tps = F->L->tps;
     P.nbuf = F->nbuf;
     P.kspan = F->L->kspan;
+    P.adj_smem = F->L->adj_smem ? 1 : 0;
     {
         double rcp[RCP_MAX + 1];
         rcp[0] = 0.0;
