@@ -161,7 +161,7 @@ static void solver_trace_row(pf_solver *S, const double *d_x, const double *d_ro
     row.optimality = NAN;
     if (!S->ref_sums.empty()) {
         DevBuf<double> proj(S->P()), sums(S->C() + 1);
-        project_device(S->inst, d_x, alpha, proj.p, S->stream);
+        project_device(S->inst, d_x, alpha, proj.p, S->stream, S->cfg.mode == PF_MODE_FAST);
         exact_commodity_sums(I, proj.p, sums.p, S->stream);
         std::vector<double> hs(S->C());
         d2h(hs.data(), sums.p, S->C(), S->stream);
@@ -398,7 +398,8 @@ static void solver_finish(pf_solver *S, double *rates, double *sums) {
     if (S->sums_out.n < (size_t)S->C() + 1) S->sums_out.alloc(S->C() + 1);
     PF_CUDA(cudaEventRecord(S->ev0, st));
     if (S->cfg.project)
-        project_device(S->inst, solver_x(S), alpha, S->rates_out.p, st);  // controller.py:275
+        project_device(S->inst, solver_x(S), alpha, S->rates_out.p, st,
+                       S->cfg.mode == PF_MODE_FAST);  // controller.py:275
     else
         PF_CUDA(cudaMemcpyAsync(S->rates_out.p, solver_x(S), sizeof(double) * S->P(), cudaMemcpyDeviceToDevice, st));
     exact_commodity_sums(I, S->rates_out.p, S->sums_out.p, st);

@@ -242,7 +242,9 @@ void violation_stats(const InstView &I, const double *x, double tol, double *d_o
                      TraceScratch &ts, pf_violation *rep, cudaStream_t s);
 
 // Projection (projection.cu).
-void project_device(const pf_instance *inst, const double *d_rates, int64_t alpha, double *d_out, cudaStream_t s);
+// fast = true (fast-mode solves): tolerance-matched parallel trims in phase 3
+void project_device(const pf_instance *inst, const double *d_rates, int64_t alpha, double *d_out, cudaStream_t s,
+                    bool fast = false);
 void score_paths_device(const pf_instance *inst, const double *d_rates, int64_t alpha, double *d_scores,
                         cudaStream_t s);
 

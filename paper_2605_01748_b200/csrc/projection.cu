@@ -324,7 +324,125 @@ __global__ void k_edge_paths(InstView I, int32_t *epath) {
     if (t < I.NP) epath[t] = I.pair_path[I.edge_pairs[t]];
 }
 
+
+// Fast-mode phase 3 (tolerance-matched, deterministic): the same walk over the
+// violated edges in order, but each pass trims an edge's paths with a CTA-wide
+// prefix sum of the score-ordered rates instead of the reference's sequential
+// `excess -= d` chain: the paths before the first prefix >= excess are zeroed,
+// that path keeps prefix - excess.  The re-sum (a fixed-order tree here) and
+// the up-to-16 passes are the reference's, so any rounding excess left by the
+// reassociated sums is trimmed by the next pass and the result is feasible.
+__device__ double cta_sum_tree(double v, double *red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        double r = l < nw ? red[l] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
+        if (l == 0) red[32] = r;
+    }
+    __syncthreads();
+    const double r = red[32];
+    __syncthreads();
+    return r;
+}
+
+__device__ double cta_edge_resum_fast(const int32_t *epath, const double *x, int32_t lo, int32_t hi, double *red) {
+    double v = 0.0;
+    for (int32_t t = lo + threadIdx.x; t < hi; t += blockDim.x) v += x[epath[t]];
+    return cta_sum_tree(v, red);
+}
+
+constexpr int FCH = 4096;  // chunk of ordered candidates: 4 per thread
+
+__global__ void __launch_bounds__(1024) k_edge_trim_fast(InstView I, const int32_t *edge_order,
+                                                          const int32_t *nviol_p, const int32_t *path_order,
+                                                          const int32_t *epath, double *x, const double *over,
+                                                          uint8_t *dirty) {
+    extern __shared__ __align__(16) char dsm[];
+    double *sx = (double *)dsm;                                      // [FCH]
+    int32_t *sp = (int32_t *)(dsm + FCH * sizeof(double));          // [FCH]
+    __shared__ double red[33], wsum[32];
+    __shared__ int32_t s_jstar;
+    const int32_t nviol = *nviol_p;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    for (int32_t vi = 0; vi < nviol; ++vi) {
+        const int32_t e = edge_order[vi];
+        const int32_t lo = I.edge_pair_ptr[e], hi = I.edge_pair_ptr[e + 1];
+        const double cap = I.capacity[e];
+        double excess = dirty[e] ? cta_edge_resum_fast(epath, x, lo, hi, red) - cap : over[e];
+        if (excess <= 0.0) continue;
+        for (int pass = 0; pass < 16; ++pass) {
+            double carry = 0.0;  // prefix of the chunks already zeroed
+            for (int32_t base = lo; base < hi; base += FCH) {
+                const int32_t n = hi - base < FCH ? hi - base : FCH;
+                double v[4], incl[4];
+                double tsum = 0.0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int32_t j = 4 * tid + u;
+                    double xv = 0.0;
+                    if (j < n) {
+                        const int32_t p = path_order[base + j];
+                        sp[j] = p;
+                        xv = x[p];
+                    }
+                    v[u] = xv;
+                    tsum += xv;
+                    incl[u] = tsum;
+                }
+                // block exclusive scan of the thread sums
+                double ws = tsum;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double t = __shfl_up_sync(0xffffffffu, ws, o);
+                    if (lane >= o) ws += t;
+                }
+                if (lane == 31) wsum[warp] = ws;
+                if (tid == 0) s_jstar = INT_MAX;
+                __syncthreads();
+                if (warp == 0) {
+                    double a = lane < nw ? wsum[lane] : 0.0;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const double t = __shfl_up_sync(0xffffffffu, a, o);
+                        if (lane >= o) a += t;
+                    }
+                    if (lane < nw) wsum[lane] = a;  // inclusive warp prefixes
+                }
+                __syncthreads();
+                const double before = carry + (warp ? wsum[warp - 1] : 0.0) + (ws - tsum);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (4 * tid + u < n && before + incl[u] >= excess) atomicMin(&s_jstar, 4 * tid + u);
+                __syncthreads();
+                const int32_t js = s_jstar;
+                const double total = wsum[nw - 1];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int32_t j = 4 * tid + u;
+                    if (j >= n) continue;
+                    double nx = v[u];
+                    if (j < js)
+                        nx = 0.0;
+                    else if (j == js)
+                        nx = max0(before + incl[u] - excess);  // prefix - excess (>= 0)
+                    sx[j] = nx;
+                }
+                __syncthreads();
+                for (int32_t j = tid; j < n; j += blockDim.x) write_back(I, x, dirty, sp[j], sx[j]);
+                __syncthreads();
+                if (js != INT_MAX) break;
+                carry += total;
+            }
+            excess = cta_edge_resum_fast(epath, x, lo, hi, red) - cap;
+            if (excess <= 0.0) break;
+        }
+    }
+}
+
 constexpr int TRIM_SMEM = 2 * TCH * (sizeof(double) + sizeof(int32_t));
+constexpr int TRIM_FAST_SMEM = FCH * (sizeof(double) + sizeof(int32_t));
 
 // Persistent scratch for the projection of one instance's index spaces (allocated
 // once; no cudaMalloc / host synchronisation inside a projection).
@@ -378,6 +496,7 @@ static ProjWS &workspace(const pf_instance *inst, cudaStream_t s) {
     ws->cub_bytes = std::max<size_t>(std::max(a, b), 16);
     ws->cub.alloc(ws->cub_bytes);
     PF_CUDA(cudaFuncSetAttribute(k_edge_trim, cudaFuncAttributeMaxDynamicSharedMemorySize, TRIM_SMEM));
+    PF_CUDA(cudaFuncSetAttribute(k_edge_trim_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, TRIM_FAST_SMEM));
     inst->proj_ws = ws;
     return *ws;
 }
@@ -398,7 +517,8 @@ void score_paths_device(const pf_instance *inst, const double *x, int64_t alpha,
     PF_CUDA(cudaStreamSynchronize(s));
 }
 
-void project_device(const pf_instance *inst, const double *rates, int64_t alpha, double *x, cudaStream_t s) {
+void project_device(const pf_instance *inst, const double *rates, int64_t alpha, double *x, cudaStream_t s,
+                    bool fast) {
     InstView I = inst->view();
     if (I.P == 0) return;
     ProjWS &ws = workspace(inst, s);
@@ -434,6 +554,10 @@ void project_device(const pf_instance *inst, const double *rates, int64_t alpha,
     }
     static const int stats = getenv("PF_PROJ_STATS") ? 1 : 0;
     PF_CUDA(cudaMemsetAsync(ws.dirty.p, 0, I.E + 1, s));
+    if (fast)
+        k_edge_trim_fast<<<1, 1024, TRIM_FAST_SMEM, s>>>(I, ws.eorder.p, ws.nviol.p, ws.porder.p, ws.epath.p, x,
+                                                         ws.over.p, ws.dirty.p);
+    else
     k_edge_trim<<<1, 1024, TRIM_SMEM, s>>>(I, ws.eorder.p, ws.nviol.p, ws.porder.p, ws.epath.p, x, ws.over.p, ws.dirty.p,
                                    stats);
     PF_CHECK_LAUNCH();

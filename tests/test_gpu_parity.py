@@ -410,3 +410,23 @@ def test_fast_large_edge_mode_matches_exact(monkeypatch):
     small = pf.solve(inst2, pf.SolverConfig(mode="fast", max_iterations=400))
     assert pf.validate_allocation(inst, big.rates).feasible
     np.testing.assert_allclose(np.sort(big.sums), np.sort(small.sums), rtol=1e-3, atol=1e-3 * float(small.sums.max()))
+
+
+def test_fast_solve_projection_feasible_and_close_to_exact():
+    """A fast-mode solve projects with the tolerance-matched parallel trim; on a
+    raw, heavily infeasible iterate it must return an exactly feasible allocation
+    whose commodity sums agree with the bitwise (reference-order) projection."""
+    from b200_helpers import generated
+    topo, tab, ps = generated(60, 8, 1.5)
+    inst = pf.build_instance(topo, tab, ps, device=0)
+    s = pf.Solver(inst, pf.SolverConfig(mode="fast", gamma=1e-12)).init()
+    s.run(12)
+    x = s.x()
+    alpha = int(s.state().alpha)
+    before = pf.validate_allocation(inst, np.maximum(x, 0.0))
+    assert not before.feasible  # the test is about real trimming
+    fast_rates, fast_sums = s.finish()
+    exact_rates = pf.project(inst, x, alpha)
+    assert pf.validate_allocation(inst, fast_rates).feasible
+    np.testing.assert_allclose(fast_sums, pf.commodity_sums(inst, exact_rates), rtol=1e-6,
+                               atol=1e-9 * float(np.max(np.abs(x))))
