@@ -16,6 +16,11 @@ e2e   : the same metric through the reference-facing C-ABI call `pf_solve`
         rates + sums D2H, all inside the timed region.
 Working set (~0.5 GB) exceeds the 126 MB L2, so no L2 flush is needed.
 
+Extra keys (rank 0, N=1): time_to_1pct on cfg1 / cfg2 / the north-star-scale
+instance at V = 0.3 x capacity; config4_link_failure_resolve (5% of the links
+cut, warm re-solve) and config5_alpha_sweep (alpha_target 0..4 and max-min) on
+the 500-node WAN (--no-ttq / --no-extras skip them).
+
 --impl reference times the reference algorithm's CPU implementation (the
 exact-order C oracle, oracle/pf_oracle.c, OpenMP over all host cores) on the
 same config; each step is one iteration.
@@ -256,6 +261,45 @@ def time_to_quality(name, device=0, cpu=True, chunk=None):
     return out
 
 
+def config45(name, device=0):
+    """BASELINE configs 4 and 5 at config-2 scale, fast mode:
+    4: after a cold solve, cut 5% of the links (rng = default_rng(1), capacity 0
+       via with_conditions, paths kept as in run_experiment) and re-solve warm
+       from the previous rates with alpha_target = the previous alpha;
+    5: the alpha_target sweep {0, 1, 2, 3, 4, None} (max-min) from cold starts.
+    Times are the solver's runtime_s (init through projection, controller.py:276)."""
+    import paper_2605_01748_b200 as pf
+    topo, tab, flat = build_inputs(name)
+    inst = pf.build_instance_flat(topo, tab, flat, device=device)
+    cold = pf.solve(inst, pf.SolverConfig(mode="fast"))
+    rng = np.random.default_rng(1)
+    E = inst.num_edges
+    cut = rng.choice(E, int(round(0.05 * E)), replace=False)
+    cap = np.array(topo.capacity, np.float64)
+    cap[cut] = 0.0
+    failed = pf.with_conditions(inst, capacity=cap)
+    warm = pf.solve(failed, pf.SolverConfig(mode="fast", alpha_target=int(cold.alpha)), warm_start=cold.rates)
+    fresh = pf.solve(failed, pf.SolverConfig(mode="fast", alpha_target=int(cold.alpha)))
+    theta = pf.default_theta(failed)
+    out4 = {"config": name, "links_cut": int(cut.size),
+            "cold_solve": {"iterations": int(cold.iterations), "alpha": int(cold.alpha),
+                           "converged": bool(cold.converged), "ms": 1e3 * cold.runtime_s},
+            "warm_resolve": {"iterations": int(warm.iterations), "converged": bool(warm.converged),
+                             "ms": 1e3 * warm.runtime_s,
+                             "feasible": bool(pf.validate_allocation(failed, warm.rates).feasible),
+                             "optimality_vs_cold_resolve": pf.optimality_from_sums(warm.sums, fresh.sums, theta)},
+            "cold_resolve": {"iterations": int(fresh.iterations), "converged": bool(fresh.converged),
+                             "ms": 1e3 * fresh.runtime_s}}
+    out5 = []
+    for at in (0, 1, 2, 3, 4, None):
+        r = pf.solve(inst, pf.SolverConfig(mode="fast", alpha_target=at))
+        out5.append({"alpha_target": at, "iterations": int(r.iterations), "alpha": int(r.alpha),
+                     "converged": bool(r.converged), "ms": 1e3 * r.runtime_s,
+                     "min_sum": float(np.min(r.sums)) if r.sums.size else None,
+                     "feasible": bool(pf.validate_allocation(inst, r.rates).feasible)})
+    return out4, out5
+
+
 def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
@@ -338,6 +382,9 @@ def run_b200(args):
     ttq = None
     if rank == 0 and not args.no_ttq:
         ttq = [time_to_quality(n, device=local, cpu=not args.no_cpu_baseline) for n in args.ttq.split(",") if n]
+    cfg4 = cfg5 = None
+    if rank == 0 and not args.no_extras:
+        cfg4, cfg5 = config45(args.extras_config, device=local)
     line = {
         "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -352,6 +399,8 @@ def run_b200(args):
         "e2e": e2e,
         "cpu_baseline": cpu,
         "time_to_1pct": ttq,
+        "config4_link_failure_resolve": cfg4,
+        "config5_alpha_sweep": cfg5,
         "clocks": clk,
         "gpu_launches": 1,
         "wall_s_timed_region": t_wall,
@@ -371,7 +420,9 @@ def main(argv=None):
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ttq", action="store_true", help="skip the time-to-within-1%% measurement")
-    ap.add_argument("--ttq", default="cfg1_v0.3,cfg2_v0.3", help="configs for time-to-within-1%%")
+    ap.add_argument("--ttq", default="cfg1_v0.3,cfg2_v0.3,target_k4_v0.3", help="configs for time-to-within-1%%")
+    ap.add_argument("--no-extras", action="store_true", help="skip the config 4 / config 5 measurements")
+    ap.add_argument("--extras-config", default="cfg2_v0.3", help="instance for the config 4 / 5 measurements")
     args = ap.parse_args(argv)
     if args.impl == "reference":
         return run_reference(args)

@@ -454,7 +454,7 @@ static pf_solver *solver_create(const pf_instance *inst, const pf_config *cfg) {
 static void solver_destroy(pf_solver *S) {
     if (!S) return;
     DeviceGuard g(S->inst->device());
-    if (S->fast) fast_destroy(S->fast);
+    if (S->fast) fast_release(S->fast);
     if (S->ev0) cudaEventDestroy(S->ev0);
     if (S->ev1) cudaEventDestroy(S->ev1);
     if (S->stream) cudaStreamDestroy(S->stream);

@@ -1347,8 +1347,64 @@ struct FastSolver {
     int dgraph_state = 0;  // 0 untried, 1 built, -1 unavailable (host-driven loop)
 };
 
+static void fast_set_config(FastSolver *F, const pf_config &cfg) {
+    const Index &I = *F->inst->idx;
+    F->cfg = cfg;
+    if (cfg.trace && !F->root_sums.p) F->root_sums.alloc(I.C ? I.C : 1);
+    Params &P = F->P;
+    P.root_sums = cfg.trace ? F->root_sums.p : nullptr;
+    P.gamma = cfg.gamma;
+    P.residual_ratio = cfg.residual_ratio;
+    P.beta_scale = cfg.beta_scale;
+    P.beta_min = cfg.beta_min;
+    P.beta_max = cfg.beta_max;
+    P.alpha_target = cfg.alpha_target;
+    P.max_iterations = cfg.max_iterations;
+    P.adapt = cfg.adapt;
+}
+
+static void pool_free(void *p) { fast_destroy((FastSolver *)p); }
+
+void fast_release(FastSolver *F) {
+    if (!F) return;
+    if (!F->comm) {
+        std::lock_guard<std::mutex> lk(F->inst->ws_mu);
+        if (!F->inst->fast_pool) {
+            F->inst->fast_pool = F;
+            F->inst->fast_pool_free = pool_free;
+            return;
+        }
+    }
+    fast_destroy(F);
+}
+
+static const cudaDeviceProp &device_props(int dev) {
+    static std::mutex mu;
+    static std::vector<std::unique_ptr<cudaDeviceProp>> props;
+    std::lock_guard<std::mutex> lk(mu);
+    if ((int)props.size() <= dev) props.resize(dev + 1);
+    if (!props[dev]) {
+        props[dev].reset(new cudaDeviceProp());
+        PF_CUDA(cudaGetDeviceProperties(props[dev].get(), dev));
+    }
+    return *props[dev];
+}
+
 FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStream_t s) {
     const Index &I = *inst->idx;
+    {  // reuse the instance's idle solver (same index spaces and layout)
+        FastSolver *pooled = nullptr;
+        {
+            std::lock_guard<std::mutex> lk(inst->ws_mu);
+            pooled = (FastSolver *)inst->fast_pool;
+            inst->fast_pool = nullptr;
+        }
+        if (pooled) {
+            fast_set_config(pooled, cfg);
+            pooled->launches = 0;
+            return pooled;
+        }
+    }
     std::unique_ptr<FastSolver> F(new FastSolver());
     F->inst = inst;
     F->cfg = cfg;
@@ -1361,8 +1417,7 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     if (const char *v = getenv("PF_FAST_NBUF")) F->nbuf = std::max(1, std::min(2, atoi(v)));
     F->smem = (size_t)smem_plan(F->L->tps, (int)I.E, F->nbuf, F->L->adj_smem).total;
     int dev = inst->device();
-    cudaDeviceProp prop;
-    PF_CUDA(cudaGetDeviceProperties(&prop, dev));
+    const cudaDeviceProp &prop = device_props(dev);
     const size_t static_smem = sizeof(Ctrl) + sizeof(CtaShared) + 64;
     require(F->smem + static_smem <= (size_t)prop.sharedMemPerBlockOptin,
             "fast mode: edge tables do not fit in shared memory (too many edges)");

@@ -158,6 +158,13 @@ struct pf_instance {
     cudaStream_t stream = nullptr;
     mutable std::mutex ws_mu;
     mutable std::shared_ptr<void> proj_ws;  // projection scratch (projection.cu)
+    // one idle fast-mode solver kept for the next solve on this instance (fused.cu):
+    // its device buffers are reused instead of re-allocated per solve
+    mutable void *fast_pool = nullptr;
+    mutable void (*fast_pool_free)(void *) = nullptr;
+    ~pf_instance() {
+        if (fast_pool && fast_pool_free) fast_pool_free(fast_pool);
+    }
     pf::InstView view() const {
         pf::InstView v;
         v.C = (int32_t)idx->C;
