@@ -200,6 +200,11 @@ void *pf_ksp_run(int32_t n_nodes, int64_t n_edges, const int64_t *edge_src, cons
 void pf_ksp_sizes(void *h, int64_t *n_paths, int64_t *n_pairs);
 void pf_ksp_export(void *h, int64_t *com_path_ptr, int64_t *path_edge_ptr, int64_t *path_edges);
 void pf_ksp_free(void *h);
+/* model.py:183-203 _check_path over every path (host, OpenMP): first bad path
+ * in commodity-major order, or -1 (build_instance's validation) */
+int64_t pf_validate_paths(int64_t n_commodities, const int64_t *com_path_ptr, const int64_t *path_edge_ptr,
+                          const int64_t *path_edges, int64_t n_edges, const int64_t *edge_src,
+                          const int64_t *edge_dst, const int64_t *com_src, const int64_t *com_dst);
 
 #ifdef __cplusplus
 }

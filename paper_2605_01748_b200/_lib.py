@@ -50,6 +50,8 @@ def _declare(L):
     L.pf_ksp_sizes.argtypes = [C.c_void_p, _i64p, _i64p]
     L.pf_ksp_export.argtypes = [C.c_void_p, _i64p, _i64p, _i64p]
     L.pf_ksp_free.argtypes = [C.c_void_p]
+    L.pf_validate_paths.restype = C.c_int64
+    L.pf_validate_paths.argtypes = [C.c_int64, _i64p, _i64p, _i64p, C.c_int64, _i64p, _i64p, _i64p, _i64p]
     from . import _abi
     _abi.declare(L)
 

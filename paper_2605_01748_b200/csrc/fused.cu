@@ -160,6 +160,7 @@ struct Params {
     InstView I;
     int32_t ntiles, G, nslices, tps, nbuf, kspan;  // kspan: power of two >= max paths per commodity
     int32_t adj_smem;                               // adjustment table in shared memory (else L1)
+    int32_t pf_dist;                                // L2 prefetch distance in tiles (single stage)
     const TileDesc *desc;
     const int32_t *cta_ptr, *cta_tiles;  // CTA g walks tiles cta_tiles[cta_ptr[g] .. cta_ptr[g + 1])
     const uint8_t *meta;
@@ -911,8 +912,8 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
                 const int nb = b ^ 1;
                 cs.sd[nb] = P.desc[tile_of(k + 1)];
                 issue_tile<MODE>(P, io, cs.sd[nb], base, sp, nb, &cs.bar[nb]);
-            } else {  // single stage: warm L2 with the next tile's pair data
-                const TileDesc dn_ = P.desc[tile_of(k + 1)];
+            } else if (k + P.pf_dist < my) {  // single stage: warm L2 with a later tile's pair data
+                const TileDesc dn_ = P.desc[tile_of(k + P.pf_dist)];
                 prefetch_l2(io.dcon_in + dn_.sb, 8u * even(dn_.np));
                 prefetch_l2(P.meta + (size_t)dn_.mb16 * 16,
                             (uint32_t)meta_off(dn_.np, dn_.p1 - dn_.p0, dn_.c1 - dn_.c0).bytes);
@@ -1493,6 +1494,8 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     P.nbuf = F->nbuf;
     P.kspan = F->L->kspan;
     P.adj_smem = F->L->adj_smem ? 1 : 0;
+    P.pf_dist = 1;
+    if (const char *v = getenv("PF_FAST_PFDIST")) P.pf_dist = std::max(1, atoi(v));
     {
         double rcp[RCP_MAX + 1];
         rcp[0] = 0.0;

@@ -345,4 +345,43 @@ void pf_ksp_export(void *h, int64_t *com_path_ptr, int64_t *path_edge_ptr, int64
 
 void pf_ksp_free(void *h) { delete (pf_ksp_result *)h; }
 
+// model.py:183-203 (_check_path) for every path, in parallel: returns the
+// first (commodity-major) path that is empty, has an out-of-range edge id, does
+// not start / end at its commodity's nodes, has non-adjacent consecutive edges
+// or revisits a node; -1 when all paths are valid.
+int64_t pf_validate_paths(int64_t n_commodities, const int64_t *com_path_ptr, const int64_t *path_edge_ptr,
+                          const int64_t *path_edges, int64_t n_edges, const int64_t *edge_src,
+                          const int64_t *edge_dst, const int64_t *com_src, const int64_t *com_dst) {
+    const int64_t P = com_path_ptr[n_commodities];
+    int64_t first = INT64_MAX;
+#pragma omp parallel
+    {
+        int64_t mine = INT64_MAX;
+        std::vector<int64_t> seen;
+#pragma omp for schedule(dynamic, 4096)
+        for (int64_t c = 0; c < n_commodities; ++c) {
+            for (int64_t p = com_path_ptr[c]; p < com_path_ptr[c + 1] && p < mine; ++p) {
+                const int64_t lo = path_edge_ptr[p], hi = path_edge_ptr[p + 1];
+                bool bad = hi <= lo;
+                for (int64_t t = lo; t < hi && !bad; ++t) bad = path_edges[t] < 0 || path_edges[t] >= n_edges;
+                if (!bad) bad = edge_src[path_edges[lo]] != com_src[c] || edge_dst[path_edges[hi - 1]] != com_dst[c];
+                for (int64_t t = lo; t + 1 < hi && !bad; ++t) bad = edge_dst[path_edges[t]] != edge_src[path_edges[t + 1]];
+                if (!bad) {  // simple: src(first) and every dst distinct
+                    seen.assign(1, edge_src[path_edges[lo]]);
+                    for (int64_t t = lo; t < hi && !bad; ++t) {
+                        const int64_t v = edge_dst[path_edges[t]];
+                        for (int64_t u : seen) bad = bad || u == v;
+                        seen.push_back(v);
+                    }
+                }
+                if (bad) mine = std::min(mine, p);
+            }
+        }
+#pragma omp critical
+        first = std::min(first, mine);
+    }
+    (void)P;
+    return first == INT64_MAX ? -1 : first;
+}
+
 }  // extern "C"

@@ -178,6 +178,16 @@ def _validate_paths(topology: Topology, table: CommodityTable, flat: FlatPathSet
     P0 = pep.shape[0] - 1
     if P0 == 0:
         return
+    # the native check (OpenMP) finds whether any path is bad; the vectorised
+    # code below only runs to name the first bad path with the reference's message
+    from ._lib import lib
+    i64 = lambda a: np.ascontiguousarray(a, np.int64)  # noqa: E731
+    arrs = [i64(cpp), i64(pep), i64(pe), i64(topology.edge_src), i64(topology.edge_dst), i64(table.src),
+            i64(table.dst)]
+    ptr = [a.ctypes.data_as(C.POINTER(C.c_int64)) for a in arrs]
+    if lib().pf_validate_paths(len(table), ptr[0], ptr[1], ptr[2], topology.num_edges, ptr[3], ptr[4], ptr[5],
+                               ptr[6]) < 0:
+        return
     m = topology.num_edges
     hops = np.diff(pep)
     owner = np.repeat(np.arange(len(table), dtype=np.int64), np.diff(cpp))
