@@ -192,6 +192,15 @@ int pf_comm_unique_id(void *id128);
 int pf_comm_create(int nranks, int rank, const void *id128, int device, pf_comm **out);
 int pf_comm_destroy(pf_comm *c);
 int pf_solver_attach_comm(pf_solver *s, pf_comm *c, int64_t global_commodities);
+/* Multi-GPU over NVLink peer memory (one process per GPU): the fused kernel
+ * writes its rank-local per-edge totals into every rank's exchange buffer and
+ * meets the other ranks at a counter barrier (no host round trip, no NCCL).
+ * xchg_create returns this rank's 64-byte CUDA IPC handle; xchg_connect takes
+ * all ranks' handles (rank order).  set_edge_counts: global paths per edge
+ * (the divisor n_e + 1 of kernels.py:94) summed over the ranks' shards. */
+int pf_solver_xchg_create(pf_solver *s, int rank, int nranks, void *handle64);
+int pf_solver_xchg_connect(pf_solver *s, const void *handles);
+int pf_solver_set_edge_counts(pf_solver *s, const double *counts);
 
 /* ---- host input preparation: k shortest paths (harness.py:138-176) ---- */
 void *pf_ksp_run(int32_t n_nodes, int64_t n_edges, const int64_t *edge_src, const int64_t *edge_dst,

@@ -86,6 +86,9 @@ SIGNATURES = {
     "pf_comm_create": (C.c_int, [C.c_int, C.c_int, vp, C.c_int, C.POINTER(vp)]),
     "pf_comm_destroy": (C.c_int, [vp]),
     "pf_solver_attach_comm": (C.c_int, [vp, vp, i64]),
+    "pf_solver_xchg_create": (C.c_int, [vp, C.c_int, C.c_int, vp]),
+    "pf_solver_xchg_connect": (C.c_int, [vp, vp]),
+    "pf_solver_set_edge_counts": (C.c_int, [vp, f64p]),
 }
 
 

@@ -805,6 +805,32 @@ int pf_solver_attach_comm(pf_solver *S, pf_comm *c, int64_t global_commodities) 
     });
 }
 
+int pf_solver_xchg_create(pf_solver *S, int rank, int nranks, void *handle64) {
+    return guard([&] {
+        require(S != nullptr && handle64 != nullptr, "null argument");
+        require(S->cfg.mode == PF_MODE_FAST, "multi-GPU solves run in PF_MODE_FAST");
+        DeviceGuard g(S->inst->device());
+        fast_xchg_create(S->fast, rank, nranks, handle64);
+    });
+}
+
+int pf_solver_xchg_connect(pf_solver *S, const void *handles) {
+    return guard([&] {
+        require(S != nullptr && handles != nullptr, "null argument");
+        DeviceGuard g(S->inst->device());
+        fast_xchg_connect(S->fast, handles);
+    });
+}
+
+int pf_solver_set_edge_counts(pf_solver *S, const double *counts) {
+    return guard([&] {
+        require(S != nullptr && counts != nullptr, "null argument");
+        require(S->cfg.mode == PF_MODE_FAST, "edge counts apply to PF_MODE_FAST");
+        DeviceGuard g(S->inst->device());
+        fast_set_edge_counts(S->fast, counts);
+    });
+}
+
 int pf_solver_destroy(pf_solver *S) {
     return guard([&] { solver_destroy(S); });
 }

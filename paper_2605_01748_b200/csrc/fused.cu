@@ -154,12 +154,19 @@ struct Ctrl {
     int64_t alpha, alpha_used, iteration, cooldown, target;
     int32_t just_incremented, stopped, status, xc, db, need_a1, need_edge, pad;
     int64_t bad;
+    uint64_t xepoch;  // multi-GPU exchanges done (mirrors *Params::xepoch)
 };
 
 struct Params {
     InstView I;
     int32_t ntiles, G, nslices, tps, nbuf, kspan;  // kspan: power of two >= max paths per commodity
     int32_t adj_smem;                               // adjustment table in shared memory (else L1)
+    // multi-GPU over peer memory (CUDA IPC): rank-local totals are written into
+    // slot [rank] of every rank's exchange buffer; nranks = 0 when single-GPU
+    int32_t rank, nranks;
+    int64_t xslot;                 // doubles per slot: T[E], L[E], 16 scalars
+    double *const *peers;          // [nranks] exchange buffer bases (peers[rank] = own)
+    unsigned long long *xepoch;    // exchanges done (device, never reset)
     int32_t pf_dist;                                // L2 prefetch distance in tiles (single stage)
     const TileDesc *desc;
     const int32_t *cta_ptr, *cta_tiles;  // CTA g walks tiles cta_tiles[cta_ptr[g] .. cta_ptr[g + 1])
@@ -962,6 +969,180 @@ __device__ __forceinline__ void cta_init(CtaShared &cs) {
     __syncthreads();
 }
 
+// ------------------------------------------------------------------ multi-GPU exchange
+//
+// Buffer layout per rank (peer-writable): [2 parities][nranks slots][xslot
+// doubles] followed by one u64 arrival counter.  Exchange number n uses parity
+// n & 1; a rank adds 1 to every rank's counter after its slot is written, so
+// exchange n is complete on a rank when its counter reaches nranks * (n + 1).
+// Two parities suffice: a rank reads exchange n before it computes the pass
+// whose totals it sends in exchange n + 1.
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ double *xb_slot(const Params &P, const double *base, uint64_t epoch, int r) {
+    return (double *)base + ((epoch & 1) * (uint64_t)P.nranks + (uint64_t)r) * (uint64_t)P.xslot;
+}
+__device__ __forceinline__ unsigned long long *xb_flag(const Params &P, const double *base) {
+    return (unsigned long long *)((double *)base + 2 * (uint64_t)P.nranks * (uint64_t)P.xslot);
+}
+
+// Rank-local totals of the pass just completed -> every rank's slot [rank]:
+// per-edge T and L (CTA partials summed in the same (slice, CTA) order as the
+// single-GPU edge phase), the 7 residual sums and the 2 error flags; then the
+// counter barrier across ranks.  Ends with a grid barrier after which every CTA
+// may read all slots of this exchange.
+__device__ __noinline__ void xchg_phase(const Params &P, Ctrl &c, cg::grid_group &grid) {
+    const InstView &I = P.I;
+    const int g = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t ep = c.xepoch;
+    const int ngroups = (I.E + RGRP - 1) / RGRP;
+    const int nitems = ngroups * P.nslices;
+    const int per = (P.G + P.nslices - 1) / P.nslices;
+    bool wrote = false;  // this thread stored into peer memory
+    for (int item = g * NW + warp; item < nitems; item += P.G * NW) {
+        const int grp = item / P.nslices, sl = item % P.nslices;
+        const int e = grp * RGRP + lane;
+        const int g0 = sl * per, g1 = g0 + per < P.G ? g0 + per : P.G;
+        double sT = 0.0, sL = 0.0;
+        if (e < I.E) {
+            for (int gg = g0; gg < g1; ++gg) {
+                sT += __ldcg(&P.partT[(size_t)gg * I.E + e]);
+                sL += __ldcg(&P.partL[(size_t)gg * I.E + e]);
+            }
+            P.sub[(size_t)sl * I.E + e] = sT;
+            P.sub[(size_t)(P.nslices + sl) * I.E + e] = sL;
+        }
+        __threadfence();
+        __syncwarp();
+        int ticket = 0;
+        if (lane == 0) ticket = atomicAdd(&P.grp_count[grp], 1);
+        ticket = __shfl_sync(FULL, ticket, 0);
+        if (ticket == P.nslices - 1) {
+            __threadfence();
+            wrote = true;
+            if (e < I.E) {
+                double T = 0.0, L = 0.0;
+                for (int k = 0; k < P.nslices; ++k) {
+                    T += __ldcg(&P.sub[(size_t)k * I.E + e]);
+                    L += __ldcg(&P.sub[(size_t)(P.nslices + k) * I.E + e]);
+                }
+                for (int r = 0; r < P.nranks; ++r) {
+                    double *d = xb_slot(P, P.peers[r], ep, P.rank);
+                    d[e] = T;
+                    d[I.E + e] = L;
+                }
+            }
+            if (lane == 0) P.grp_count[grp] = 0;
+        }
+    }
+    if (g == 0 && threadIdx.x < 32) {  // residual sums over the CTAs, error flags
+        // same association as controller_eval (lane-strided, then a shuffle tree),
+        // so one rank reproduces the single-GPU controller bitwise
+        double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+        for (int gg = threadIdx.x; gg < P.G; gg += 32)
+            for (int j = 0; j < 7; ++j) acc[j] += __ldcg(&P.res[gg * 8 + j]);
+        for (int j = 0; j < 7; ++j)
+            for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_down_sync(FULL, acc[j], o);
+        if (threadIdx.x == 0) {
+            wrote = true;
+            const double e0 = __ldcg(&P.err[0]) != INT_MAX ? 1.0 : 0.0;
+            const double e1 = __ldcg(&P.err[1]) != INT_MAX ? 1.0 : 0.0;
+            for (int r = 0; r < P.nranks; ++r) {
+                double *d = xb_slot(P, P.peers[r], ep, P.rank) + 2 * I.E;
+                for (int j = 0; j < 7; ++j) d[j] = acc[j];
+                d[7] = e0;
+                d[8] = e1;
+            }
+        }
+    }
+    if (wrote) __threadfence_system();  // this thread's peer stores before the arrival signal
+    grid.sync();
+    __shared__ int s_timeout;
+    if (threadIdx.x == 0) {
+        s_timeout = 0;
+        if (g == 0) {
+            __threadfence_system();
+            for (int r = 0; r < P.nranks; ++r) atomicAdd_system(xb_flag(P, P.peers[r]), 1ull);
+        }
+        // every CTA waits for all ranks' slots (bounded: ~20 s, then PF_ERR_COMM)
+        const unsigned long long want = (unsigned long long)P.nranks * (ep + 1);
+        const unsigned long long *flag = xb_flag(P, P.peers[P.rank]);
+        const long long t0 = clock64();
+        while (ld_acquire_sys(flag) < want) {
+            if (clock64() - t0 > 40000000000ll) {
+                s_timeout = 1;
+                break;
+            }
+            __nanosleep(64);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_timeout) c.status = PF_ERR_COMM;
+        c.xepoch = ep + 1;
+    }
+    __syncthreads();
+}
+
+// Sum of slot values over the ranks in rank order (identical on every rank).
+__device__ __forceinline__ double xsum(const Params &P, uint64_t ep, int64_t off) {
+    double v = __ldcg(&xb_slot(P, P.peers[P.rank], ep, 0)[off]);
+    for (int r = 1; r < P.nranks; ++r) v += __ldcg(&xb_slot(P, P.peers[P.rank], ep, r)[off]);
+    return v;
+}
+
+// kernels.py:212 and :94-96 from the exchanged totals of the last exchange
+__device__ __noinline__ void xchg_edge_apply(const Params &P, const Ctrl &c, double f) {
+    const InstView &I = P.I;
+    const uint64_t ep = c.xepoch - 1;
+    const int ngroups = (I.E + RGRP - 1) / RGRP;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int grp = blockIdx.x * NW + warp; grp < ngroups; grp += P.G * NW) {
+        const int e = grp * RGRP + lane;
+        double rdc = 0.0;
+        if (e < I.E) {
+            const double T = xsum(P, ep, e), L = xsum(P, ep, I.E + e);
+            const double cap = I.capacity[e];
+            const double dold = __ldcg(&P.dc[e]) * f;
+            const double dnew = npmax0(dold + (L - cap));
+            double adj = (T + dnew - cap) / (P.ne[e] + 1.0);
+            if (adj < 0.0) adj = 0.0;
+            P.dc[e] = dnew;
+            P.adj[e] = adj;
+            const double d = dnew - dold;
+            rdc = d * d;
+        }
+        for (int o = 16; o > 0; o >>= 1) rdc += __shfl_down_sync(FULL, rdc, o);
+        if (lane == 0) P.res_dc[grp] = rdc;
+    }
+}
+
+// controller_eval from the exchanged residual sums (every CTA, same result)
+__device__ void xchg_controller_eval(const Params &P, Ctrl &c) {
+    if (threadIdx.x < 32) {
+        const uint64_t ep = c.xepoch - 1;
+        const int64_t b = 2 * (int64_t)P.I.E;
+        const int par = (int)(c.iteration & 1);
+        double dcs = 0.0;
+        const int ngroups = (P.I.E + RGRP - 1) / RGRP;
+        for (int g = threadIdx.x; g < ngroups; g += 32) dcs += __ldcg(&P.res_dc[g]);
+        for (int o = 16; o > 0; o >>= 1) dcs += __shfl_down_sync(FULL, dcs, o);
+        if (threadIdx.x == 0) {
+            const double dx = xsum(P, ep, b + 0), rdd = xsum(P, ep, b + 1 + 3 * par),
+                         rdcon = xsum(P, ep, b + 2 + 3 * par), rdn = xsum(P, ep, b + 3 + 3 * par);
+            const bool fc = xsum(P, ep, b + 7) > 0.0, fr = xsum(P, ep, b + 8) > 0.0;
+            const int32_t ec = fc ? (__ldcg(&P.err[0]) != INT_MAX ? __ldcg(&P.err[0]) : -1) : INT_MAX;
+            const int32_t er = fr ? (__ldcg(&P.err[1]) != INT_MAX ? __ldcg(&P.err[1]) : -1) : INT_MAX;
+            if (!c.status) controller_step(P, c, sqrt(dx), sqrt(((rdd + dcs) + rdcon) + rdn), ec, er);
+        }
+    }
+    __syncthreads();
+}
+
 // ------------------------------------------------------------------ kernels
 
 __global__ void __launch_bounds__(NT, 2) k_fused(const __grid_constant__ Params P) {
@@ -973,9 +1154,11 @@ __global__ void __launch_bounds__(NT, 2) k_fused(const __grid_constant__ Params 
     uint32_t seq = 0;
     if (threadIdx.x == 0) c = *P.ctrl;
     __syncthreads();
+    const bool dist = P.nranks > 0;
     if (c.need_a1) {
         pass_tiles<MODE_A1>(P, c, smem_raw, cs, seq);
         grid.sync();
+        if (dist) xchg_phase(P, c, grid);
         if (threadIdx.x == 0) {
             c.need_a1 = 0;
             c.db ^= 1;
@@ -989,7 +1172,10 @@ __global__ void __launch_bounds__(NT, 2) k_fused(const __grid_constant__ Params 
         // continuing, so a stopped / paused state keeps adj_k for export
         if (c.stopped || c.status || c.iteration >= c.target || c.iteration >= P.max_iterations) break;
         if (c.need_edge) {
-            edge_phase(P, c.f);
+            if (dist)
+                xchg_edge_apply(P, c, c.f);
+            else
+                edge_phase(P, c.f);
             grid.sync();
             __syncthreads();
             if (threadIdx.x == 0) {
@@ -1009,16 +1195,25 @@ __global__ void __launch_bounds__(NT, 2) k_fused(const __grid_constant__ Params 
             c.db ^= 1;
         }
         __syncthreads();
-        controller_eval(P, c);
+        if (dist) {
+            xchg_phase(P, c, grid);
+            xchg_controller_eval(P, c);
+        } else {
+            controller_eval(P, c);
+        }
         if (!c.stopped && !c.status && c.f != 1.0) {
             pass_tiles<MODE_RB>(P, c, smem_raw, cs, seq);
             grid.sync();
+            if (dist) xchg_phase(P, c, grid);
         }
         __syncthreads();
         if (threadIdx.x == 0) c.need_edge = 1;
         __syncthreads();
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) *P.ctrl = c;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *P.ctrl = c;
+        if (dist) *P.xepoch = c.xepoch;
+    }
 }
 
 // ------------------------------------------------------------------ multi-GPU split kernels
@@ -1346,6 +1541,12 @@ struct FastSolver {
     cudaGraph_t dgraph = nullptr;
     cudaGraphExec_t dexec = nullptr;
     int dgraph_state = 0;  // 0 untried, 1 built, -1 unavailable (host-driven loop)
+    // multi-GPU over peer memory (CUDA IPC): see xchg_phase
+    int rank = 0, nranks = 0;
+    DevBuf<double> xb;                       // this rank's exchange buffer
+    DevBuf<double *> peers_dev;              // [nranks] peer bases
+    std::vector<void *> opened;              // IPC mappings to close
+    DevBuf<unsigned long long> xepoch;       // exchanges done
 };
 
 static void fast_set_config(FastSolver *F, const pf_config &cfg) {
@@ -1368,7 +1569,7 @@ static void pool_free(void *p) { fast_destroy((FastSolver *)p); }
 
 void fast_release(FastSolver *F) {
     if (!F) return;
-    if (!F->comm) {
+    if (!F->comm && !F->nranks) {
         std::lock_guard<std::mutex> lk(F->inst->ws_mu);
         if (!F->inst->fast_pool) {
             F->inst->fast_pool = F;
@@ -1544,6 +1745,7 @@ void fast_destroy(FastSolver *F) {
     if (!F) return;
     if (F->dexec) cudaGraphExecDestroy(F->dexec);
     if (F->dgraph) cudaGraphDestroy(F->dgraph);
+    for (void *p : F->opened) cudaIpcCloseMemHandle(p);
     if (F->e0) cudaEventDestroy(F->e0);
     if (F->e1) cudaEventDestroy(F->e1);
     delete F;
@@ -1739,6 +1941,9 @@ void fast_init(FastSolver *F, const double *d_x0, int64_t alpha0, double beta0, 
     c.db = 0;
     c.need_a1 = 1;
     c.need_edge = 0;
+    c.xepoch = 0;
+    if (F->nranks) d2h(&c.xepoch, (uint64_t *)F->xepoch.p, 1, s);  // exchange numbering continues
+    PF_CUDA(cudaStreamSynchronize(s));
     h2d(F->ctrl.p, &c, 1, s);
     PF_CUDA(cudaStreamSynchronize(s));
 }
@@ -1820,6 +2025,52 @@ void fast_export_state(FastSolver *F, double *x, double *y, double *dd, double *
     scaled(F->dd[dcur].p, I.C, dd);
     scaled(F->dc.p, I.E, dc);
     scaled(F->dn[dcur].p, I.P, dn);
+}
+
+void fast_xchg_create(FastSolver *F, int rank, int nranks, void *handle64) {
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank / world size");
+    require(!F->comm, "solver already has an NCCL communicator");
+    const Index &I = *F->inst->idx;
+    const int64_t xslot = (2 * I.E + 16 + 15) / 16 * 16;
+    F->rank = rank;
+    F->nranks = nranks;
+    F->xb.alloc((size_t)2 * nranks * xslot + 16);  // + the arrival counter
+    PF_CUDA(cudaMemset(F->xb.p, 0, F->xb.bytes()));
+    F->xepoch.alloc(1);
+    PF_CUDA(cudaMemset(F->xepoch.p, 0, sizeof(unsigned long long)));
+    cudaIpcMemHandle_t h;
+    PF_CUDA(cudaIpcGetMemHandle(&h, F->xb.p));
+    static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+    std::memcpy(handle64, &h, 64);
+    F->P.xslot = xslot;
+    F->P.xepoch = F->xepoch.p;
+}
+
+void fast_xchg_connect(FastSolver *F, const void *handles) {
+    require(F->nranks >= 1, "call pf_solver_xchg_create first");
+    std::vector<double *> bases(F->nranks);
+    for (int r = 0; r < F->nranks; ++r) {
+        if (r == F->rank) {
+            bases[r] = F->xb.p;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, (const char *)handles + 64 * r, 64);
+        void *p = nullptr;
+        PF_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        F->opened.push_back(p);
+        bases[r] = (double *)p;
+    }
+    F->peers_dev.alloc(F->nranks);
+    PF_CUDA(cudaMemcpy(F->peers_dev.p, bases.data(), sizeof(double *) * F->nranks, cudaMemcpyHostToDevice));
+    F->P.peers = F->peers_dev.p;
+    F->P.rank = F->rank;
+    F->P.nranks = F->nranks;
+}
+
+void fast_set_edge_counts(FastSolver *F, const double *counts) {
+    const Index &I = *F->inst->idx;
+    if (I.E) PF_CUDA(cudaMemcpy(F->ne.p, counts, sizeof(double) * I.E, cudaMemcpyHostToDevice));
 }
 
 void fast_stats(FastSolver *F, int64_t *launches, int64_t *tiles, int64_t *grid, int64_t *bytes) {

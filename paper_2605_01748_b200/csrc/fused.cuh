@@ -40,4 +40,12 @@ struct CommOps {
 };
 void fast_set_comm(FastSolver *f, const CommOps *ops);
 
+// Multi-GPU over peer memory (one process per GPU, CUDA IPC): allocate this
+// rank's exchange buffer and return its 64-byte IPC handle; connect with the
+// handles of all ranks (rank order); the suggestion divisor n_e + 1 counts the
+// paths of all ranks (kernels.py:94), set from the host.
+void fast_xchg_create(FastSolver *f, int rank, int nranks, void *handle64);
+void fast_xchg_connect(FastSolver *f, const void *handles);
+void fast_set_edge_counts(FastSolver *f, const double *counts);
+
 }  // namespace pf

@@ -4,12 +4,21 @@ One process per GPU (torchrun).  Each rank owns a contiguous range of
 commodities (split so every rank holds about the same number of demand-path
 pairs), builds the incidence store of its shard on its own GPU, and runs the
 fused solver on it.  Everything is shard-local except the per-edge sums
-T_e = sum(x + dcon') and L_e = sum(y) and the residual norms, which one NCCL
-allreduce of 2E + 16 doubles per iteration combines over NVLink
-(csrc/fused.cu, `fast_run_dist`); every rank then evaluates the same controller
-step, so all ranks take identical branches.  The dual-capacity / adjustment
-update per edge is replicated.  torch.distributed is plumbing only: it
-exchanges the NCCL unique id and gathers the final rates for the projection.
+T_e = sum(x + dcon') and L_e = sum(y) and the residual norms (2E + 16 doubles
+per iteration).  Two transports (csrc/fused.cu):
+
+* "ipc" (default): the persistent fused kernel itself writes its rank-local
+  totals into every rank's exchange buffer over NVLink peer memory (CUDA IPC)
+  and meets the other ranks at a counter barrier; every rank sums the ranks'
+  slots in rank order, so all ranks hold identical totals (deterministic, and
+  at world size 1 bitwise equal to the single-GPU kernel);
+* "nccl": split kernels around one ncclAllReduce per iteration, the loop run as
+  one CUDA graph with device-side conditions.
+
+Every rank then evaluates the same controller step, so all ranks take identical
+branches; the dual-capacity / adjustment update per edge is replicated.
+torch.distributed is plumbing only: it exchanges the IPC handles / NCCL unique
+id, sums the paths-per-edge counts once, and gathers the final rates.
 """
 
 from __future__ import annotations
@@ -103,7 +112,7 @@ class ShardedSolver:
     """Fast-mode solver over this rank's commodity shard, coupled by NCCL."""
 
     def __init__(self, topology, table: CommodityTable, flat: FlatPathSet, config: SolverConfig | None = None,
-                 rank: int = 0, world: int = 1, device: int = 0, group=None):
+                 rank: int = 0, world: int = 1, device: int = 0, group=None, transport: str | None = None):
         self.config = config if config is not None else SolverConfig(mode="fast")
         if self.config.mode != "fast":
             raise ValueError("sharded solves run in fast mode")
@@ -114,9 +123,34 @@ class ShardedSolver:
         self.instance = build_instance_flat(topology, sub_tab, sub_flat, device=device)
         self.path_ranges = kept_path_ranges(table, flat, self.ranges)
         self.solver = Solver(self.instance, self.config)
-        self.comm = Comm(rank, world, device, group)
-        n_kept = int(np.sum((np.asarray(table.demand) > 0) & (np.diff(flat.com_path_ptr) > 0)))
-        check(lib().pf_solver_attach_comm(self.solver._h, self.comm.handle, n_kept))
+        # transport: "ipc" = the fused kernel exchanges edge totals over NVLink peer
+        # memory (CUDA IPC buffers, no host round trip); "nccl" = split kernels
+        # around one ncclAllReduce per iteration, run as a CUDA graph
+        self.transport = transport or os.environ.get("PF_DIST_TRANSPORT", "ipc")
+        if self.transport == "ipc":
+            self.comm = None
+            self._connect_ipc(group)
+        elif self.transport == "nccl":
+            self.comm = Comm(rank, world, device, group)
+            n_kept = int(np.sum((np.asarray(table.demand) > 0) & (np.diff(flat.com_path_ptr) > 0)))
+            check(lib().pf_solver_attach_comm(self.solver._h, self.comm.handle, n_kept))
+        else:
+            raise ValueError(f"unknown transport {self.transport!r}")
+
+    def _connect_ipc(self, group=None):
+        import torch
+        import torch.distributed as dist
+        h = C.create_string_buffer(64)
+        check(lib().pf_solver_xchg_create(self.solver._h, self.rank, self.world, h))
+        parts = [None] * self.world
+        dist.all_gather_object(parts, bytes(h.raw), group=group)
+        allh = C.create_string_buffer(b"".join(parts), 64 * self.world)
+        check(lib().pf_solver_xchg_connect(self.solver._h, allh))
+        # n_e of kernels.py:94 counts the paths of every shard
+        ne = torch.tensor(np.asarray(self.instance.edge_path_count, np.float64))
+        dist.all_reduce(ne, group=group)
+        ne = np.ascontiguousarray(ne.numpy(), np.float64)
+        check(lib().pf_solver_set_edge_counts(self.solver._h, ne.ctypes.data_as(C.POINTER(C.c_double))))
 
     def init(self, warm_start=None):
         if warm_start is not None:
@@ -185,7 +219,11 @@ def bench_main(args, bench):
                 "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": args.config, "pairs": NPt, "parallelism": f"dp{world} (commodity shards)",
-                           "collective": "one ncclAllReduce of 2E+16 fp64 per iteration",
+                           "transport": sh.transport,
+                           "collective": ("per-iteration exchange of 2E+16 fp64 rank totals inside the fused kernel "
+                                          "over NVLink peer memory (CUDA IPC), counter barrier, rank-order sums"
+                                          if sh.transport == "ipc" else
+                                          "one ncclAllReduce of 2E+16 fp64 per iteration (CUDA-graph loop)"),
                            "l2": "inputs larger than L2 (no flush)"},
                 "roofline": {"bound": "hbm", "achieved": ach, "peak": peak * world, "unit": "GB/s",
                              "frac": ach / (peak * world), "traffic": None, "peak_kind": kind},

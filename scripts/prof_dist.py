@@ -22,10 +22,10 @@ dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, w
 topo, tab, flat = bench.build_inputs(name)
 cfg = pf.SolverConfig(mode="fast", gamma=1e-12, max_iterations=10 ** 9)
 xs = {}
-for mode in ("graph", "host"):
+for mode in ("ipc", "graph", "host"):
     if mode == "host":
         os.environ["PF_DIST_NO_GRAPH"] = "1"
-    sh = D.ShardedSolver(topo, tab, flat, cfg, 0, 1, 0).init()
+    sh = D.ShardedSolver(topo, tab, flat, cfg, 0, 1, 0, transport="ipc" if mode == "ipc" else "nccl").init()
     sh.time_loop(5)
     ms, _ = sh.time_loop(iters)
     st = sh.solver.kernel_stats()
@@ -33,9 +33,11 @@ for mode in ("graph", "host"):
           flush=True)
     xs[mode] = sh.local_x()
 print("graph == host bitwise:", bool(np.array_equal(xs["graph"], xs["host"])))
+xs_ipc = xs["ipc"]
 inst = pf.build_instance_flat(topo, tab, flat, device=0)
 f = pf.Solver(inst, cfg).init()
 f.time_loop(5)
 ms, _ = f.time_loop(iters)
 print(f"{name} fused: {iters} its {ms:.2f} ms = {1e3 * ms / iters:.1f} us/iter", flush=True)
+print("ipc == single-GPU fused bitwise:", bool(np.array_equal(xs_ipc, f.x())))
 dist.destroy_process_group()

@@ -113,7 +113,8 @@ def test_gloo_world2_id_exchange_and_shards():
 
 
 @pytest.mark.gpu
-def test_nccl_world1_matches_single_gpu():
+@pytest.mark.parametrize("transport", ["ipc", "nccl"])
+def test_world1_matches_single_gpu(transport):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -126,7 +127,7 @@ def test_nccl_world1_matches_single_gpu():
         topo = pf.random_topology(40, seed=40)
         tab = pf.gravity_table(topo, 0.3 * float(topo.capacity.sum()))
         cfg = pf.SolverConfig(mode="fast", max_iterations=5000)
-        sh = D.ShardedSolver(topo, tab, flat, cfg, 0, 1, 0).init()
+        sh = D.ShardedSolver(topo, tab, flat, cfg, 0, 1, 0, transport=transport).init()
         sh.run(5000)
         r = sh.result()
         x = sh.gather_x()
@@ -163,7 +164,7 @@ def test_nccl_world1_graph_loop_matches_host_loop(monkeypatch):
         for mode in ("graph", "host"):
             if mode == "host":
                 monkeypatch.setenv("PF_DIST_NO_GRAPH", "1")
-            sh = D.ShardedSolver(topo, tab, flat, cfg, 0, 1, 0).init()
+            sh = D.ShardedSolver(topo, tab, flat, cfg, 0, 1, 0, transport="nccl").init()
             sh.run(120)
             sh.run(180)  # two runs: the graph is relaunched with a new target
             r = sh.result()
@@ -172,5 +173,37 @@ def test_nccl_world1_graph_loop_matches_host_loop(monkeypatch):
         assert ig == ih == 300 and bg == bh
         assert np.array_equal(xg, xh)
         assert lg < 20 < lh  # the graph replaced ~5 launches per iteration
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_ipc_world1_bitwise_equals_single_gpu():
+    """The peer-memory transport: the fused kernel exchanges its rank totals
+    through its own exchange buffer at world size 1 and must reproduce the
+    single-GPU fused kernel bitwise, across launches and rollback iterations,
+    with one kernel launch per run."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.distributed as dist
+
+    import paper_2605_01748_b200 as pf
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1)
+    try:
+        topo = pf.random_topology(40, seed=40)
+        tab = pf.gravity_table(topo, 0.3 * float(topo.capacity.sum()))
+        flat = pf.k_shortest_paths(topo, tab, 4)
+        cfg = pf.SolverConfig(mode="fast", max_iterations=5000, gamma=1e-12)
+        sh = D.ShardedSolver(topo, tab, flat, cfg, 0, 1, 0, transport="ipc").init()
+        sh.run(150)
+        sh.run(150)
+        inst = pf.build_instance_flat(topo, tab, flat, device=0)
+        single = pf.Solver(inst, cfg).init()
+        single.run(300)
+        r1, r2 = sh.result(), single.result()
+        assert int(r1.iterations) == int(r2.iterations) == 300 and float(r1.beta) == float(r2.beta)
+        assert np.array_equal(sh.local_x(), single.x())
+        assert int(sh.solver.kernel_stats()["launches"]) == 2
     finally:
         dist.destroy_process_group()
