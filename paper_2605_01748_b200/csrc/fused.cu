@@ -1145,6 +1145,9 @@ __device__ void xchg_controller_eval(const Params &P, Ctrl &c) {
 
 // ------------------------------------------------------------------ kernels
 
+// DIST: the multi-GPU variant with the in-kernel peer-memory exchange (a
+// separate instantiation keeps the single-GPU kernel's registers untouched)
+template <bool DIST>
 __global__ void __launch_bounds__(NT, 2) k_fused(const __grid_constant__ Params P) {
     extern __shared__ __align__(128) char smem_raw[];
     __shared__ Ctrl c;
@@ -1154,7 +1157,7 @@ __global__ void __launch_bounds__(NT, 2) k_fused(const __grid_constant__ Params 
     uint32_t seq = 0;
     if (threadIdx.x == 0) c = *P.ctrl;
     __syncthreads();
-    const bool dist = P.nranks > 0;
+    constexpr bool dist = DIST;
     if (c.need_a1) {
         pass_tiles<MODE_A1>(P, c, smem_raw, cs, seq);
         grid.sync();
@@ -1623,12 +1626,18 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     const size_t static_smem = sizeof(Ctrl) + sizeof(CtaShared) + 64;
     require(F->smem + static_smem <= (size_t)prop.sharedMemPerBlockOptin,
             "fast mode: edge tables do not fit in shared memory (too many edges)");
-    PF_CUDA(cudaFuncSetAttribute(k_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F->smem));
+    PF_CUDA(cudaFuncSetAttribute(k_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F->smem));
+    PF_CUDA(cudaFuncSetAttribute(k_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F->smem));
     PF_CUDA(cudaFuncSetAttribute(k_pass<MODE_M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F->smem));
     PF_CUDA(cudaFuncSetAttribute(k_pass<MODE_RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F->smem));
     PF_CUDA(cudaFuncSetAttribute(k_pass<MODE_A1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F->smem));
     int per_sm = 0;
-    PF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused, NT, F->smem));
+    PF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused<false>, NT, F->smem));
+    {  // the multi-GPU variant must be co-resident with the same grid
+        int per_sm_d = 0;
+        PF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_d, k_fused<true>, NT, F->smem));
+        per_sm = std::min(per_sm, per_sm_d);
+    }
     require(per_sm >= 1, "fast kernel does not fit on an SM");
     int G = prop.multiProcessorCount * per_sm;
     G = std::max(1, std::min(G, F->L->ntiles));
@@ -1963,7 +1972,8 @@ int64_t fast_run(FastSolver *F, int64_t max_steps, cudaStream_t s, float *ms) {
                             cudaMemcpyHostToDevice, s));
     void *args[] = {(void *)&F->P};
     PF_CUDA(cudaEventRecord(F->e0, s));
-    PF_CUDA(cudaLaunchCooperativeKernel((const void *)k_fused, dim3(F->G), dim3(NT), args, F->smem, s));
+    const void *kern = F->nranks ? (const void *)k_fused<true> : (const void *)k_fused<false>;
+    PF_CUDA(cudaLaunchCooperativeKernel(kern, dim3(F->G), dim3(NT), args, F->smem, s));
     PF_CHECK_LAUNCH();
     PF_CUDA(cudaEventRecord(F->e1, s));
     ++F->launches;
