@@ -297,6 +297,25 @@ __device__ double block_sum(double v, double *red) {
     return r;  // valid in thread 0
 }
 
+// Four block reductions at once, each with block_sum's association (so the
+// results are bitwise those of four block_sum calls): valid in thread 0.
+__device__ void block_sum4(double v[4], double (*red4)[4]) {
+    for (int j = 0; j < 4; ++j)
+        for (int o = 16; o > 0; o >>= 1) v[j] += __shfl_down_sync(FULL, v[j], o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0)
+        for (int j = 0; j < 4; ++j) red4[w][j] = v[j];
+    __syncthreads();
+    if (w == 0) {
+        for (int j = 0; j < 4; ++j) {
+            double r = l < NW ? red4[l][j] : 0.0;
+            for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(FULL, r, o);
+            v[j] = r;
+        }
+    }
+}
+
 // Inclusive sum over the lane segment [first, lane] (Hillis-Steele, fixed tree),
 // then broadcast the segment total from lane `last`.
 __device__ __forceinline__ double seg_total(double v, int lane, int first, int last, int span) {
@@ -474,22 +493,30 @@ __device__ __noinline__ void edge_phase(const Params &P, double f) {
                 sT += __ldcg(&P.partT[(size_t)gg * I.E + e]);
                 sL += __ldcg(&P.partL[(size_t)gg * I.E + e]);
             }
-            P.sub[(size_t)sl * I.E + e] = sT;
-            P.sub[(size_t)(P.nslices + sl) * I.E + e] = sL;
+            if (P.nslices > 1) {
+                P.sub[(size_t)sl * I.E + e] = sT;
+                P.sub[(size_t)(P.nslices + sl) * I.E + e] = sL;
+            }
         }
-        __threadfence();
-        __syncwarp();
         int ticket = 0;
-        if (lane == 0) ticket = atomicAdd(&P.grp_count[grp], 1);
-        ticket = __shfl_sync(FULL, ticket, 0);
-        if (ticket == P.nslices - 1) {
+        if (P.nslices > 1) {  // the last slice of a group combines the slices
             __threadfence();
-            double T = 0.0, L = 0.0, rdc = 0.0;
-            if (e < I.E) {
+            __syncwarp();
+            if (lane == 0) ticket = atomicAdd(&P.grp_count[grp], 1);
+            ticket = __shfl_sync(FULL, ticket, 0);
+        }
+        if (ticket == P.nslices - 1) {
+            double T = sT, L = sL, rdc = 0.0;
+            if (P.nslices > 1) __threadfence();
+            if (e < I.E && P.nslices > 1) {
+                T = 0.0;
+                L = 0.0;
                 for (int k = 0; k < P.nslices; ++k) {
                     T += __ldcg(&P.sub[(size_t)k * I.E + e]);
                     L += __ldcg(&P.sub[(size_t)(P.nslices + k) * I.E + e]);
                 }
+            }
+            if (e < I.E) {
                 double cap = I.capacity[e];
                 double dold = __ldcg(&P.dc[e]) * f;
                 double dnew = npmax0(dold + (L - cap));
@@ -503,7 +530,7 @@ __device__ __noinline__ void edge_phase(const Params &P, double f) {
             for (int o = 16; o > 0; o >>= 1) rdc += __shfl_down_sync(FULL, rdc, o);
             if (lane == 0) {
                 P.res_dc[grp] = rdc;
-                P.grp_count[grp] = 0;
+                if (P.nslices > 1) P.grp_count[grp] = 0;
             }
         }
     }
@@ -869,6 +896,7 @@ struct CtaShared {
     PassIO io;
     Tail tails[NW];
     double red[NW];
+    double red4[NW][4];
 };
 
 // One pass over this CTA's tiles (static assignment tile = g + k*G, so every
@@ -944,17 +972,14 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
         if (MODE != MODE_RB) P.partL[(size_t)g * E + e] = v.y;
     }
     double *r = P.res + g * 8;
-    double t;
-    if (MODE == MODE_M) {
-        t = block_sum(r_x, cs.red);
-        if (tid == 0) r[0] = t;
+    double v4[4] = {r_x, r_dd, r_dcon, r_dn};
+    block_sum4(v4, cs.red4);
+    if (tid == 0) {
+        if (MODE == MODE_M) r[0] = v4[0];
+        r[1 + 3 * io.par] = v4[1];
+        r[2 + 3 * io.par] = v4[2];
+        r[3 + 3 * io.par] = v4[3];
     }
-    t = block_sum(r_dd, cs.red);
-    if (tid == 0) r[1 + 3 * io.par] = t;
-    t = block_sum(r_dcon, cs.red);
-    if (tid == 0) r[2 + 3 * io.par] = t;
-    t = block_sum(r_dn, cs.red);
-    if (tid == 0) r[3 + 3 * io.par] = t;
     // the generic-proxy stores of this pass (dual_consensus, rates, ...) are read
     // by TMA in the next pass
     fence_proxy_async();
@@ -1013,22 +1038,30 @@ __device__ __noinline__ void xchg_phase(const Params &P, Ctrl &c, cg::grid_group
                 sT += __ldcg(&P.partT[(size_t)gg * I.E + e]);
                 sL += __ldcg(&P.partL[(size_t)gg * I.E + e]);
             }
-            P.sub[(size_t)sl * I.E + e] = sT;
-            P.sub[(size_t)(P.nslices + sl) * I.E + e] = sL;
+            if (P.nslices > 1) {
+                P.sub[(size_t)sl * I.E + e] = sT;
+                P.sub[(size_t)(P.nslices + sl) * I.E + e] = sL;
+            }
         }
-        __threadfence();
-        __syncwarp();
         int ticket = 0;
-        if (lane == 0) ticket = atomicAdd(&P.grp_count[grp], 1);
-        ticket = __shfl_sync(FULL, ticket, 0);
-        if (ticket == P.nslices - 1) {
+        if (P.nslices > 1) {
             __threadfence();
+            __syncwarp();
+            if (lane == 0) ticket = atomicAdd(&P.grp_count[grp], 1);
+            ticket = __shfl_sync(FULL, ticket, 0);
+        }
+        if (ticket == P.nslices - 1) {
+            if (P.nslices > 1) __threadfence();
             wrote = true;
             if (e < I.E) {
-                double T = 0.0, L = 0.0;
-                for (int k = 0; k < P.nslices; ++k) {
-                    T += __ldcg(&P.sub[(size_t)k * I.E + e]);
-                    L += __ldcg(&P.sub[(size_t)(P.nslices + k) * I.E + e]);
+                double T = sT, L = sL;
+                if (P.nslices > 1) {
+                    T = 0.0;
+                    L = 0.0;
+                    for (int k = 0; k < P.nslices; ++k) {
+                        T += __ldcg(&P.sub[(size_t)k * I.E + e]);
+                        L += __ldcg(&P.sub[(size_t)(P.nslices + k) * I.E + e]);
+                    }
                 }
                 for (int r = 0; r < P.nranks; ++r) {
                     double *d = xb_slot(P, P.peers[r], ep, P.rank);
@@ -1036,7 +1069,7 @@ __device__ __noinline__ void xchg_phase(const Params &P, Ctrl &c, cg::grid_group
                     d[I.E + e] = L;
                 }
             }
-            if (lane == 0) P.grp_count[grp] = 0;
+            if (lane == 0 && P.nslices > 1) P.grp_count[grp] = 0;
         }
     }
     if (g == 0 && threadIdx.x < 32) {  // residual sums over the CTAs, error flags
@@ -1644,8 +1677,12 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     F->G = G;
     int ngroups = (int)((I.E + RGRP - 1) / RGRP);
     int warps = G * NW;
-    F->nslices = std::max(1, std::min(G, warps / std::max(ngroups, 1)));
-    F->nslices = std::min(F->nslices, 32);
+    // edge phase: each group's CTA partials are summed in up to 32 slices by
+    // different warps, then combined by the last slice (PF_FAST_NSLICES=1: one
+    // warp per group sums all partials -- measured equal at cfg1, 3% slower at cfg2)
+    F->nslices = std::max(1, std::min({G, 32, warps / std::max(ngroups, 1)}));
+    if (const char *v = getenv("PF_FAST_NSLICES"))
+        F->nslices = std::max(1, std::min({atoi(v), G, 32, std::max(1, warps / std::max(ngroups, 1))}));
     int64_t E = I.E ? I.E : 1;
     for (int b = 0; b < 2; ++b) {
         F->dcon[b].alloc(F->L->nslots + SLOT_ALIGN);
