@@ -187,7 +187,7 @@ struct Params {
     double gamma, residual_ratio, beta_scale, beta_min, beta_max;
     int64_t alpha_target, max_iterations;
     int32_t adapt;
-    int32_t ablate;  // tuning only (PF_FAST_ABLATE): 1 skip y/paths/commodities, 2 skip the edge scan
+    int32_t ablate;  // tuning only (PF_FAST_ABLATE): 1 skip y/paths/commodities/dcon, 2 skip the edge scan, 16 skip commodities, 32 skip K, 64 skip y
 };
 
 // ------------------------------------------------------------------ TMA / mbarrier
@@ -645,7 +645,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     if (!(P.ablate & 1)) {
     // (1) pairs: y (kernels.py:98-100); the path's rate comes from its lane
     const double xlane = gp0 + lane < gp1 ? (MODE == MODE_RB ? st.xo[gp0 + lane] : st.xk[gp0 + lane]) : 0.0;
-    pairs_y<MODE>(l0, l1, gp0, lane, xlane, spath, eid, dcon, A.adj, !P.adj_smem, ys);
+    if (!(P.ablate & 64)) pairs_y<MODE>(l0, l1, gp0, lane, xlane, spath, eid, dcon, A.adj, !P.adj_smem, ys);
     __syncwarp();
     // (2) paths (lane = path) and commodities (lane segments)
     double xnew_lane = 0.0;  // x' of this lane's path
@@ -666,7 +666,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
             double K = 0.0, wgt = 0.0;
             if (valid) {
                 const int lo = poff[p], hi = poff[p + 1];
-                K = path_k(lo, hi, ys, dcon);
+                K = (P.ablate & 32) ? 0.0 : path_k(lo, hi, ys, dcon);
                 const double dnv = st.dn[p];
                 if (xk < dnv) {  // frozen non-negativity activity (kernels.py:114-119)
                     K += dnv;
