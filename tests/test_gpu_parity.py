@@ -430,3 +430,21 @@ def test_fast_solve_projection_feasible_and_close_to_exact():
     assert pf.validate_allocation(inst, fast_rates).feasible
     np.testing.assert_allclose(fast_sums, pf.commodity_sums(inst, exact_rates), rtol=1e-6,
                                atol=1e-9 * float(np.max(np.abs(x))))
+
+
+@pytest.mark.parametrize("scale", [1e300, 1e308])
+def test_overflowing_warm_start_raises_like_exact(scale):
+    """Non-finite coefficients / roots / iterates raise KernelError (naming the
+    commodity) or SolverError exactly as the exact-order path (the reference's
+    order of checks: kernels.py:270-281 before controller.py:238-239)."""
+    inst = chain()
+    warm = np.full(inst.num_paths, scale)
+    errs = {}
+    for mode in ("exact", "fast"):
+        try:
+            pf.solve(inst, pf.SolverConfig(mode=mode, max_iterations=50), warm_start=warm)
+            errs[mode] = None
+        except (pf.KernelError, pf.SolverError) as exc:
+            errs[mode] = (type(exc), str(exc) if isinstance(exc, pf.KernelError) else None)
+    assert errs["exact"] is not None
+    assert errs["fast"] == errs["exact"]
