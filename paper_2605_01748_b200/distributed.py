@@ -179,6 +179,33 @@ class ShardedSolver:
         return np.concatenate(parts) if self.rank == 0 else None
 
 
+def consistency_check(sh, topo, tab, flat, world, rank):
+    """After a sharded run: every rank must hold the identical controller state
+    (iteration, alpha, beta, residuals -- they all evaluate the same controller
+    on the same exchanged totals), and the gathered rates, projected on rank 0,
+    must be feasible.  Raises on a mismatch (a transport bug must not pass as a
+    number)."""
+    import torch.distributed as dist
+    r = sh.result()
+    mine = (int(r.iterations), int(r.alpha), float(r.beta), int(r.converged))
+    allst = [None] * world
+    dist.all_gather_object(allst, mine)
+    if any(a != allst[0] for a in allst):
+        raise RuntimeError(f"ranks diverged: {allst}")
+    x = sh.gather_x()
+    out = {"ranks_agree": True, "state": list(allst[0])}
+    if rank == 0:
+        from .model import build_instance_flat as _bif
+        from .projection import project
+        from .model import validate_allocation
+        full = _bif(topo, tab, flat, device=sh.device)
+        rates = project(full, x, int(r.alpha))
+        out["projected_feasible"] = bool(validate_allocation(full, rates).feasible)
+        if not out["projected_feasible"]:
+            raise RuntimeError("projected sharded rates are infeasible")
+    return out
+
+
 def bench_main(args, bench):
     """bench.py --gpus N under torchrun: config 2 sharded over N GPUs (strong scaling)."""
     import json
@@ -208,6 +235,7 @@ def bench_main(args, bench):
     NP = np.array([sh.instance.num_pairs], np.int64)
     tn = torch.tensor(NP)
     dist.all_reduce(tn)
+    check_ = consistency_check(sh, topo, tab, flat, world, rank)
     if rank == 0:
         C_, P_, E_ = len(tab), int(flat.com_path_ptr[-1]), topo.num_edges
         NPt = int(tn.item())
@@ -227,7 +255,8 @@ def bench_main(args, bench):
                            "l2": "inputs larger than L2 (no flush)"},
                 "roofline": {"bound": "hbm", "achieved": ach, "peak": peak * world, "unit": "GB/s",
                              "frac": ach / (peak * world), "traffic": None, "peak_kind": kind},
-                "clocks": clk, "gpu_launches": int(st["launches"]), "max_over_ranks_ms": ms_max}
+                "clocks": clk, "gpu_launches": int(st["launches"]), "max_over_ranks_ms": ms_max,
+                "check": check_}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
     return 0
