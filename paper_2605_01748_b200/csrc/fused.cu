@@ -109,7 +109,8 @@ struct SmemPlan {
     int stage, s_dcon, s_meta, s_xk, s_xo, s_dn, s_D, s_dd;  // offsets inside a stage
     int y, adj, acc, total;                                 // offsets from the base
 };
-__host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E, int nbuf, bool adj_smem = true) {
+__host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E, int nbuf, bool adj_smem = true,
+                                                      bool acc_smem = true) {
     SmemPlan s;
     int o = 0;
     s.s_dcon = o;
@@ -132,15 +133,16 @@ __host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E, int nbuf,
     o += 8 * tps;
     s.adj = o;  // per-edge adjustment table (absent for large E: read through L1)
     if (adj_smem) o += r16(8 * E);
-    s.acc = o;  // double2 {T, L} per edge
-    o += r16(16 * E);
+    s.acc = o;  // double2 {T, L} per edge (absent for large E: the CTA's partial rows in L2)
+    if (acc_smem) o += r16(16 * E);
     s.total = o;
     return s;
 }
 
 struct TileLayout {
     int32_t ntiles = 0, tps = TPS_MIN, kspan = 1;
-    bool adj_smem = true;  // false for large E: one CTA per SM, the adjustment table read through L1
+    bool adj_smem = true;  // false for large E: the adjustment table read through L1
+    bool acc_smem = true;  // false for large E: run totals accumulate in the CTA's partial rows (L2)
     int64_t nslots = 0, meta_bytes = 0;
     DevBuf<TileDesc> desc;      // per tile
     DevBuf<uint8_t> meta;       // per-tile metadata blocks
@@ -161,6 +163,7 @@ struct Params {
     InstView I;
     int32_t ntiles, G, nslices, tps, nbuf, kspan;  // kspan: power of two >= max paths per commodity
     int32_t adj_smem;                               // adjustment table in shared memory (else L1)
+    int32_t acc_smem;                               // edge accumulators in shared memory (else L2 rows)
     // multi-GPU over peer memory (CUDA IPC): rank-local totals are written into
     // slot [rank] of every rank's exchange buffer; nranks = 0 when single-GPU
     int32_t rank, nranks;
@@ -546,15 +549,21 @@ struct Tail {
 
 struct Acc {
     double *adj, *y;
-    double2 *acc;  // per edge {T, L}
+    double2 *acc;      // per edge {T, L} in shared memory, or
+    double *gT, *gL;   // this CTA's partial rows (large E)
 };
 
 template <int MODE>
-__device__ __forceinline__ void acc_add(double2 *acc, int e, double T, double L) {
-    double2 v = acc[e];
-    v.x += T;
-    if (MODE != MODE_RB) v.y += L;
-    acc[e] = v;
+__device__ __forceinline__ void acc_add(const Acc &A, int e, double T, double L) {
+    if (A.acc) {
+        double2 v = A.acc[e];
+        v.x += T;
+        if (MODE != MODE_RB) v.y += L;
+        A.acc[e] = v;
+    } else {  // L2-resident CTA-private rows (bypass L1: it holds the adjustment table)
+        __stcg(&A.gT[e], __ldcg(&A.gT[e]) + T);
+        if (MODE != MODE_RB) __stcg(&A.gL[e], __ldcg(&A.gL[e]) + L);
+    }
 }
 
 struct Fix {
@@ -766,7 +775,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
         if (s + 1 < b) kp = skp[s + 1];  // next item's key in flight while this one computes
         const int k = (int)(cur >> 16);
         if (k != pk) {  // run head at s: the previous run ended inside the lane
-            acc_add<MODE>(A.acc, pk, cT, cL);
+            acc_add<MODE>(A, pk, cT, cL);
             cT = 0.0;
             cL = 0.0;
             pk = k;
@@ -814,7 +823,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
                     fx.L = tL;
                     fx.w = w;
                 } else {
-                    acc_add<MODE>(A.acc, pkey, tT, tL);
+                    acc_add<MODE>(A, pkey, tT, tL);
                 }
             } else if (b == s1) {
                 tails[w] = Tail{tT, tL, copen ? 1 : 0, 0};
@@ -823,7 +832,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
         // last run of a lane with a head: started inside the lane
         if (hh) {
             if (knext != pk) {
-                acc_add<MODE>(A.acc, pk, cT, cL);
+                acc_add<MODE>(A, pk, cT, cL);
             } else if (b == s1) {
                 tails[w] = Tail{cT, cL, 0, 0};
             }
@@ -842,7 +851,7 @@ __device__ __forceinline__ void apply_fix(Fix &fx, const Tail *tails, const Acc 
         cL += tails[ww].L;
         if (!tails[ww].open) break;
     }
-    acc_add<MODE>(A.acc, fx.key, cT + fx.T, cL + fx.L);
+    acc_add<MODE>(A, fx.key, cT + fx.T, cL + fx.L);
     fx.on = false;
 }
 
@@ -908,10 +917,12 @@ template <int MODE>
 __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *base, CtaShared &cs, uint32_t &seq) {
     const int g = blockIdx.x, tid = threadIdx.x;
     const int E = P.I.E;
-    const SmemPlan sp = smem_plan(P.tps, E, P.nbuf, P.adj_smem);
+    const SmemPlan sp = smem_plan(P.tps, E, P.nbuf, P.adj_smem, P.acc_smem);
     Acc A;
     A.adj = P.adj_smem ? (double *)(base + sp.adj) : P.adj;
-    A.acc = (double2 *)(base + sp.acc);
+    A.acc = P.acc_smem ? (double2 *)(base + sp.acc) : nullptr;
+    A.gT = P.partT + (size_t)g * E;
+    A.gL = P.partL + (size_t)g * E;
     A.y = (double *)(base + sp.y);
     const int t0 = P.cta_ptr[g], my = P.cta_ptr[g + 1] - t0;
     const bool rev = (c.iteration & 1) != 0;
@@ -927,7 +938,12 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
         }
     }
     for (int e = tid; e < E; e += NT) {
-        A.acc[e] = make_double2(0.0, 0.0);
+        if (P.acc_smem) {
+            A.acc[e] = make_double2(0.0, 0.0);
+        } else {
+            __stcg(&A.gT[e], 0.0);
+            if (MODE != MODE_RB) __stcg(&A.gL[e], 0.0);
+        }
         if (P.adj_smem) A.adj[e] = MODE == MODE_A1 ? 0.0 : __ldcg(&P.adj[e]);
     }
     // without the shared table adj is read through L1 (ld.global.ca); it was
@@ -967,6 +983,7 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
     }
     __syncthreads();  // last tile's fix-ups
     for (int e = tid; e < E; e += NT) {
+        if (!P.acc_smem) break;  // the rows are the partials already
         const double2 v = A.acc[e];
         P.partT[(size_t)g * E + e] = v.x;
         if (MODE != MODE_RB) P.partL[(size_t)g * E + e] = v.y;
@@ -1420,11 +1437,25 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         PF_CUDA(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, inst->device()));
         const int64_t budget = per_sm / 2 - reserved - 1024;
         if (smem_plan(1024, (int)I.E, 1).total > budget || getenv("PF_FAST_LARGE_E")) {
-            // large E: the per-edge tables rule out two CTAs per SM; run one CTA per
-            // SM with large tiles and the adjustment table read through L1
+            // large E: the shared-memory edge tables rule out two CTAs per SM; the
+            // adjustment table is read through L1 (one CTA per SM, large tiles), or
+            // the run totals also move to the CTA's private partial rows in L2
+            // (read-modify-write by one thread per run, tiles separated by block
+            // barriers: deterministic) for two CTAs per SM
+            // (measured at config 3: shared-memory accumulators at one CTA per SM
+            // 11.4 ms/iteration, L2 rows at two CTAs per SM 12.5 ms: the row
+            // read-modify-writes cost more than the second CTA gains;
+            // PF_FAST_ACC_L2=1 selects the L2 rows)
             L->adj_smem = false;
-            const int64_t budget1 = per_sm - reserved - 1024;
-            while (tps_min > 512 && smem_plan((int)tps_min, (int)I.E, 1, false).total > budget1) tps_min -= 256;
+            if (getenv("PF_FAST_ACC_L2")) {
+                L->acc_smem = false;
+                while (tps_min > 512 && smem_plan((int)tps_min, (int)I.E, 1, false, false).total > budget)
+                    tps_min -= 256;
+            } else {
+                const int64_t budget1 = per_sm - reserved - 1024;
+                while (tps_min > 512 && smem_plan((int)tps_min, (int)I.E, 1, false).total > budget1)
+                    tps_min -= 256;
+            }
         } else {
             while (tps_min > 1024 && smem_plan((int)tps_min, (int)I.E, 1).total > budget) tps_min -= 256;
         }
@@ -1653,7 +1684,7 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     }
     F->nbuf = 1;  // measured: a second stage costs an SM's second CTA, which hides more
     if (const char *v = getenv("PF_FAST_NBUF")) F->nbuf = std::max(1, std::min(2, atoi(v)));
-    F->smem = (size_t)smem_plan(F->L->tps, (int)I.E, F->nbuf, F->L->adj_smem).total;
+    F->smem = (size_t)smem_plan(F->L->tps, (int)I.E, F->nbuf, F->L->adj_smem, F->L->acc_smem).total;
     int dev = inst->device();
     const cudaDeviceProp &prop = device_props(dev);
     const size_t static_smem = sizeof(Ctrl) + sizeof(CtaShared) + 64;
@@ -1741,6 +1772,7 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     P.nbuf = F->nbuf;
     P.kspan = F->L->kspan;
     P.adj_smem = F->L->adj_smem ? 1 : 0;
+    P.acc_smem = F->L->acc_smem ? 1 : 0;
     P.pf_dist = 1;
     if (const char *v = getenv("PF_FAST_PFDIST")) P.pf_dist = std::max(1, atoi(v));
     {

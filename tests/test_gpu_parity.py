@@ -448,3 +448,28 @@ def test_overflowing_warm_start_raises_like_exact(scale):
             errs[mode] = (type(exc), str(exc) if isinstance(exc, pf.KernelError) else None)
     assert errs["exact"] is not None
     assert errs["fast"] == errs["exact"]
+
+
+def test_fast_l2_accumulators_match_exact(monkeypatch):
+    """Large-E layout with the edge run totals accumulated in the CTAs' L2 partial
+    rows (PF_FAST_LARGE_E + PF_FAST_ACC_L2): iterations 1-3 agree with the exact
+    path to 1e-10 and runs are bit-reproducible."""
+    from b200_helpers import generated
+    monkeypatch.setenv("PF_FAST_LARGE_E", "1")
+    monkeypatch.setenv("PF_FAST_ACC_L2", "1")
+    topo, tab, ps = generated(60, 8, 1.5)
+    inst = pf.build_instance(topo, tab, ps, device=0)
+    ex = pf.Solver(inst, pf.SolverConfig(mode="exact")).init()
+    fa = pf.Solver(inst, pf.SolverConfig(mode="fast")).init()
+    for it in (1, 2, 3):
+        ex.run(1)
+        fa.run(1)
+        a, b = ex.state(), fa.state()
+        for f in ("x", "y", "dual_demand", "dual_capacity", "dual_consensus", "dual_nonneg"):
+            np.testing.assert_allclose(getattr(b, f), getattr(a, f), rtol=1e-10, atol=1e-10, err_msg=f"{it} {f}")
+    r1 = pf.Solver(inst, pf.SolverConfig(mode="fast", gamma=1e-12)).init()
+    r2 = pf.Solver(inst, pf.SolverConfig(mode="fast", gamma=1e-12)).init()
+    r1.run(150)
+    r2.run(60)
+    r2.run(90)
+    assert np.array_equal(r1.x(), r2.x())
