@@ -48,6 +48,7 @@
 #include <algorithm>
 #include <array>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -190,8 +191,18 @@ struct Params {
     double gamma, residual_ratio, beta_scale, beta_min, beta_max;
     int64_t alpha_target, max_iterations;
     int32_t adapt;
+    int32_t probe;   // tuning only (PF_FAST_PROBE): iteration-phase times of CTA 0 into g_probe
     int32_t ablate;  // tuning only (PF_FAST_ABLATE): 1 skip y/paths/commodities/dcon, 2 skip the edge scan, 16 skip commodities, 32 skip K, 64 skip y
 };
+
+// Iteration-phase probe (tuning only, PF_FAST_PROBE): %globaltimer deltas of
+// CTA 0, thread 0, summed into g_probe[phase] (ns).
+__device__ unsigned long long g_probe[8];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 // ------------------------------------------------------------------ TMA / mbarrier
 
@@ -382,6 +393,15 @@ __device__ __forceinline__ double fast_commodity_term(double S, double D, double
     return gain - npmax0(S - (D - dd));
 }
 
+// Ticket for the last-slice combine: an acq_rel device-scope atomic orders this
+// warp's slice stores (made visible to lane 0 by __syncwarp) before the ticket,
+// and gives the last arriver the other slices' stores -- no full fences.
+__device__ __forceinline__ int ticket_acq_rel(int *p) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;\n" : "=r"(old) : "l"(p) : "memory");
+    return old;
+}
+
 // ------------------------------------------------------------------ controller
 
 // controller.py:237-273 on the residuals of the iteration just completed.
@@ -503,14 +523,12 @@ __device__ __noinline__ void edge_phase(const Params &P, double f) {
         }
         int ticket = 0;
         if (P.nslices > 1) {  // the last slice of a group combines the slices
-            __threadfence();
             __syncwarp();
-            if (lane == 0) ticket = atomicAdd(&P.grp_count[grp], 1);
+            if (lane == 0) ticket = ticket_acq_rel(&P.grp_count[grp]);
             ticket = __shfl_sync(FULL, ticket, 0);
         }
         if (ticket == P.nslices - 1) {
             double T = sT, L = sL, rdc = 0.0;
-            if (P.nslices > 1) __threadfence();
             if (e < I.E && P.nslices > 1) {
                 T = 0.0;
                 L = 0.0;
@@ -1062,13 +1080,12 @@ __device__ __noinline__ void xchg_phase(const Params &P, Ctrl &c, cg::grid_group
         }
         int ticket = 0;
         if (P.nslices > 1) {
-            __threadfence();
             __syncwarp();
-            if (lane == 0) ticket = atomicAdd(&P.grp_count[grp], 1);
+            if (lane == 0) ticket = ticket_acq_rel(&P.grp_count[grp]);
             ticket = __shfl_sync(FULL, ticket, 0);
         }
         if (ticket == P.nslices - 1) {
-            if (P.nslices > 1) __threadfence();
+            __syncwarp();
             wrote = true;
             if (e < I.E) {
                 double T = sT, L = sL;
@@ -1220,6 +1237,15 @@ __global__ void __launch_bounds__(NT, 2) k_fused(const __grid_constant__ Params 
         }
         __syncthreads();
     }
+    const bool prb = P.probe && blockIdx.x == 0 && threadIdx.x == 0;
+    unsigned long long pt = prb ? gtimer() : 0;
+    auto mark = [&](int i) {
+        if (prb) {
+            const unsigned long long t = gtimer();
+            g_probe[i] += t - pt;
+            pt = t;
+        }
+    };
     for (;;) {
         // the pending edge phase belongs to the next iteration: run it only when
         // continuing, so a stopped / paused state keeps adj_k for export
@@ -1229,7 +1255,9 @@ __global__ void __launch_bounds__(NT, 2) k_fused(const __grid_constant__ Params 
                 xchg_edge_apply(P, c, c.f);
             else
                 edge_phase(P, c.f);
+            mark(0);
             grid.sync();
+            mark(1);
             __syncthreads();
             if (threadIdx.x == 0) {
                 c.need_edge = 0;
@@ -1238,7 +1266,9 @@ __global__ void __launch_bounds__(NT, 2) k_fused(const __grid_constant__ Params 
             __syncthreads();
         }
         pass_tiles<MODE_M>(P, c, smem_raw, cs, seq);
+        mark(2);
         grid.sync();
+        mark(3);
         __syncthreads();
         if (threadIdx.x == 0) {
             c.iteration += 1;
@@ -1254,6 +1284,7 @@ __global__ void __launch_bounds__(NT, 2) k_fused(const __grid_constant__ Params 
         } else {
             controller_eval(P, c);
         }
+        mark(4);
         if (!c.stopped && !c.status && c.f != 1.0) {
             pass_tiles<MODE_RB>(P, c, smem_raw, cs, seq);
             grid.sync();
@@ -1815,6 +1846,7 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     P.adapt = cfg.adapt;
     P.ablate = 0;
     if (const char *v = getenv("PF_FAST_ABLATE")) P.ablate = atoi(v);
+    P.probe = getenv("PF_FAST_PROBE") ? 1 : 0;
     PF_CUDA(cudaStreamSynchronize(s));
     return F.release();
 }
@@ -2051,6 +2083,16 @@ int64_t fast_run(FastSolver *F, int64_t max_steps, cudaStream_t s, float *ms) {
     float t = 0.f;
     PF_CUDA(cudaEventElapsedTime(&t, F->e0, F->e1));
     if (ms) *ms = t;
+    if (F->P.probe) {
+        unsigned long long pr[8];
+        PF_CUDA(cudaMemcpyFromSymbol(pr, g_probe, sizeof(pr)));
+        const double n = (double)std::max<int64_t>(1, c.iteration - start);
+        fprintf(stderr, "[probe] per iteration (CTA 0): edge %.2f us, sync %.2f us, pass %.2f us, sync %.2f us, "
+                        "controller %.2f us\n", pr[0] / n / 1e3, pr[1] / n / 1e3, pr[2] / n / 1e3, pr[3] / n / 1e3,
+                pr[4] / n / 1e3);
+        unsigned long long z[8] = {0};
+        PF_CUDA(cudaMemcpyToSymbol(g_probe, z, sizeof(z)));
+    }
     return c.iteration - start;
 }
 
