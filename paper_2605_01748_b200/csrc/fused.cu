@@ -198,6 +198,7 @@ struct Params {
 // Iteration-phase probe (tuning only, PF_FAST_PROBE): %globaltimer deltas of
 // CTA 0, thread 0, summed into g_probe[phase] (ns).
 __device__ unsigned long long g_probe[8];
+__device__ unsigned long long g_pmax[3];  // per-phase max over CTAs (reset per launch read)
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -393,6 +394,45 @@ __device__ __forceinline__ double fast_commodity_term(double S, double D, double
     return gain - npmax0(S - (D - dd));
 }
 
+// Sequential sum v = p[0] + p[st] + ... + p[(n-1) st] in index order (the same
+// association as the plain loop, so bitwise the same), with the L2 loads issued
+// 8 ahead: a runtime-trip-count loop would otherwise pay one L2 round trip per term.
+__device__ __forceinline__ double sum_cg(const double *p, int n, size_t st, double v = 0.0) {
+    int k = 0;
+    for (; k + 8 <= n; k += 8) {
+        double b[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) b[u] = __ldcg(p + (size_t)(k + u) * st);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v += b[u];
+    }
+    for (; k < n; ++k) v += __ldcg(p + (size_t)k * st);
+    return v;
+}
+
+// Lane-strided sums of NV fields of the CTAs' residual records (res[g * 8 + off[j]]
+// for g = lane, lane + 32, ...), each in index order (bitwise the plain loop),
+// the loads of 4 CTAs issued ahead.
+template <int NV>
+__device__ __forceinline__ void res_sums(const double *res, int G, int lane, const int (&off)[NV], double (&acc)[NV]) {
+    for (int j = 0; j < NV; ++j) acc[j] = 0.0;
+    int g = lane;
+    for (; g + 96 < G; g += 128) {
+        double b[4][NV];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int j = 0; j < NV; ++j) b[u][j] = __ldcg(&res[(g + 32 * u) * 8 + off[j]]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int j = 0; j < NV; ++j) acc[j] += b[u][j];
+    }
+    for (; g < G; g += 32)
+#pragma unroll
+        for (int j = 0; j < NV; ++j) acc[j] += __ldcg(&res[g * 8 + off[j]]);
+}
+
 // Ticket for the last-slice combine: an acq_rel device-scope atomic orders this
 // warp's slice stores (made visible to lane 0 by __syncwarp) before the ticket,
 // and gives the last arriver the other slices' stores -- no full fences.
@@ -473,17 +513,12 @@ __device__ __noinline__ void controller_step(const Params &P, Ctrl &c, double s,
 __device__ void controller_eval(const Params &P, Ctrl &c) {
     if (threadIdx.x < 32) {
         const int par = (int)(c.iteration & 1);
-        double acc[4] = {0, 0, 0, 0};  // dx, dd, dcon, dn
-        for (int g = threadIdx.x; g < P.G; g += 32) {
-            const double *r = P.res + g * 8;
-            acc[0] += __ldcg(&r[0]);
-            acc[1] += __ldcg(&r[1 + 3 * par]);
-            acc[2] += __ldcg(&r[2 + 3 * par]);
-            acc[3] += __ldcg(&r[3 + 3 * par]);
-        }
-        double dcs = 0.0;
+        double acc[4];  // dx, dd, dcon, dn: lane-strided over the CTAs
+        const int off[4] = {0, 1 + 3 * par, 2 + 3 * par, 3 + 3 * par};
+        res_sums<4>(P.res, P.G, threadIdx.x, off, acc);
         int ngroups = (P.I.E + RGRP - 1) / RGRP;
-        for (int g = threadIdx.x; g < ngroups; g += 32) dcs += __ldcg(&P.res_dc[g]);
+        double dcs = sum_cg(P.res_dc + threadIdx.x, threadIdx.x < ngroups ? (ngroups - 1 - threadIdx.x) / 32 + 1 : 0,
+                            32);
         for (int j = 0; j < 4; ++j)
             for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_down_sync(FULL, acc[j], o);
         for (int o = 16; o > 0; o >>= 1) dcs += __shfl_down_sync(FULL, dcs, o);
@@ -512,10 +547,8 @@ __device__ __noinline__ void edge_phase(const Params &P, double f) {
         int g0 = sl * per, g1 = g0 + per < P.G ? g0 + per : P.G;
         double sT = 0.0, sL = 0.0;
         if (e < I.E) {
-            for (int gg = g0; gg < g1; ++gg) {
-                sT += __ldcg(&P.partT[(size_t)gg * I.E + e]);
-                sL += __ldcg(&P.partL[(size_t)gg * I.E + e]);
-            }
+            sT = sum_cg(&P.partT[(size_t)g0 * I.E + e], g1 - g0, I.E);
+            sL = sum_cg(&P.partL[(size_t)g0 * I.E + e], g1 - g0, I.E);
             if (P.nslices > 1) {
                 P.sub[(size_t)sl * I.E + e] = sT;
                 P.sub[(size_t)(P.nslices + sl) * I.E + e] = sL;
@@ -530,12 +563,8 @@ __device__ __noinline__ void edge_phase(const Params &P, double f) {
         if (ticket == P.nslices - 1) {
             double T = sT, L = sL, rdc = 0.0;
             if (e < I.E && P.nslices > 1) {
-                T = 0.0;
-                L = 0.0;
-                for (int k = 0; k < P.nslices; ++k) {
-                    T += __ldcg(&P.sub[(size_t)k * I.E + e]);
-                    L += __ldcg(&P.sub[(size_t)(P.nslices + k) * I.E + e]);
-                }
+                T = sum_cg(&P.sub[e], P.nslices, I.E);
+                L = sum_cg(&P.sub[(size_t)P.nslices * I.E + e], P.nslices, I.E);
             }
             if (e < I.E) {
                 double cap = I.capacity[e];
@@ -1069,10 +1098,8 @@ __device__ __noinline__ void xchg_phase(const Params &P, Ctrl &c, cg::grid_group
         const int g0 = sl * per, g1 = g0 + per < P.G ? g0 + per : P.G;
         double sT = 0.0, sL = 0.0;
         if (e < I.E) {
-            for (int gg = g0; gg < g1; ++gg) {
-                sT += __ldcg(&P.partT[(size_t)gg * I.E + e]);
-                sL += __ldcg(&P.partL[(size_t)gg * I.E + e]);
-            }
+            sT = sum_cg(&P.partT[(size_t)g0 * I.E + e], g1 - g0, I.E);
+            sL = sum_cg(&P.partL[(size_t)g0 * I.E + e], g1 - g0, I.E);
             if (P.nslices > 1) {
                 P.sub[(size_t)sl * I.E + e] = sT;
                 P.sub[(size_t)(P.nslices + sl) * I.E + e] = sL;
@@ -1090,12 +1117,8 @@ __device__ __noinline__ void xchg_phase(const Params &P, Ctrl &c, cg::grid_group
             if (e < I.E) {
                 double T = sT, L = sL;
                 if (P.nslices > 1) {
-                    T = 0.0;
-                    L = 0.0;
-                    for (int k = 0; k < P.nslices; ++k) {
-                        T += __ldcg(&P.sub[(size_t)k * I.E + e]);
-                        L += __ldcg(&P.sub[(size_t)(P.nslices + k) * I.E + e]);
-                    }
+                    T = sum_cg(&P.sub[e], P.nslices, I.E);
+                    L = sum_cg(&P.sub[(size_t)P.nslices * I.E + e], P.nslices, I.E);
                 }
                 for (int r = 0; r < P.nranks; ++r) {
                     double *d = xb_slot(P, P.peers[r], ep, P.rank);
@@ -1109,9 +1132,9 @@ __device__ __noinline__ void xchg_phase(const Params &P, Ctrl &c, cg::grid_group
     if (g == 0 && threadIdx.x < 32) {  // residual sums over the CTAs, error flags
         // same association as controller_eval (lane-strided, then a shuffle tree),
         // so one rank reproduces the single-GPU controller bitwise
-        double acc[7] = {0, 0, 0, 0, 0, 0, 0};
-        for (int gg = threadIdx.x; gg < P.G; gg += 32)
-            for (int j = 0; j < 7; ++j) acc[j] += __ldcg(&P.res[gg * 8 + j]);
+        double acc[7];
+        const int off[7] = {0, 1, 2, 3, 4, 5, 6};
+        res_sums<7>(P.res, P.G, threadIdx.x, off, acc);
         for (int j = 0; j < 7; ++j)
             for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_down_sync(FULL, acc[j], o);
         if (threadIdx.x == 0) {
@@ -1194,9 +1217,9 @@ __device__ void xchg_controller_eval(const Params &P, Ctrl &c) {
         const uint64_t ep = c.xepoch - 1;
         const int64_t b = 2 * (int64_t)P.I.E;
         const int par = (int)(c.iteration & 1);
-        double dcs = 0.0;
         const int ngroups = (P.I.E + RGRP - 1) / RGRP;
-        for (int g = threadIdx.x; g < ngroups; g += 32) dcs += __ldcg(&P.res_dc[g]);
+        double dcs = sum_cg(P.res_dc + threadIdx.x, threadIdx.x < ngroups ? (ngroups - 1 - threadIdx.x) / 32 + 1 : 0,
+                            32);
         for (int o = 16; o > 0; o >>= 1) dcs += __shfl_down_sync(FULL, dcs, o);
         if (threadIdx.x == 0) {
             const double dx = xsum(P, ep, b + 0), rdd = xsum(P, ep, b + 1 + 3 * par),
@@ -1237,12 +1260,17 @@ __global__ void __launch_bounds__(NT, 2) k_fused(const __grid_constant__ Params 
         }
         __syncthreads();
     }
-    const bool prb = P.probe && blockIdx.x == 0 && threadIdx.x == 0;
+    // CTA 0 sums its phase times into g_probe[0..4]; every CTA's per-phase time
+    // also goes into a running maximum over CTAs, summed per iteration in g_probe[5..7]
+    // (edge, pass, controller) by CTA 0 (approximate: the max of the previous iteration)
+    const bool prb = P.probe && threadIdx.x == 0;
     unsigned long long pt = prb ? gtimer() : 0;
     auto mark = [&](int i) {
         if (prb) {
             const unsigned long long t = gtimer();
-            g_probe[i] += t - pt;
+            if (blockIdx.x == 0) g_probe[i] += t - pt;
+            const int slot = i == 0 ? 0 : i == 2 ? 1 : i == 4 ? 2 : -1;
+            if (slot >= 0) atomicMax(&g_pmax[slot], t - pt);
             pt = t;
         }
     };
@@ -1328,13 +1356,8 @@ __global__ void __launch_bounds__(NT, 2) k_pass(const __grid_constant__ Params P
 __global__ void k_local_reduce(const __grid_constant__ Params P) {
     const int E = P.I.E;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
-        double t = 0.0, l = 0.0;
-        for (int g = 0; g < P.G; ++g) {
-            t += __ldcg(&P.partT[(size_t)g * E + e]);
-            l += __ldcg(&P.partL[(size_t)g * E + e]);
-        }
-        P.tot[e] = t;
-        P.tot[E + e] = l;
+        P.tot[e] = sum_cg(&P.partT[e], P.G, E);
+        P.tot[E + e] = sum_cg(&P.partL[e], P.G, E);
     }
     if (blockIdx.x == 0 && threadIdx.x < 7) {
         double r = 0.0;
@@ -2087,9 +2110,14 @@ int64_t fast_run(FastSolver *F, int64_t max_steps, cudaStream_t s, float *ms) {
         unsigned long long pr[8];
         PF_CUDA(cudaMemcpyFromSymbol(pr, g_probe, sizeof(pr)));
         const double n = (double)std::max<int64_t>(1, c.iteration - start);
+        unsigned long long mx[3];
+        PF_CUDA(cudaMemcpyFromSymbol(mx, g_pmax, sizeof(mx)));
         fprintf(stderr, "[probe] per iteration (CTA 0): edge %.2f us, sync %.2f us, pass %.2f us, sync %.2f us, "
+                        "controller %.2f us; max over CTAs and iterations: edge %.2f us, pass %.2f us, "
                         "controller %.2f us\n", pr[0] / n / 1e3, pr[1] / n / 1e3, pr[2] / n / 1e3, pr[3] / n / 1e3,
-                pr[4] / n / 1e3);
+                pr[4] / n / 1e3, mx[0] / 1e3, mx[1] / 1e3, mx[2] / 1e3);
+        unsigned long long zm[3] = {0, 0, 0};
+        PF_CUDA(cudaMemcpyToSymbol(g_pmax, zm, sizeof(zm)));
         unsigned long long z[8] = {0};
         PF_CUDA(cudaMemcpyToSymbol(g_probe, z, sizeof(z)));
     }
