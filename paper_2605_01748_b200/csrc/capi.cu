@@ -1,3 +1,4 @@
+#include <cstdio>
 // C-ABI entry points: kernel-level functions, projection, and the solve loop.
 //
 // pf_solve / pf_solver_* reproduce pathfair/controller.py:197-284:
@@ -176,6 +177,10 @@ static void solver_init(pf_solver *S, const double *warm) {
     InstView I = S->inst->view();
     cudaStream_t st = S->stream;
     S->t0 = wall();
+    static const bool timing = getenv("PF_TIMING") != nullptr;
+    auto lap = [&](const char *what) {
+        if (timing) fprintf(stderr, "[solver_init] %s at %.2f ms\n", what, 1e3 * (wall() - S->t0));
+    };
     S->trace.clear();
     S->loop_ms = S->proj_ms = 0.0;
     S->status = PF_OK;
@@ -184,29 +189,41 @@ static void solver_init(pf_solver *S, const double *warm) {
     HostCtrl c;
     c.beta = S->cfg.beta0;
     if (warm) {  // controller.py:104-111
-        for (int64_t p = 0; p < S->P(); ++p)
-            require(std::isfinite(warm[p]), "warm start contains non-finite rates");
+        bool finite = true;
+        for (int64_t p = 0; p < S->P(); ++p) finite = finite && std::isfinite(warm[p]);
+        require(finite, "warm start contains non-finite rates");
         c.alpha = S->cfg.alpha_target >= 0 ? S->cfg.alpha_target : 0;
     }
     S->ctrl = c;
-    DevBuf<double> x0(S->P() ? S->P() : 1);
+    lap("checks");
+    DevBuf<double> x0own;
+    double *x0 = nullptr;
+    if (S->cfg.mode == PF_MODE_FAST) {
+        x0 = fast_scratch(S->fast, 0);  // pooled with the solver: no allocation per solve
+    } else {
+        x0own.alloc(S->P() ? S->P() : 1);
+        x0 = x0own.p;
+    }
+    lap("x0 alloc");
     if (warm)
-        h2d(x0.p, warm, S->P(), st);
+        h2d(x0, warm, S->P(), st);
     else if (I.P)
-        k_init_cold<<<ceil_div(I.P, 256), 256, 0, st>>>(I, x0.p);
+        k_init_cold<<<ceil_div(I.P, 256), 256, 0, st>>>(I, x0);
     PF_CHECK_LAUNCH();
     if (S->cfg.mode == PF_MODE_EXACT) {
-        PF_CUDA(cudaMemcpyAsync(S->cur.x.p, x0.p, sizeof(double) * S->P(), cudaMemcpyDeviceToDevice, st));
-        if (I.NP) k_gather_pairs<<<ceil_div(I.NP, 256), 256, 0, st>>>(I, x0.p, S->cur.y.p);
+        PF_CUDA(cudaMemcpyAsync(S->cur.x.p, x0, sizeof(double) * S->P(), cudaMemcpyDeviceToDevice, st));
+        if (I.NP) k_gather_pairs<<<ceil_div(I.NP, 256), 256, 0, st>>>(I, x0, S->cur.y.p);
         PF_CHECK_LAUNCH();
         PF_CUDA(cudaMemsetAsync(S->cur.dd.p, 0, sizeof(double) * S->C(), st));
         PF_CUDA(cudaMemsetAsync(S->cur.dc.p, 0, sizeof(double) * S->E(), st));
         PF_CUDA(cudaMemsetAsync(S->cur.dcon.p, 0, sizeof(double) * S->NP(), st));
         PF_CUDA(cudaMemsetAsync(S->cur.dn.p, 0, sizeof(double) * S->P(), st));
     } else {
-        fast_init(S->fast, x0.p, c.alpha, c.beta, st);
+        lap("h2d issued");
+        fast_init(S->fast, x0, c.alpha, c.beta, st);
     }
     PF_CUDA(cudaStreamSynchronize(st));
+    lap("fast_init + sync");
     S->initialized = true;
 }
 
@@ -394,18 +411,26 @@ static void solver_finish(pf_solver *S, double *rates, double *sums) {
         }
     }
     int64_t alpha = S->cfg.mode == PF_MODE_EXACT ? S->ctrl.alpha : fast_status(S->fast, st).alpha;
-    if (S->rates_out.n < (size_t)S->P()) S->rates_out.alloc(S->P());
-    if (S->sums_out.n < (size_t)S->C() + 1) S->sums_out.alloc(S->C() + 1);
+    double *rates_d, *sums_d;
+    if (S->cfg.mode == PF_MODE_FAST) {  // pooled with the solver
+        rates_d = fast_scratch(S->fast, 1);
+        sums_d = fast_scratch(S->fast, 2);
+    } else {
+        if (S->rates_out.n < (size_t)S->P()) S->rates_out.alloc(S->P());
+        if (S->sums_out.n < (size_t)S->C() + 1) S->sums_out.alloc(S->C() + 1);
+        rates_d = S->rates_out.p;
+        sums_d = S->sums_out.p;
+    }
     PF_CUDA(cudaEventRecord(S->ev0, st));
     if (S->cfg.project)
-        project_device(S->inst, solver_x(S), alpha, S->rates_out.p, st,
+        project_device(S->inst, solver_x(S), alpha, rates_d, st,
                        S->cfg.mode == PF_MODE_FAST);  // controller.py:275
     else
-        PF_CUDA(cudaMemcpyAsync(S->rates_out.p, solver_x(S), sizeof(double) * S->P(), cudaMemcpyDeviceToDevice, st));
-    exact_commodity_sums(I, S->rates_out.p, S->sums_out.p, st);
+        PF_CUDA(cudaMemcpyAsync(rates_d, solver_x(S), sizeof(double) * S->P(), cudaMemcpyDeviceToDevice, st));
+    exact_commodity_sums(I, rates_d, sums_d, st);
     PF_CUDA(cudaEventRecord(S->ev1, st));
-    if (rates) d2h(rates, S->rates_out.p, S->P(), st);
-    if (sums) d2h(sums, S->sums_out.p, S->C(), st);
+    if (rates) d2h(rates, rates_d, S->P(), st);
+    if (sums) d2h(sums, sums_d, S->C(), st);
     PF_CUDA(cudaStreamSynchronize(st));
     float ms = 0.f;
     PF_CUDA(cudaEventElapsedTime(&ms, S->ev0, S->ev1));
@@ -840,11 +865,20 @@ int pf_solve(const pf_instance *inst, const pf_config *cfg, const double *warm, 
     pf_solver *S = nullptr;
     int st = guard([&] {
         require(inst && cfg && res, "null argument");
+        static const bool timing = getenv("PF_TIMING") != nullptr;  // tuning: phase wall times
+        const double t0 = wall();
         S = solver_create(inst, cfg);
+        const double t1 = wall();
         solver_init(S, warm);
+        const double t2 = wall();
         if (S->P() > 0) solver_run(S, cfg->max_iterations);
+        const double t3 = wall();
         solver_finish(S, rates, sums);
+        const double t4 = wall();
         solver_status(S, res);
+        if (timing)
+            fprintf(stderr, "[pf_solve] create %.2f ms, init %.2f ms, run %.2f ms, finish %.2f ms\n",
+                    1e3 * (t1 - t0), 1e3 * (t2 - t1), 1e3 * (t3 - t2), 1e3 * (t4 - t3));
         if (trace && trace_len) {
             int64_t n = (int64_t)S->trace.size() < trace_cap ? (int64_t)S->trace.size() : trace_cap;
             std::memcpy(trace, S->trace.data(), sizeof(pf_trace_row) * (size_t)n);
@@ -859,7 +893,9 @@ int pf_solve(const pf_instance *inst, const pf_config *cfg, const double *warm, 
     if (S) {
         char keep[1024];
         pf_last_error(keep, sizeof keep);
+        const double t5 = wall();
         solver_destroy(S);
+        if (getenv("PF_TIMING")) fprintf(stderr, "[pf_solve] destroy %.2f ms\n", 1e3 * (wall() - t5));
         set_error(keep);
     }
     return st;

@@ -1668,6 +1668,8 @@ struct FastSolver {
     DevBuf<double *> peers_dev;              // [nranks] peer bases
     std::vector<void *> opened;              // IPC mappings to close
     DevBuf<unsigned long long> xepoch;       // exchanges done
+    // per-solve scratch kept with the (pooled) solver: warm-start staging, outputs
+    DevBuf<double> x0stage, rates_out, sums_out;
 };
 
 static void fast_set_config(FastSolver *F, const pf_config &cfg) {
@@ -2220,6 +2222,14 @@ void fast_xchg_connect(FastSolver *F, const void *handles) {
 void fast_set_edge_counts(FastSolver *F, const double *counts) {
     const Index &I = *F->inst->idx;
     if (I.E) PF_CUDA(cudaMemcpy(F->ne.p, counts, sizeof(double) * I.E, cudaMemcpyHostToDevice));
+}
+
+double *fast_scratch(FastSolver *F, int which) {
+    const Index &I = *F->inst->idx;
+    DevBuf<double> &b = which == 0 ? F->x0stage : which == 1 ? F->rates_out : F->sums_out;
+    const size_t n = (size_t)std::max<int64_t>(1, which == 2 ? I.C + 1 : I.P);
+    if (b.n < n) b.alloc(n);
+    return b.p;
 }
 
 void fast_stats(FastSolver *F, int64_t *launches, int64_t *tiles, int64_t *grid, int64_t *bytes) {
