@@ -351,7 +351,19 @@ __device__ double cta_sum_tree(double v, double *red) {
 
 __device__ double cta_edge_resum_fast(const int32_t *epath, const double *x, int32_t lo, int32_t hi, double *red) {
     double v = 0.0;
-    for (int32_t t = lo + threadIdx.x; t < hi; t += blockDim.x) v += x[epath[t]];
+    const int32_t nt = blockDim.x;
+    int32_t t = lo + threadIdx.x;
+    for (; t + 7 * nt < hi; t += 8 * nt) {  // 8 independent gathers in flight
+        int32_t pi[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) pi[u] = epath[t + u * nt];
+        double xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xv[u] = x[pi[u]];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v += xv[u];
+    }
+    for (; t < hi; t += nt) v += x[epath[t]];
     return cta_sum_tree(v, red);
 }
 
