@@ -84,7 +84,7 @@ struct pf_solver {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // exact mode
     DevState cur, nxt;
-    DevBuf<double> sums_tmp, loads_tmp, pk, pw, wsum, q, root_sums, sqtmp, norms;
+    DevBuf<double> sums_tmp, loads_tmp, pk, pw, wsum, q, root_sums, sqtmp, norms, svals;
     DevBuf<Flags> flags;
     HostCtrl ctrl;
     // fast mode
@@ -237,7 +237,7 @@ static bool exact_step(pf_solver *S) {
     exact_update_duals(I, s0, S->sums_tmp.p, S->loads_tmp.p, nxt.dd.p, nxt.dc.p, nxt.dcon.p, nxt.dn.p, st);
     // update_slacks (controller.py:228) is bookkeeping never read by the loop; skipped.
     StatePtrs s1{cur.x.p, cur.y.p, nxt.dd.p, nxt.dc.p, nxt.dcon.p, nxt.dn.p};
-    exact_suggest(I, s1, nxt.y.p, st);
+    exact_suggest(I, s1, nxt.y.p, st, S->svals.p);
     StatePtrs s2{cur.x.p, nxt.y.p, nxt.dd.p, nxt.dc.p, nxt.dcon.p, nxt.dn.p};
     exact_coefficients(I, s2, S->pk.p, S->pw.p, S->wsum.p, S->q.p, st);
     reset_flags(S->flags.p, st);
@@ -461,6 +461,7 @@ static pf_solver *solver_create(const pf_instance *inst, const pf_config *cfg) {
         S->nxt.alloc(I);
         S->sums_tmp.alloc(I.C + 1);
         S->loads_tmp.alloc(I.E + 1);
+        S->svals.alloc(I.NP + 1);
         S->pk.alloc(I.P + 1);
         S->pw.alloc(I.P + 1);
         S->wsum.alloc(I.C + 1);
@@ -626,8 +627,8 @@ int pf_update_rate_suggestions(const pf_instance *inst, const pf_state_view *v, 
         const Index &I = *inst->idx;
         cudaStream_t s = inst->stream;
         Upload U(inst, v, s);
-        DevBuf<double> oy(I.NP + 1);
-        exact_suggest(inst->view(), U.ptrs, oy.p, s);
+        DevBuf<double> oy(I.NP + 1), sv(I.NP + 1);
+        exact_suggest(inst->view(), U.ptrs, oy.p, s, sv.p);
         d2h(y, oy.p, I.NP, s);
         PF_CUDA(cudaStreamSynchronize(s));
     });

@@ -104,6 +104,50 @@ __global__ void k_slack_sc(int32_t E, const double *dc, double beta, const doubl
     if (e < E) out[e] = npmax0(dc[e] / beta + (cap[e] - loads[e]));
 }
 
+// kernels.py:90-91 values of _k_suggest's per-edge sums, x[pair_path] + dcon',
+// laid out in edge-major order (one thread per edge-major position: the same
+// single addition the sequential walk does)
+__global__ void k_suggest_vals(InstView I, const double *__restrict__ x, const double *__restrict__ dcon,
+                               double *__restrict__ vals) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= I.NP) return;
+    const int32_t pr = I.edge_pairs[t];
+    vals[t] = x[I.pair_path[pr]] + dcon[pr];
+}
+
+// kernels.py:88-100 from the edge-major values: lane 0 of the edge's warp walks
+// the sequential total (ascending pair order, exactly the reference's chain)
+// over the contiguous values with 8 loads in flight; then the warp writes y.
+__global__ void k_suggest_seq(InstView I, const double *__restrict__ vals, const double *__restrict__ dc,
+                              double *__restrict__ y) {
+    const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (e >= I.E) return;
+    const int32_t lo = I.edge_pair_ptr[e], hi = I.edge_pair_ptr[e + 1];
+    if (hi == lo) return;
+    // the warp loads 32-value chunks two ahead (coalesced); every lane adds the
+    // current chunk's values in order via shuffles (identical totals on all lanes)
+    double total = 0.0;
+    double v0 = lo + lane < hi ? vals[lo + lane] : 0.0;
+    double v1 = lo + 32 + lane < hi ? vals[lo + 32 + lane] : 0.0;
+    for (int32_t base = lo; base < hi; base += 32) {
+        const int32_t t2 = base + 64 + lane;
+        const double v2 = t2 < hi ? vals[t2] : 0.0;
+        const int n = hi - base < 32 ? hi - base : 32;
+        if (n == 32) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) total += __shfl_sync(0xffffffffu, v0, j);
+        } else {
+            for (int j = 0; j < n; ++j) total += __shfl_sync(0xffffffffu, v0, j);
+        }
+        v0 = v1;
+        v1 = v2;
+    }
+    double adjust = (total + dc[e] - I.capacity[e]) / ((double)I.edge_path_count[e] + 1.0);
+    if (adjust < 0.0) adjust = 0.0;
+    for (int32_t t = lo + lane; t < hi; t += 32) y[I.edge_pairs[t]] = max0(vals[t] - adjust);
+}
+
 // kernels.py:76-100 _k_suggest: warp per edge; the per-edge total is one
 // sequential chain (total += x + dcon) walked 32 gathered values at a time.
 __global__ void k_suggest(InstView I, const double *__restrict__ x, const double *__restrict__ dcon,
@@ -369,8 +413,14 @@ void exact_update_slacks(const InstView &I, const StatePtrs &st, double beta, do
     PF_CHECK_LAUNCH();
 }
 
-void exact_suggest(const InstView &I, const StatePtrs &st, double *y_out, cudaStream_t s) {
-    if (I.E) k_suggest<<<ceil_div((int64_t)I.E * 32, 128), 128, 0, s>>>(I, st.x, st.dcon, st.dc, y_out);
+void exact_suggest(const InstView &I, const StatePtrs &st, double *y_out, cudaStream_t s, double *scratch) {
+    if (!I.E) return;
+    if (scratch && I.NP) {  // parallel value pass, then the sequential totals over a contiguous array
+        k_suggest_vals<<<ceil_div(I.NP, 256), 256, 0, s>>>(I, st.x, st.dcon, scratch);
+        k_suggest_seq<<<ceil_div((int64_t)I.E * 32, 128), 128, 0, s>>>(I, scratch, st.dc, y_out);
+    } else {
+        k_suggest<<<ceil_div((int64_t)I.E * 32, 128), 128, 0, s>>>(I, st.x, st.dcon, st.dc, y_out);
+    }
     PF_CHECK_LAUNCH();
 }
 

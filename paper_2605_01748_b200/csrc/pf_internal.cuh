@@ -223,7 +223,9 @@ void exact_update_duals(const InstView &I, const StatePtrs &st, double *sums_tmp
                         double *dc, double *dcon, double *dn, cudaStream_t s);
 void exact_update_slacks(const InstView &I, const StatePtrs &st, double beta, double *sums_tmp, double *loads_tmp,
                          double *sd, double *sc, cudaStream_t s);
-void exact_suggest(const InstView &I, const StatePtrs &st, double *y_out, cudaStream_t s);
+// scratch: optional [NP] doubles (edge-major values; faster sequential chains)
+void exact_suggest(const InstView &I, const StatePtrs &st, double *y_out, cudaStream_t s,
+                   double *scratch = nullptr);
 void exact_coefficients(const InstView &I, const StatePtrs &st, double *pk, double *pw, double *wsum, double *q,
                         cudaStream_t s);
 void exact_roots(const InstView &I, const double *wsum, const double *q, const double *dd, double beta,
