@@ -234,7 +234,8 @@ static bool exact_step(pf_solver *S) {
     HostCtrl &c = S->ctrl;
     DevState &cur = S->cur, &nxt = S->nxt;
     StatePtrs s0{cur.x.p, cur.y.p, cur.dd.p, cur.dc.p, cur.dcon.p, cur.dn.p};
-    exact_update_duals(I, s0, S->sums_tmp.p, S->loads_tmp.p, nxt.dd.p, nxt.dc.p, nxt.dcon.p, nxt.dn.p, st);
+    exact_update_duals(I, s0, S->sums_tmp.p, S->loads_tmp.p, nxt.dd.p, nxt.dc.p, nxt.dcon.p, nxt.dn.p, st,
+                       S->svals.p);
     // update_slacks (controller.py:228) is bookkeeping never read by the loop; skipped.
     StatePtrs s1{cur.x.p, cur.y.p, nxt.dd.p, nxt.dc.p, nxt.dcon.p, nxt.dn.p};
     exact_suggest(I, s1, nxt.y.p, st, S->svals.p);

@@ -104,6 +104,41 @@ __global__ void k_slack_sc(int32_t E, const double *dc, double beta, const doubl
     if (e < E) out[e] = npmax0(dc[e] / beta + (cap[e] - loads[e]));
 }
 
+// edge-major copy of a per-pair array: vals[t] = pv[edge_pairs[t]]
+__global__ void k_gather_edge_major(InstView I, const double *__restrict__ pv, double *__restrict__ vals) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < I.NP) vals[t] = pv[I.edge_pairs[t]];
+}
+
+// _reduce.py:60-65 over an edge-major contiguous array: one warp per edge,
+// lane j sums the j-th 32-element chunk of each 1024-block (a full chunk's 32
+// loads are independent of the sum and issue together), chunk partials added in
+// chunk order -- the same association as k_edge_gather_blk.
+__global__ void k_edge_blk_contig(InstView I, const double *__restrict__ vals, double *__restrict__ out) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= I.E) return;
+    const int64_t lo = I.edge_pair_ptr[warp], hi = I.edge_pair_ptr[warp + 1];
+    double total = 0.0;
+    for (int64_t base = lo; base < hi; base += BLK * 32) {
+        const int64_t cs = base + (int64_t)lane * BLK;
+        double part = 0.0;
+        if (cs + BLK <= hi) {
+            double b[BLK];
+#pragma unroll
+            for (int u = 0; u < BLK; ++u) b[u] = vals[cs + u];
+#pragma unroll
+            for (int u = 0; u < BLK; ++u) part += b[u];
+        } else if (cs < hi) {
+            for (int64_t t = cs; t < hi; ++t) part += vals[t];
+        }
+        const int64_t rem = hi - base;
+        const int nch = rem >= BLK * 32 ? 32 : (int)((rem + BLK - 1) / BLK);
+        for (int j = 0; j < nch; ++j) total += __shfl_sync(0xffffffffu, part, j);
+    }
+    if (lane == 0) out[warp] = total;
+}
+
 // kernels.py:90-91 values of _k_suggest's per-edge sums, x[pair_path] + dcon',
 // laid out in edge-major order (one thread per edge-major position: the same
 // single addition the sequential walk does)
@@ -394,9 +429,14 @@ void exact_edge_loads_of_rates(const InstView &I, const double *rates, double *o
 }
 
 void exact_update_duals(const InstView &I, const StatePtrs &st, double *sums, double *loads, double *dd, double *dc,
-                        double *dcon, double *dn, cudaStream_t s) {
+                        double *dcon, double *dn, cudaStream_t s, double *scratch) {
     exact_commodity_sums(I, st.x, sums, s);
-    exact_edge_loads_from_pairs(I, st.y, loads, s);
+    if (scratch && I.NP && I.E) {  // edge-major copy, then blocked sums over contiguous memory
+        k_gather_edge_major<<<ceil_div(I.NP, 256), 256, 0, s>>>(I, st.y, scratch);
+        k_edge_blk_contig<<<ceil_div((int64_t)I.E * 32, 128), 128, 0, s>>>(I, scratch, loads);
+    } else {
+        exact_edge_loads_from_pairs(I, st.y, loads, s);
+    }
     if (I.C) k_dual_dd<<<ceil_div(I.C, TB), TB, 0, s>>>(I.C, st.dd, sums, I.demand, dd);
     if (I.E) k_dual_dc<<<ceil_div(I.E, TB), TB, 0, s>>>(I.E, st.dc, loads, I.capacity, dc);
     if (I.NP) k_dual_dcon<<<ceil_div(I.NP, TB), TB, 0, s>>>(I.NP, st.dcon, st.x, I.pair_path, st.y, dcon);

@@ -220,7 +220,7 @@ void exact_commodity_sums(const InstView &I, const double *x, double *out, cudaS
 void exact_edge_loads_from_pairs(const InstView &I, const double *pair_vals, double *out, cudaStream_t s);
 void exact_edge_loads_of_rates(const InstView &I, const double *rates, double *out, cudaStream_t s);
 void exact_update_duals(const InstView &I, const StatePtrs &st, double *sums_tmp, double *loads_tmp, double *dd,
-                        double *dc, double *dcon, double *dn, cudaStream_t s);
+                        double *dc, double *dcon, double *dn, cudaStream_t s, double *scratch = nullptr);
 void exact_update_slacks(const InstView &I, const StatePtrs &st, double beta, double *sums_tmp, double *loads_tmp,
                          double *sd, double *sc, cudaStream_t s);
 // scratch: optional [NP] doubles (edge-major values; faster sequential chains)
