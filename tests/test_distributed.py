@@ -207,3 +207,57 @@ def test_ipc_world1_bitwise_equals_single_gpu():
         assert int(sh.solver.kernel_stats()["launches"]) == 2
     finally:
         dist.destroy_process_group()
+
+
+def _ipc_rank_worker(rank, world, port, iters, q):
+    import torch.distributed as dist
+
+    import paper_2605_01748_b200 as pf
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        topo = pf.random_topology(24, seed=24)
+        tab = pf.gravity_table(topo, 0.3 * float(topo.capacity.sum()))
+        flat = pf.k_shortest_paths(topo, tab, 4)
+        cfg = pf.SolverConfig(mode="fast", gamma=1e-12, max_iterations=10 ** 6)
+        sh = D.ShardedSolver(topo, tab, flat, cfg, rank, world, 0, transport="ipc").init()
+        sh.run(iters)
+        r = sh.result()
+        x = sh.gather_x()
+        single = None
+        if rank == 0:
+            inst = pf.build_instance_flat(topo, tab, flat, device=0)
+            s1 = pf.Solver(inst, cfg).init()
+            s1.run(iters)
+            single = s1.x()
+        q.put((rank, int(r.iterations), float(r.beta), int(r.alpha), x, single))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_ipc_multirank_on_one_gpu(world):
+    """Real multi-rank exchange of the peer-memory transport: `world` processes
+    on the one B200 (the driver time-slices their cooperative kernels), shards
+    of a 24-node instance.  Every rank must end with the identical controller
+    state and the gathered rates must equal the single-GPU solve at the same
+    iteration count up to the reassociated edge sums."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_ipc_rank_worker, args=(r, world, port, 40, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
+    for p in ps:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in ps)
+    states = [t[1:4] for t in res]
+    assert all(s == states[0] for s in states) and states[0][0] == 40
+    xg, xs = res[0][4], res[0][5]
+    assert xg.shape == xs.shape
+    assert float(np.max(np.abs(xg - xs))) <= 1e-6 * float(np.max(np.abs(xs)))
