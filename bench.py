@@ -62,6 +62,11 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("PF_BENCH_SHARE_GPU") == "1":
+        # test hook: time-slice several ranks on the GPUs present (the line then
+        # says so in config.shared_gpus); never set by the driver
+        import torch
+        local %= max(1, torch.cuda.device_count())
     return rank, world, local
 
 
@@ -82,7 +87,9 @@ def build_inputs(name):
         log(f"[bench] k_shortest_paths({name}) {time.perf_counter() - t:.1f}s (native, {os.cpu_count()} threads)")
         try:
             os.makedirs(os.path.dirname(cache), exist_ok=True)
-            np.savez(cache, cpp=flat.com_path_ptr, pep=flat.path_edge_ptr, pe=flat.path_edges)
+            tmp = f"{cache}.{os.getpid()}.tmp.npz"  # atomic: ranks may race on the cache
+            np.savez(tmp, cpp=flat.com_path_ptr, pep=flat.path_edge_ptr, pe=flat.path_edges)
+            os.replace(tmp, cache)
         except OSError:
             pass
     return topo, tab, flat

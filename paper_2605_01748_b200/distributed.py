@@ -276,7 +276,9 @@ def bench_main(args, bench):
                                           "over NVLink peer memory (CUDA IPC), counter barrier, rank-order sums"
                                           if sh.transport == "ipc" else
                                           "one ncclAllReduce of 2E+16 fp64 per iteration (CUDA-graph loop)"),
-                           "l2": "inputs larger than L2 (no flush)"},
+                           "l2": "inputs larger than L2 (no flush)",
+                           **({"shared_gpus": torch.cuda.device_count()}
+                              if os.environ.get("PF_BENCH_SHARE_GPU") == "1" else {})},
                 "roofline": {"bound": "hbm", "achieved": ach, "peak": peak * world, "unit": "GB/s",
                              "frac": ach / (peak * world), "traffic": None, "peak_kind": kind},
                 "clocks": clk, "gpu_launches": int(st["launches"]), "max_over_ranks_ms": ms_max,
