@@ -388,7 +388,9 @@ def run_b200(args):
     stats = solver.kernel_stats()
 
     # e2e through the C-ABI with host buffers (pf_solve: H2D warm start, K its, projection, D2H)
-    warm = solver.x()
+    # the step's input (warm-start rates) in pinned host memory
+    warm = torch.empty(P, dtype=torch.float64).pin_memory().numpy()
+    warm[:] = solver.x()
     e2e_cfg = pf.SolverConfig(mode="fast", gamma=1e-12, max_iterations=args.steps)
     pf.solve(inst, pf.SolverConfig(mode="fast", gamma=1e-12, max_iterations=3), warm_start=warm)  # warm
     torch.cuda.synchronize()
@@ -397,7 +399,7 @@ def run_b200(args):
     e2e_s = time.perf_counter() - t
     e2e = {"value": args.steps / e2e_s, "unit": "iterations/s", "h2d_bytes_per_step": 8 * P / args.steps,
            "d2h_bytes_per_step": 8 * (P + C) / args.steps, "projection_ms": res.projection_ms,
-           "call": "pf_solve (host warm start -> K iterations -> GPU projection -> host rates/sums)"}
+           "call": "pf_solve (pinned host warm start -> K iterations -> GPU projection -> host rates/sums)"}
 
     cpu = cpu_baseline(flat, tab, topo) if (rank == 0 and not args.no_cpu_baseline) else None
     ttq = None

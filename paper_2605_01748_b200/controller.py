@@ -119,9 +119,9 @@ def _check_warm(instance, warm_start):
     x = np.ascontiguousarray(warm_start, np.float64)
     if x.shape != (instance.num_paths,):
         raise InputError(f"warm start has {x.shape[0]} rates, expected {instance.num_paths}")
-    if not np.all(np.isfinite(x)):
-        raise InputError("warm start contains non-finite rates")
-    return x.copy()
+    # finiteness (controller.py:104-111) is checked by the native init on the
+    # device copy; the array is only read during the call, so no copy here
+    return x
 
 
 def _raise(instance, rc, res_bad, it):
@@ -154,6 +154,8 @@ def solve(instance: Instance, config: SolverConfig | None = None, warm_start=Non
     keep = []
     cfg = config.to_c(keep=keep)
     if config.reference_sums is not None and np.asarray(config.reference_sums).shape != (instance.num_commodities,):
+        if warm is not None and not np.all(np.isfinite(warm)):  # the reference checks the warm start first
+            raise InputError("warm start contains non-finite rates")
         raise InputError("commodity sets differ between allocation and reference")
     rates = np.empty(instance.num_paths)
     sums = np.empty(instance.num_commodities)
@@ -193,7 +195,7 @@ class Solver:
 
     def init(self, warm_start=None):
         warm = _check_warm(self.instance, warm_start)
-        check(lib().pf_solver_init(self._h, _p(warm) if warm is not None else None))
+        _raise(self.instance, lib().pf_solver_init(self._h, _p(warm) if warm is not None else None), -1, 0)
         return self
 
     def run(self, steps: int) -> int:

@@ -172,6 +172,14 @@ static void solver_trace_row(pf_solver *S, const double *d_x, const double *d_ro
     S->trace.push_back(row);
 }
 
+// Sets *flag = 1 if any x[i] is NaN or infinite (benign same-value stores).
+__global__ void k_flag_nonfinite(const double *__restrict__ x, int64_t n, double *flag) {
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(x[i]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *flag = 1.0;
+}
+
 static void solver_init(pf_solver *S, const double *warm) {
     DeviceGuard g(S->inst->device());
     InstView I = S->inst->view();
@@ -181,6 +189,7 @@ static void solver_init(pf_solver *S, const double *warm) {
     auto lap = [&](const char *what) {
         if (timing) fprintf(stderr, "[solver_init] %s at %.2f ms\n", what, 1e3 * (wall() - S->t0));
     };
+    S->initialized = false;  // a failed init leaves no runnable state
     S->trace.clear();
     S->loop_ms = S->proj_ms = 0.0;
     S->status = PF_OK;
@@ -188,12 +197,7 @@ static void solver_init(pf_solver *S, const double *warm) {
     S->finished = false;
     HostCtrl c;
     c.beta = S->cfg.beta0;
-    if (warm) {  // controller.py:104-111
-        bool finite = true;
-        for (int64_t p = 0; p < S->P(); ++p) finite = finite && std::isfinite(warm[p]);
-        require(finite, "warm start contains non-finite rates");
-        c.alpha = S->cfg.alpha_target >= 0 ? S->cfg.alpha_target : 0;
-    }
+    if (warm) c.alpha = S->cfg.alpha_target >= 0 ? S->cfg.alpha_target : 0;  // controller.py:104-111
     S->ctrl = c;
     lap("checks");
     DevBuf<double> x0own;
@@ -205,9 +209,24 @@ static void solver_init(pf_solver *S, const double *warm) {
         x0 = x0own.p;
     }
     lap("x0 alloc");
-    if (warm)
+    // the warm start's finiteness (controller.py:104-111) is checked on the
+    // device copy: one read of x0 instead of a host pass over P doubles
+    DevBuf<double> flagown;
+    double *flag = nullptr;
+    double hflag = 0.0;
+    if (warm) {
         h2d(x0, warm, S->P(), st);
-    else if (I.P)
+        if (S->cfg.mode == PF_MODE_FAST) {
+            flag = fast_scratch(S->fast, 3);
+        } else {
+            flagown.alloc(1);
+            flag = flagown.p;
+        }
+        PF_CUDA(cudaMemsetAsync(flag, 0, sizeof(double), st));
+        if (I.P) k_flag_nonfinite<<<std::min<int64_t>(ceil_div(I.P, 256), 1184), 256, 0, st>>>(x0, I.P, flag);
+        PF_CHECK_LAUNCH();
+        d2h(&hflag, flag, 1, st);
+    } else if (I.P)
         k_init_cold<<<ceil_div(I.P, 256), 256, 0, st>>>(I, x0);
     PF_CHECK_LAUNCH();
     if (S->cfg.mode == PF_MODE_EXACT) {
@@ -224,6 +243,7 @@ static void solver_init(pf_solver *S, const double *warm) {
     }
     PF_CUDA(cudaStreamSynchronize(st));
     lap("fast_init + sync");
+    require(hflag == 0.0, "warm start contains non-finite rates");
     S->initialized = true;
 }
 

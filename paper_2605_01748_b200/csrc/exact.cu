@@ -15,6 +15,8 @@
 // _k_suggest) are walked by one warp with the gathers issued 32-wide.
 #include <climits>
 
+#include <math_constants.h>
+
 #include "pf_internal.cuh"
 
 namespace pf {
@@ -108,6 +110,13 @@ __global__ void k_slack_sc(int32_t E, const double *dc, double beta, const doubl
 __global__ void k_gather_edge_major(InstView I, const double *__restrict__ pv, double *__restrict__ vals) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t < I.NP) vals[t] = pv[I.edge_pairs[t]];
+}
+
+// edge-major copy of the per-path rates: vals[t] = x[pair_path[edge_pairs[t]]]
+__global__ void k_gather_rates_edge_major(int64_t NP, const int32_t *__restrict__ epath,
+                                          const double *__restrict__ x, double *__restrict__ vals) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < NP) vals[t] = x[epath[t]];
 }
 
 // _reduce.py:60-65 over an edge-major contiguous array: one warp per edge,
@@ -339,8 +348,82 @@ __device__ double np_pairwise(const double *a, int64_t n) {
     return np_pairwise(a, n2) + np_pairwise(a + n2, n - n2);
 }
 
-__global__ void k_np_sum(const double *a, int64_t n, double *out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) *out = np_pairwise(a, n);
+// np_pairwise(a, n) by one CTA, bitwise the same: thread 0 enumerates the
+// tree's leaves (<= 128 elements, >= 64 unless n <= 128) left to right, the
+// block sums the leaves in parallel, thread 0 adds them up the same tree.
+// Both traversals are iterative over one small stack (depth <= 27 for
+// n < 2^32).  leaf_lo and leaf_sum hold n / 32 + 8 entries.  Every thread gets
+// the result.
+__device__ double cta_np_pairwise(const double *a, int64_t n, int64_t *leaf_lo, double *leaf_sum) {
+    __shared__ int64_t s_L;
+    __shared__ double s_res;
+    if (threadIdx.x == 0) {
+        int64_t stk[64];  // enumeration: (lo, m) pairs; combine: m to visit / ~m to add
+        int sp = 0;
+        int64_t L = 0;
+        if (n > 0) {
+            stk[0] = 0;
+            stk[1] = n;
+            sp = 2;
+        }
+        while (sp) {
+            sp -= 2;
+            const int64_t lo = stk[sp], m = stk[sp + 1];
+            if (m <= 128) {
+                leaf_lo[L++] = lo;
+            } else {
+                int64_t n2 = m / 2;
+                n2 -= n2 % 8;
+                stk[sp] = lo + n2;  // right, visited after the left
+                stk[sp + 1] = m - n2;
+                stk[sp + 2] = lo;
+                stk[sp + 3] = n2;
+                sp += 4;
+            }
+        }
+        leaf_lo[L] = n;
+        s_L = L;
+    }
+    __syncthreads();
+    const int64_t L = s_L;
+    for (int64_t l = threadIdx.x; l < L; l += blockDim.x)
+        leaf_sum[l] = np_pairwise(a + leaf_lo[l], leaf_lo[l + 1] - leaf_lo[l]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double res = 0.0;
+        if (n > 0) {
+            int64_t stk[64];
+            double val[32];
+            int sp = 0, vp = 0;
+            int64_t i = 0;
+            stk[sp++] = n;
+            while (sp) {
+                const int64_t m = stk[--sp];
+                if (m < 0) {  // both children done: left + right (np_pairwise's order)
+                    const double b = val[--vp], c = val[--vp];
+                    val[vp++] = c + b;
+                } else if (m <= 128) {
+                    val[vp++] = leaf_sum[i++];
+                } else {
+                    int64_t n2 = m / 2;
+                    n2 -= n2 % 8;
+                    stk[sp++] = ~m;
+                    stk[sp++] = m - n2;
+                    stk[sp++] = n2;
+                }
+            }
+            res = val[0];
+        }
+        s_res = res;
+    }
+    __syncthreads();
+    return s_res;
+}
+
+__global__ void __launch_bounds__(1024) k_np_sum(const double *a, int64_t n, double *out, int64_t *leaf_lo,
+                                                 double *leaf_sum) {
+    const double r = cta_np_pairwise(a, n, leaf_lo, leaf_sum);
+    if (threadIdx.x == 0) *out = r;
 }
 
 // kernels.py:47-66 utility of max(S, 1e-12) (controller.py:175)
@@ -379,32 +462,51 @@ __global__ void k_violations(InstView I, const double *x, const double *loads, c
     }
 }
 
+// max of -x over x < -tol, grid-wide (order-free: max is exact).  *out must
+// hold +0.0 before the launch; the maxima are >= 0, so their bit patterns
+// order like the values.
 __global__ void k_worst_negative(int32_t P, const double *x, double tol, double *out) {
-    // max of -x over x < -tol (single pass, order-free: max is exact)
-    __shared__ double sm[256];
     double m = 0.0;
-    for (int i = threadIdx.x; i < P; i += blockDim.x)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x)
         if (x[i] < -tol && -x[i] > m) m = -x[i];
-    sm[threadIdx.x] = m;
-    __syncthreads();
-    for (int s = 128; s > 0; s >>= 1) {
-        if (threadIdx.x < s && sm[threadIdx.x + s] > sm[threadIdx.x]) sm[threadIdx.x] = sm[threadIdx.x + s];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *out = sm[0];
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.0)
+        atomicMax((unsigned long long *)out, (unsigned long long)__double_as_longlong(m));
 }
 
 // Stable compaction of the non-NaN relative violations (edges first, then
-// commodities: np.concatenate order, model.py:358-362) followed by np.mean.
-__global__ void k_compact_mean(const double *rel_e, int32_t E, const double *rel_c, int32_t C, double *tmp,
-                               double *out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    int64_t n = 0;
-    for (int32_t i = 0; i < E; ++i)
-        if (!isnan(rel_e[i])) tmp[n++] = rel_e[i];
-    for (int32_t i = 0; i < C; ++i)
-        if (!isnan(rel_c[i])) tmp[n++] = rel_c[i];
-    *out = n ? np_pairwise(tmp, n) / (double)n : 0.0;
+// commodities: np.concatenate order, model.py:358-362) followed by np.mean,
+// one CTA: block-scan compaction, then the pairwise tree with parallel leaves.
+__global__ void __launch_bounds__(1024) k_compact_mean(const double *rel_e, int32_t E, const double *rel_c,
+                                                       int32_t C, double *tmp, double *out, int64_t *leaf_lo,
+                                                       double *leaf_sum) {
+    __shared__ int32_t wcnt[32];
+    __shared__ int64_t s_base;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int64_t N = (int64_t)E + C;
+    if (tid == 0) s_base = 0;
+    __syncthreads();
+    for (int64_t c0 = 0; c0 < N; c0 += blockDim.x) {
+        const int64_t i = c0 + tid;
+        const double v = i < E ? rel_e[i] : (i < N ? rel_c[i - E] : CUDART_NAN);
+        const bool keep = !isnan(v);
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) wcnt[warp] = __popc(bal);
+        __syncthreads();
+        int32_t before = 0, total = 0;
+        for (int w = 0; w < nw; ++w) {
+            before += w < warp ? wcnt[w] : 0;
+            total += wcnt[w];
+        }
+        const int64_t base = s_base;
+        if (keep) tmp[base + before + __popc(bal & ((1u << lane) - 1u))] = v;
+        __syncthreads();
+        if (tid == 0) s_base = base + total;
+    }
+    __syncthreads();
+    const int64_t n = s_base;
+    const double r = cta_np_pairwise(tmp, n, leaf_lo, leaf_sum);
+    if (tid == 0) *out = n ? r / (double)n : 0.0;
 }
 
 }  // namespace
@@ -425,6 +527,14 @@ void exact_edge_loads_from_pairs(const InstView &I, const double *pv, double *ou
 
 void exact_edge_loads_of_rates(const InstView &I, const double *rates, double *out, cudaStream_t s) {
     if (I.E) k_edge_gather_blk<1><<<ceil_div((int64_t)I.E * 32, 128), 128, 0, s>>>(I, rates, out);
+    PF_CHECK_LAUNCH();
+}
+
+void exact_edge_loads_of_rates_em(const InstView &I, const double *rates, const int32_t *epath, double *scratch,
+                                  double *out, cudaStream_t s) {
+    if (!I.E) return;
+    if (I.NP) k_gather_rates_edge_major<<<ceil_div(I.NP, 256), 256, 0, s>>>(I.NP, epath, rates, scratch);
+    k_edge_blk_contig<<<ceil_div((int64_t)I.E * 32, 128), 128, 0, s>>>(I, scratch, out);
     PF_CHECK_LAUNCH();
 }
 
@@ -511,6 +621,9 @@ static void ensure_trace_scratch(const InstView &I, TraceScratch &ts) {
     if (ts.sums.n < (size_t)I.C + 1) ts.sums.alloc(I.C + 1);
     if (ts.rel.n < (size_t)(I.E + I.C) + 1) ts.rel.alloc(I.E + I.C + 1);
     if (ts.tmp.n < (size_t)(I.E + I.C) + 1) ts.tmp.alloc(I.E + I.C + 1);
+    const size_t nleaf = (size_t)(I.E + I.C) / 32 + 8;
+    if (ts.leaf_sum.n < nleaf) ts.leaf_sum.alloc(nleaf);
+    if (ts.leaf_lo.n < nleaf) ts.leaf_lo.alloc(nleaf);
     if (ts.cnt.n < 4) ts.cnt.alloc(4);
     if (ts.out.n < 8) ts.out.alloc(8);
 }
@@ -521,7 +634,7 @@ void trace_stats(const InstView &I, const double *x, const double *root_sums, in
     ensure_trace_scratch(I, ts);
     if (I.C) {
         k_utility<<<ceil_div(I.C, TB), TB, 0, s>>>(I.C, root_sums, alpha, ts.tmp.p);
-        k_np_sum<<<1, 32, 0, s>>>(ts.tmp.p, I.C, ts.out.p + 0);
+        k_np_sum<<<1, 1024, 0, s>>>(ts.tmp.p, I.C, ts.out.p + 0, ts.leaf_lo.p, ts.leaf_sum.p);
     } else {
         PF_CUDA(cudaMemsetAsync(ts.out.p, 0, sizeof(double), s));
     }
@@ -548,8 +661,10 @@ void violation_stats(const InstView &I, const double *x, double tol, double *d_o
     if (n)
         k_violations<<<ceil_div(n, TB), TB, 0, s>>>(I, x, ts.loads.p, ts.sums.p, tol, d_overload, d_excess, ts.rel.p,
                                                      ts.rel.p + I.E, ts.cnt.p);
-    k_compact_mean<<<1, 32, 0, s>>>(ts.rel.p, I.E, ts.rel.p + I.E, I.C, ts.tmp.p, ts.out.p + 1);
-    k_worst_negative<<<1, 256, 0, s>>>(I.P, x, tol, ts.out.p + 2);
+    k_compact_mean<<<1, 1024, 0, s>>>(ts.rel.p, I.E, ts.rel.p + I.E, I.C, ts.tmp.p, ts.out.p + 1, ts.leaf_lo.p,
+                                      ts.leaf_sum.p);
+    PF_CUDA(cudaMemsetAsync(ts.out.p + 2, 0, sizeof(double), s));
+    if (I.P) k_worst_negative<<<std::min<int64_t>(ceil_div(I.P, 256), 592), 256, 0, s>>>(I.P, x, tol, ts.out.p + 2);
     PF_CHECK_LAUNCH();
     int32_t cnt[4];
     double mr[2];

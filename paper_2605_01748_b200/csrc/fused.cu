@@ -1669,7 +1669,7 @@ struct FastSolver {
     std::vector<void *> opened;              // IPC mappings to close
     DevBuf<unsigned long long> xepoch;       // exchanges done
     // per-solve scratch kept with the (pooled) solver: warm-start staging, outputs
-    DevBuf<double> x0stage, rates_out, sums_out;
+    DevBuf<double> x0stage, rates_out, sums_out, flag;
 };
 
 static void fast_set_config(FastSolver *F, const pf_config &cfg) {
@@ -2226,8 +2226,8 @@ void fast_set_edge_counts(FastSolver *F, const double *counts) {
 
 double *fast_scratch(FastSolver *F, int which) {
     const Index &I = *F->inst->idx;
-    DevBuf<double> &b = which == 0 ? F->x0stage : which == 1 ? F->rates_out : F->sums_out;
-    const size_t n = (size_t)std::max<int64_t>(1, which == 2 ? I.C + 1 : I.P);
+    DevBuf<double> &b = which == 0 ? F->x0stage : which == 1 ? F->rates_out : which == 2 ? F->sums_out : F->flag;
+    const size_t n = (size_t)std::max<int64_t>(1, which == 3 ? 1 : which == 2 ? I.C + 1 : I.P);
     if (b.n < n) b.alloc(n);
     return b.p;
 }

@@ -24,7 +24,7 @@ void fast_destroy(FastSolver *f);
 // Return a solver to its instance's pool (kept for the next solve), or destroy it.
 void fast_release(FastSolver *f);
 // Device scratch owned by the (pooled) solver, grown on demand: 0 warm-start
-// staging [P], 1 projected rates [P], 2 commodity sums [C + 1].
+// staging [P], 1 projected rates [P], 2 commodity sums [C + 1], 3 one flag.
 double *fast_scratch(FastSolver *f, int which);
 void fast_init(FastSolver *f, const double *d_x0, int64_t alpha0, double beta0, cudaStream_t s);
 // Runs up to max_steps iterations (fewer if the controller stops); returns the count.

@@ -219,6 +219,10 @@ struct Flags {
 void exact_commodity_sums(const InstView &I, const double *x, double *out, cudaStream_t s);
 void exact_edge_loads_from_pairs(const InstView &I, const double *pair_vals, double *out, cudaStream_t s);
 void exact_edge_loads_of_rates(const InstView &I, const double *rates, double *out, cudaStream_t s);
+// Same sums (same association) through an edge-major copy: epath[t] =
+// pair_path[edge_pairs[t]], scratch holds NP doubles.
+void exact_edge_loads_of_rates_em(const InstView &I, const double *rates, const int32_t *epath, double *scratch,
+                                  double *out, cudaStream_t s);
 void exact_update_duals(const InstView &I, const StatePtrs &st, double *sums_tmp, double *loads_tmp, double *dd,
                         double *dc, double *dcon, double *dn, cudaStream_t s, double *scratch = nullptr);
 void exact_update_slacks(const InstView &I, const StatePtrs &st, double beta, double *sums_tmp, double *loads_tmp,
@@ -241,7 +245,8 @@ void reset_flags(Flags *f, cudaStream_t s);
 
 // Trace helpers (model.py:335-369, kernels.py:47-66 summed with numpy pairwise order).
 struct TraceScratch {
-    DevBuf<double> loads, sums, rel, tmp;
+    DevBuf<double> loads, sums, rel, tmp, leaf_sum;
+    DevBuf<int64_t> leaf_lo;
     DevBuf<int32_t> cnt;
     DevBuf<double> out;  // [4]: objective, pct, mean_rel, n_viol
 };

@@ -15,8 +15,11 @@
 // (scores are fixed during phase 3) are one segmented stable radix sort.
 // All arithmetic keeps the reference's order, so the projection is bitwise
 // identical to the reference whenever its inputs are (alpha <= 1 scores).
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
+#include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -453,6 +456,142 @@ __global__ void __launch_bounds__(1024) k_edge_trim_fast(InstView I, const int32
     }
 }
 
+// Fast-mode phase 3 on a thread-block cluster (same trim rule as
+// k_edge_trim_fast, fewer round trips): the violated edge's score-ordered
+// paths are split into contiguous slices, one per CTA, gathered ONCE into
+// shared memory; every pass is a local block scan plus two DSMEM exchanges
+// (slice totals, then each slice's first crossing index), the trim and the
+// re-check of the load stay on chip, and the changed rates are written back
+// once per edge.  The load, the carries and the cut index are computed from
+// values every CTA holds identically, so all decisions are uniform across the
+// cluster and the result is deterministic.
+namespace cg = cooperative_groups;
+constexpr int CL_NT = 1024;
+constexpr int CL_CAP = 18432;  // slice capacity per CTA (12 B per entry: 216 KB)
+constexpr int CL_SMEM = CL_CAP * (sizeof(double) + sizeof(int32_t));
+
+__global__ void __launch_bounds__(CL_NT, 1) k_edge_trim_cluster(InstView I, const int32_t *edge_order,
+                                                               const int32_t *nviol_p, const int32_t *path_order,
+                                                               double *x, int stats) {
+    extern __shared__ __align__(16) char dsm[];
+    double *sx = (double *)dsm;                                  // [CL_CAP]
+    int32_t *sp = (int32_t *)(dsm + CL_CAP * sizeof(double));   // [CL_CAP]
+    __shared__ double s_part[2][8];                              // slice totals, by rank (written remotely)
+    __shared__ int32_t s_found[2][8];                            // slice-local cut index or INT_MAX
+    __shared__ double wsum[32];
+    __shared__ int32_t s_js;
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank(), ncl = (int)cl.num_blocks();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = CL_NT >> 5;
+    const int32_t nviol = *nviol_p;
+    long long st_trimmed = 0, st_passes = 0;
+    int ph = 0;
+    // every edge is gathered anyway, so its load is always the fresh sum of the
+    // gathered rates (the reference re-sums each edge at its turn,
+    // projection.py:84-88); no dirty-edge bookkeeping
+    for (int32_t vi = 0; vi < nviol; ++vi) {
+        const int32_t e = edge_order[vi];
+        const int32_t lo = I.edge_pair_ptr[e], n = I.edge_pair_ptr[e + 1] - lo;
+        const double cap = I.capacity[e];
+        const int32_t chunk = (n + ncl - 1) / ncl;
+        const int32_t a = min(n, rank * chunk), len = min(n, a + chunk) - a;
+        if (vi + 1 < nviol) {  // the next edge's slice of the path order into L2 (independent of x)
+            const int32_t e2 = edge_order[vi + 1];
+            const int32_t lo2 = I.edge_pair_ptr[e2], n2 = I.edge_pair_ptr[e2 + 1] - lo2;
+            const int32_t c2 = (n2 + ncl - 1) / ncl, a2 = min(n2, rank * c2), l2 = min(n2, a2 + c2) - a2;
+            for (int32_t j = tid * 32; j < l2; j += CL_NT * 32)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(path_order + lo2 + a2 + j));
+        }
+        for (int32_t j0 = tid; j0 < len; j0 += 8 * CL_NT) {  // gather: 8 independent loads in flight
+            int32_t pi[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int32_t j = j0 + u * CL_NT;
+                pi[u] = j < len ? __ldcg(path_order + lo + a + j) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int32_t j = j0 + u * CL_NT;
+                if (j < len) {
+                    sp[j] = pi[u];
+                    sx[j] = __ldcg(x + pi[u]);
+                }
+            }
+        }
+        const int32_t m = (len + CL_NT - 1) / CL_NT;  // each thread owns a contiguous run
+        const int32_t r0 = min(len, tid * m), r1 = min(len, r0 + m);
+        int32_t maxchg = -1;  // highest slice index changed on this edge (uniform in the CTA)
+        __syncthreads();
+        for (int pass = 0;; ++pass) {
+            double ts = 0.0;
+            for (int32_t j = r0; j < r1; ++j) ts += sx[j];
+            double ws = ts;
+            for (int o = 1; o < 32; o <<= 1) {
+                const double t = __shfl_up_sync(0xffffffffu, ws, o);
+                if (lane >= o) ws += t;
+            }
+            if (lane == 31) wsum[warp] = ws;
+            if (tid == 0) s_js = INT_MAX;
+            __syncthreads();
+            if (warp == 0) {
+                double v = lane < nw ? wsum[lane] : 0.0;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double t = __shfl_up_sync(0xffffffffu, v, o);
+                    if (lane >= o) v += t;
+                }
+                if (lane < nw) wsum[lane] = v;
+            }
+            __syncthreads();
+            if (tid < ncl) *cl.map_shared_rank(&s_part[ph][rank], tid) = wsum[nw - 1];
+            cl.sync();
+            double load = 0.0, carry = 0.0;
+            for (int q = 0; q < ncl; ++q) {
+                if (q == rank) carry = load;
+                load += s_part[ph][q];
+            }
+            const double excess = load - cap;
+            if (!(excess > 0.0) || pass == 16) break;  // uniform
+            st_passes += 1;
+            // first index of the slice whose prefix reaches the excess
+            double pre = carry + (warp ? wsum[warp - 1] : 0.0) + (ws - ts);
+            for (int32_t j = r0; j < r1; ++j) {
+                pre += sx[j];
+                if (pre >= excess) {
+                    atomicMin(&s_js, j);
+                    break;
+                }
+            }
+            __syncthreads();
+            const int32_t js = s_js;
+            if (tid < ncl) *cl.map_shared_rank(&s_found[ph][rank], tid) = js;
+            cl.sync();
+            bool earlier = false;
+            for (int q = 0; q < rank; ++q) earlier |= s_found[ph][q] != INT_MAX;
+            if (!earlier) {
+                // zero up to the cut; the cut keeps prefix - excess (recomputed by its owner)
+                const int32_t cut = js == INT_MAX ? len : js;
+                if (cut < len && cut >= r0 && cut < r1) {
+                    double p2 = carry + (warp ? wsum[warp - 1] : 0.0) + (ws - ts);
+                    for (int32_t j = r0; j <= cut; ++j) p2 += sx[j];
+                    sx[cut] = max0(p2 - excess);
+                }
+                __syncthreads();
+                for (int32_t j = tid; j < cut; j += CL_NT) sx[j] = 0.0;
+                maxchg = max(maxchg, cut < len ? cut : len - 1);
+            }
+            ph ^= 1;
+            __syncthreads();
+        }
+        ph ^= 1;
+        for (int32_t j = tid; j <= maxchg; j += CL_NT) x[sp[j]] = sx[j];
+        st_trimmed += maxchg >= 0;
+        cl.sync();  // the written rates are visible to the whole cluster before the next gather
+    }
+    if (stats && tid == 0)
+        printf("[k_edge_trim_cluster] rank %d/%d violated %d slices trimmed %lld passes %lld\n", rank, ncl, nviol,
+               st_trimmed, st_passes);
+}
+
 constexpr int TRIM_SMEM = 2 * TCH * (sizeof(double) + sizeof(int32_t));
 constexpr int TRIM_FAST_SMEM = FCH * (sizeof(double) + sizeof(int32_t));
 
@@ -472,6 +611,13 @@ static ProjWS &workspace(const pf_instance *inst, cudaStream_t s) {
     std::lock_guard<std::mutex> lk(inst->ws_mu);
     if (inst->proj_ws) return *static_cast<ProjWS *>(inst->proj_ws.get());
     InstView I = inst->view();
+    static const bool timing = getenv("PF_TIMING") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto lap = [&](const char *what) {
+        if (timing)
+            fprintf(stderr, "[proj_workspace] %s at %.2f ms\n", what,
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    };
     auto ws = std::make_shared<ProjWS>();
     ws->scores.alloc(I.P + 1);
     ws->sums.alloc(I.C + 1);
@@ -492,12 +638,14 @@ static ProjWS &workspace(const pf_instance *inst, cudaStream_t s) {
     ws->porder.alloc(I.NP + 1);
     ws->sb.alloc(I.E + 1);
     ws->se.alloc(I.E + 1);
+    lap("allocs");
     ws->epath.alloc(I.NP + 1);  // path of each edge-major pair: pair_path[edge_pairs[t]]
     if (I.NP) k_edge_paths<<<ceil_div(I.NP, 256), 256, 0, s>>>(I, ws->epath.p);
     PF_CHECK_LAUNCH();
     std::vector<int32_t> eptr(I.E + 1);
     d2h(eptr.data(), I.edge_pair_ptr, I.E + 1, s);
     PF_CUDA(cudaStreamSynchronize(s));
+    lap("edge paths + sync");
     for (int32_t e = 0; e < I.E; ++e) ws->max_ne = std::max(ws->max_ne, eptr[e + 1] - eptr[e]);
     ws->parts.alloc((ws->max_ne + BLK - 1) / BLK + 1);
     size_t a = 0, b = 0;
@@ -506,18 +654,39 @@ static ProjWS &workspace(const pf_instance *inst, cudaStream_t s) {
     PF_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, b, ws->pkeys.p, ws->pkeys_out.p, ws->pvals.p,
                                                      ws->porder.p, I.NP, I.E, ws->sb.p, ws->se.p, 0, 64, s));
     ws->cub_bytes = std::max<size_t>(std::max(a, b), 16);
+    lap("cub sizing");
     ws->cub.alloc(ws->cub_bytes);
     PF_CUDA(cudaFuncSetAttribute(k_edge_trim, cudaFuncAttributeMaxDynamicSharedMemorySize, TRIM_SMEM));
     PF_CUDA(cudaFuncSetAttribute(k_edge_trim_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, TRIM_FAST_SMEM));
+    PF_CUDA(cudaFuncSetAttribute(k_edge_trim_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SMEM));
+    lap("attributes");
     inst->proj_ws = ws;
     return *ws;
 }
 
+// Fast-mode edge loads: one CTA per edge, 8 gathers in flight per thread, fixed
+// tree (deterministic; a reassociation of model.py:305-311).
+__global__ void __launch_bounds__(256) k_edge_loads_fast(InstView I, const int32_t *__restrict__ epath,
+                                                         const double *__restrict__ x, double *__restrict__ out) {
+    __shared__ double red[33];
+    const int32_t e = blockIdx.x;
+    out[e] = cta_edge_resum_fast(epath, x, I.edge_pair_ptr[e], I.edge_pair_ptr[e + 1], red);
+}
+
+static void edge_loads_ws(const InstView &I, ProjWS &ws, const double *x, bool fast, cudaStream_t s) {
+    if (fast) {
+        if (I.E) k_edge_loads_fast<<<I.E, 256, 0, s>>>(I, ws.epath.p, x, ws.loads.p);
+        PF_CHECK_LAUNCH();
+    } else {  // pkeys_out is dead outside the phase-3 sort: edge-major scratch
+        exact_edge_loads_of_rates_em(I, x, ws.epath.p, (double *)ws.pkeys_out.p, ws.loads.p, s);
+    }
+}
+
 static void score_paths_ws(const pf_instance *inst, ProjWS &ws, const double *x, int64_t alpha, double *scores,
-                           cudaStream_t s) {
+                           cudaStream_t s, bool fast = false, bool loads_ready = false) {
     InstView I = inst->view();
     exact_commodity_sums(I, x, ws.sums.p, s);
-    exact_edge_loads_of_rates(I, x, ws.loads.p, s);
+    if (!loads_ready) edge_loads_ws(I, ws, x, fast, s);
     if (I.E) k_violated_edges<<<ceil_div(I.E, TB), TB, 0, s>>>(I.E, ws.loads.p, I.capacity, 1e-9, ws.viol.p);
     if (I.P) k_scores<<<ceil_div(I.P, TB), TB, 0, s>>>(I, ws.sums.p, ws.viol.p, alpha, scores);
     PF_CHECK_LAUNCH();
@@ -540,11 +709,11 @@ void project_device(const pf_instance *inst, const double *rates, int64_t alpha,
     k_clamp<<<ceil_div(I.P, TB), TB, 0, s>>>(I.P, rates, x, ws.bad.p);
     PF_CHECK_LAUNCH();
     // phase 2 (projection.py:63-74)
-    score_paths_ws(inst, ws, x, alpha, ws.scores.p, s);
+    score_paths_ws(inst, ws, x, alpha, ws.scores.p, s, fast);
     if (I.C) k_demand_trim<<<ceil_div(I.C, 128), 128, 0, s>>>(I, ws.scores.p, x, ws.order.p);
     PF_CHECK_LAUNCH();
     // phase 3 (projection.py:76-106): violated edges in stable descending overload
-    exact_edge_loads_of_rates(I, x, ws.loads.p, s);
+    edge_loads_ws(I, ws, x, fast, s);
     if (I.E)
         k_over<<<ceil_div(I.E, TB), TB, 0, s>>>(I.E, ws.loads.p, I.capacity, ws.over.p, ws.ekeys.p, ws.eids.p,
                                                  ws.nviol.p);
@@ -554,7 +723,8 @@ void project_device(const pf_instance *inst, const double *rates, int64_t alpha,
         PF_CUDA(cub::DeviceRadixSort::SortPairs(ws.cub.p, bytes, ws.ekeys.p, ws.ekeys_out.p, ws.eids.p, ws.eorder.p,
                                                 I.E, 0, 64, s));
     }
-    score_paths_ws(inst, ws, x, alpha, ws.scores.p, s);  // projection.py:81 (post-phase-2 rates)
+    // projection.py:81 (post-phase-2 rates): the loads of these rates were just computed
+    score_paths_ws(inst, ws, x, alpha, ws.scores.p, s, fast, true);
     if (I.E) k_violated_segments<<<ceil_div(I.E, TB), TB, 0, s>>>(I.E, ws.over.p, I.edge_pair_ptr, ws.sb.p, ws.se.p);
     if (I.NP) k_edge_path_keys_violated<<<ceil_div(I.NP, TB), TB, 0, s>>>(I, ws.scores.p, ws.over.p, ws.pkeys.p,
                                                                          ws.pvals.p);
@@ -566,7 +736,36 @@ void project_device(const pf_instance *inst, const double *rates, int64_t alpha,
     }
     static const int stats = getenv("PF_PROJ_STATS") ? 1 : 0;
     PF_CUDA(cudaMemsetAsync(ws.dirty.p, 0, I.E + 1, s));
-    if (fast)
+    // PF_PROJ_CLUSTER: CTAs per cluster for the fast trim (0 = single-CTA kernel)
+    static const int cl_env = getenv("PF_PROJ_CLUSTER") ? atoi(getenv("PF_PROJ_CLUSTER")) : -1;
+    int ncl = 0;
+    if (fast && ws.max_ne <= 8 * CL_CAP) {
+        const int need = (ws.max_ne + CL_CAP - 1) / CL_CAP, want = (ws.max_ne + 6143) / 6144;
+        ncl = 1;
+        while (ncl < 8 && (ncl < need || ncl < want)) ncl *= 2;
+        if (cl_env == 0) {
+            ncl = 0;
+        } else if (cl_env > 0) {  // the requested size, at least what the largest edge needs
+            ncl = 1;
+            while (ncl < 8 && (ncl < cl_env || ncl < need)) ncl *= 2;
+        }
+    }
+    if (fast && ncl > 0) {
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(ncl);
+        lc.blockDim = dim3(CL_NT);
+        lc.dynamicSmemBytes = CL_SMEM;
+        lc.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = ncl;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        PF_CUDA(cudaLaunchKernelEx(&lc, k_edge_trim_cluster, I, (const int32_t *)ws.eorder.p,
+                                   (const int32_t *)ws.nviol.p, (const int32_t *)ws.porder.p, x, stats));
+    } else if (fast)
         k_edge_trim_fast<<<1, 1024, TRIM_FAST_SMEM, s>>>(I, ws.eorder.p, ws.nviol.p, ws.porder.p, ws.epath.p, x,
                                                          ws.over.p, ws.dirty.p);
     else

@@ -363,10 +363,20 @@ def test_edge_cases(mode):
     res = pf.solve(inst, pf.SolverConfig(max_iterations=3, mode=mode))
     assert not res.converged and res.iterations == 3
     assert pf.validate_allocation(inst, res.rates).feasible
-    with pytest.raises(pf.InputError):
-        pf.solve(inst, pf.SolverConfig(mode=mode), warm_start=np.array([1.0, np.nan, 2.0]))
+    for bad in (np.nan, np.inf, -np.inf):
+        with pytest.raises(pf.InputError, match="warm start contains non-finite rates"):
+            pf.solve(inst, pf.SolverConfig(mode=mode), warm_start=np.array([1.0, bad, 2.0]))
     with pytest.raises(pf.InputError):
         pf.solve(inst, pf.SolverConfig(mode=mode), warm_start=np.array([1.0, 2.0]))
+    # the check runs on the device copy: a failed init leaves nothing runnable
+    s = pf.Solver(inst, pf.SolverConfig(mode=mode)).init()
+    s.run(2)
+    with pytest.raises(pf.InputError, match="non-finite"):
+        s.init(np.array([1.0, 2.0, np.nan]))
+    with pytest.raises(Exception, match="not initialized"):
+        s.run(1)
+    s.init(np.array([1.0, 2.0, 3.0]))
+    assert s.run(2) == 2
 
 
 @pytest.mark.parametrize("n,k", [(60, 8), (50, 1), (45, 3)])
@@ -430,6 +440,27 @@ def test_fast_solve_projection_feasible_and_close_to_exact():
     assert pf.validate_allocation(inst, fast_rates).feasible
     np.testing.assert_allclose(fast_sums, pf.commodity_sums(inst, exact_rates), rtol=1e-6,
                                atol=1e-9 * float(np.max(np.abs(x))))
+
+
+@pytest.mark.parametrize("ncl", ["1", "2", "8", "0"])
+def test_fast_projection_cluster_variants(ncl):
+    """The cluster-resident fast trim (1, 2 and 8 CTAs per cluster; slices of
+    multi-element runs per thread) and the single-CTA kernel ("0") on a raw
+    iterate with edges of thousands of paths: exactly feasible, commodity sums
+    matching the bitwise projection, bit-reproducible run to run."""
+    import json
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, PF_PROJ_CLUSTER=ncl)
+    r = subprocess.run([sys.executable, os.path.join(here, "_proj_variant.py"), "150", "4", "12"], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["infeasible_before"] and out["max_edge_paths"] > 2048
+    assert out["feasible"] and out["deterministic"]
+    assert out["sums_rel"] <= 1e-6, out
 
 
 @pytest.mark.parametrize("scale", [1e300, 1e308])
