@@ -120,6 +120,12 @@ class ClockSampler:
             h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
 
+            # the first NVML queries are slow: issue them here, outside the timed
+            # region, and return only once the thread is sampling
+            pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            first = threading.Event()
+
             def run():
                 while not self._stop.is_set():
                     try:
@@ -128,9 +134,11 @@ class ClockSampler:
                         self.samples.append((mhz, rs))
                     except Exception:  # noqa: BLE001
                         pass
+                    first.set()
                     time.sleep(self.period)
             self.th = threading.Thread(target=run, daemon=True)
             self.th.start()
+            first.wait(timeout=5)
         except Exception:  # noqa: BLE001
             self.nvml = None
         return self
@@ -437,7 +445,7 @@ def run_b200(args):
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])

@@ -97,7 +97,7 @@ struct pf_solver {
     int status = PF_OK;
     int64_t bad_commodity = -1;
     bool initialized = false, finished = false;
-    DevBuf<double> rates_out, sums_out;
+    DevBuf<double> rates_out, sums_out, trace_proj, trace_sums;
     pf_comm *comm = nullptr;
     int64_t global_C = 0;
 
@@ -161,11 +161,13 @@ static void solver_trace_row(pf_solver *S, const double *d_x, const double *d_ro
     row.mean_relative_violation = st[2];
     row.optimality = NAN;
     if (!S->ref_sums.empty()) {
-        DevBuf<double> proj(S->P()), sums(S->C() + 1);
-        project_device(S->inst, d_x, alpha, proj.p, S->stream, S->cfg.mode == PF_MODE_FAST);
-        exact_commodity_sums(I, proj.p, sums.p, S->stream);
+        // per-row scratch kept on the solver (no cudaMalloc / cudaFree per iteration)
+        if (S->trace_proj.n < (size_t)S->P() + 1) S->trace_proj.alloc(S->P() + 1);
+        if (S->trace_sums.n < (size_t)S->C() + 1) S->trace_sums.alloc(S->C() + 1);
+        project_device(S->inst, d_x, alpha, S->trace_proj.p, S->stream, S->cfg.mode == PF_MODE_FAST);
+        exact_commodity_sums(I, S->trace_proj.p, S->trace_sums.p, S->stream);
         std::vector<double> hs(S->C());
-        d2h(hs.data(), sums.p, S->C(), S->stream);
+        d2h(hs.data(), S->trace_sums.p, S->C(), S->stream);
         PF_CUDA(cudaStreamSynchronize(S->stream));
         row.optimality = optimality_from_sums(hs, S->ref_sums, default_theta(S->h_demand));
     }
@@ -474,9 +476,11 @@ static pf_solver *solver_create(const pf_instance *inst, const pf_config *cfg) {
     PF_CUDA(cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking));
     PF_CUDA(cudaEventCreate(&S->ev0));
     PF_CUDA(cudaEventCreate(&S->ev1));
-    S->h_demand.resize(I.C);
-    d2h(S->h_demand.data(), inst->demand.p, I.C, S->stream);
-    PF_CUDA(cudaStreamSynchronize(S->stream));
+    if (!S->ref_sums.empty()) {  // only the trace's optimality column needs the demands on the host
+        S->h_demand.resize(I.C);
+        d2h(S->h_demand.data(), inst->demand.p, I.C, S->stream);
+        PF_CUDA(cudaStreamSynchronize(S->stream));
+    }
     if (cfg->mode == PF_MODE_EXACT) {
         S->cur.alloc(I);
         S->nxt.alloc(I);
