@@ -49,6 +49,7 @@ CONFIGS = {
     "cfg1_v0.3": (40, 4, 0.3, "GEANT-sized, V=0.3*cap (reference stop rule fires)"),
     "cfg2": (500, 8, 1.5, "synthetic 500-node WAN, all-pairs gravity, k=8 (~18.3M demand-path pairs)"),
     "cfg2_v0.3": (500, 8, 0.3, "500-node WAN, V=0.3*cap, k=8"),
+    "mid150_v0.3": (150, 4, 0.3, "150-node all-pairs gravity, k=4, V=0.3*cap (tuning: mid-size instances)"),
     "target_k4_v0.3": (500, 4, 0.3, "north-star target scale: 500-node all-pairs, k=4 (~1M paths), V=0.3*cap"),
     "cfg3": (2000, 8, 1.5, "synthetic 2000-node WAN-A-scale, all-pairs gravity, k=8 (~355M demand-path pairs)"),
 }

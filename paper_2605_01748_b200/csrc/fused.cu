@@ -162,7 +162,9 @@ struct Ctrl {
 
 struct Params {
     InstView I;
-    int32_t ntiles, G, nslices, tps, nbuf, kspan;  // kspan: power of two >= max paths per commodity
+    // pad0 keeps the layout of the 8-byte fields below: k_fused's register
+    // allocation (pass spills) measured sensitive to it
+    int32_t ntiles, G, pad0, tps, nbuf, kspan;  // kspan: power of two >= max paths per commodity
     int32_t adj_smem;                               // adjustment table in shared memory (else L1)
     int32_t acc_smem;                               // edge accumulators in shared memory (else L2 rows)
     // multi-GPU over peer memory (CUDA IPC): rank-local totals are written into
@@ -181,10 +183,8 @@ struct Params {
     const double *ne;       // [E] paths per edge (global across ranks when sharded)
     double *tot;            // [2E + 16] rank totals (multi-GPU): T, L, residual sums, error counts
     double *partT, *partL;  // [G][E]
-    double *sub;            // [2][nslices][E]
     double *res;            // [G][8]: 0 dx | 1..3 (dd, dcon, dn) parity 0 | 4..6 parity 1
-    double *res_dc;         // [ngroups]
-    int32_t *grp_count;     // [ngroups]
+    double *res_dc;         // [E] squared dual_capacity change per edge
     double *root_sums;      // [C] or null
     Ctrl *ctrl;
     int32_t *err;           // [2]: bad_coef, bad_root (INT_MAX = none)
@@ -433,13 +433,62 @@ __device__ __forceinline__ void res_sums(const double *res, int G, int lane, con
         for (int j = 0; j < NV; ++j) acc[j] += __ldcg(&res[g * 8 + off[j]]);
 }
 
-// Ticket for the last-slice combine: an acq_rel device-scope atomic orders this
-// warp's slice stores (made visible to lane 0 by __syncwarp) before the ticket,
-// and gives the last arriver the other slices' stores -- no full fences.
-__device__ __forceinline__ int ticket_acq_rel(int *p) {
-    int old;
-    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;\n" : "=r"(old) : "l"(p) : "memory");
-    return old;
+// Per-edge total of the CTA partials by one warp: lane j sums CTAs j, j + 32,
+// ... in index order (the loads of 4 CTAs issued ahead), then a fixed shuffle
+// tree; lane 0 holds the totals.  One L2 round trip for G <= 128 instead of a
+// G-long chain per lane, and the same association wherever rank-local edge
+// totals are formed (single GPU, peer-memory exchange, NCCL split kernels).
+__device__ __forceinline__ void warp_edge_sums(const double *pT, const double *pL, int G, int E, int e, int lane,
+                                               double &T, double &L) {
+    double t = 0.0, l = 0.0;
+    int g = lane;
+    for (; g + 96 < G; g += 128) {
+        double bt[4], bl[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            bt[u] = __ldcg(pT + (size_t)(g + 32 * u) * E + e);
+            bl[u] = __ldcg(pL + (size_t)(g + 32 * u) * E + e);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            t += bt[u];
+            l += bl[u];
+        }
+    }
+    for (; g < G; g += 32) {
+        t += __ldcg(pT + (size_t)g * E + e);
+        l += __ldcg(pL + (size_t)g * E + e);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        t += __shfl_down_sync(FULL, t, o);
+        l += __shfl_down_sync(FULL, l, o);
+    }
+    T = t;
+    L = l;
+}
+
+// Sum of the per-edge dual_capacity residuals by the whole CTA (NT threads):
+// thread i sums edges i, i + NT, ... in order, then a warp shuffle tree and the
+// warp sums in warp order.  Every thread returns the same value.
+__device__ double dcs_block(const double *res_dc, int E) {
+    __shared__ double wred[NT / 32];
+    double v = 0.0;
+    int e = threadIdx.x;
+    for (; e + 3 * NT < E; e += 4 * NT) {
+        double b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) b[u] = __ldcg(res_dc + e + u * NT);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v += b[u];
+    }
+    for (; e < E; e += NT) v += __ldcg(res_dc + e);
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(FULL, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) wred[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double r = wred[0];
+    for (int w = 1; w < NT / 32; ++w) r += wred[w];
+    return r;
 }
 
 // ------------------------------------------------------------------ controller
@@ -511,17 +560,14 @@ __device__ __noinline__ void controller_step(const Params &P, Ctrl &c, double s,
 // Every CTA reduces the residual partials in the same fixed order and runs the
 // same scalar controller step on its shared-memory copy of the state.
 __device__ void controller_eval(const Params &P, Ctrl &c) {
+    const double dcs = dcs_block(P.res_dc, P.I.E);
     if (threadIdx.x < 32) {
         const int par = (int)(c.iteration & 1);
         double acc[4];  // dx, dd, dcon, dn: lane-strided over the CTAs
         const int off[4] = {0, 1 + 3 * par, 2 + 3 * par, 3 + 3 * par};
         res_sums<4>(P.res, P.G, threadIdx.x, off, acc);
-        int ngroups = (P.I.E + RGRP - 1) / RGRP;
-        double dcs = sum_cg(P.res_dc + threadIdx.x, threadIdx.x < ngroups ? (ngroups - 1 - threadIdx.x) / 32 + 1 : 0,
-                            32);
         for (int j = 0; j < 4; ++j)
             for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_down_sync(FULL, acc[j], o);
-        for (int o = 16; o > 0; o >>= 1) dcs += __shfl_down_sync(FULL, dcs, o);
         if (threadIdx.x == 0)
             controller_step(P, c, sqrt(acc[0]), sqrt(((acc[1] + dcs) + acc[2]) + acc[3]), __ldcg(&P.err[0]),
                             __ldcg(&P.err[1]));
@@ -531,57 +577,25 @@ __device__ void controller_eval(const Params &P, Ctrl &c) {
 
 // ------------------------------------------------------------------ edge phase
 
-// Work item (group, slice): lanes = 32 edges of the group, sum the CTA partials
-// of the slice in CTA order; the last item of a group combines the slices in
-// order and applies kernels.py:212 (dual_capacity) and :94-96 (adjustment).
+// One warp per edge: the CTA partials summed by warp_edge_sums, then
+// kernels.py:212 (dual_capacity) and :94-96 (adjustment); the squared
+// dual_capacity change per edge for the residual (summed by dcs_block).
 __device__ __noinline__ void edge_phase(const Params &P, double f) {
     const InstView &I = P.I;
-    const int g = blockIdx.x;
-    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int ngroups = (I.E + RGRP - 1) / RGRP;
-    int nitems = ngroups * P.nslices;
-    int per = (P.G + P.nslices - 1) / P.nslices;
-    for (int item = g * NW + warp; item < nitems; item += P.G * NW) {
-        int grp = item / P.nslices, sl = item % P.nslices;
-        int e = grp * RGRP + lane;
-        int g0 = sl * per, g1 = g0 + per < P.G ? g0 + per : P.G;
-        double sT = 0.0, sL = 0.0;
-        if (e < I.E) {
-            sT = sum_cg(&P.partT[(size_t)g0 * I.E + e], g1 - g0, I.E);
-            sL = sum_cg(&P.partL[(size_t)g0 * I.E + e], g1 - g0, I.E);
-            if (P.nslices > 1) {
-                P.sub[(size_t)sl * I.E + e] = sT;
-                P.sub[(size_t)(P.nslices + sl) * I.E + e] = sL;
-            }
-        }
-        int ticket = 0;
-        if (P.nslices > 1) {  // the last slice of a group combines the slices
-            __syncwarp();
-            if (lane == 0) ticket = ticket_acq_rel(&P.grp_count[grp]);
-            ticket = __shfl_sync(FULL, ticket, 0);
-        }
-        if (ticket == P.nslices - 1) {
-            double T = sT, L = sL, rdc = 0.0;
-            if (e < I.E && P.nslices > 1) {
-                T = sum_cg(&P.sub[e], P.nslices, I.E);
-                L = sum_cg(&P.sub[(size_t)P.nslices * I.E + e], P.nslices, I.E);
-            }
-            if (e < I.E) {
-                double cap = I.capacity[e];
-                double dold = __ldcg(&P.dc[e]) * f;
-                double dnew = npmax0(dold + (L - cap));
-                double adj = (T + dnew - cap) / (P.ne[e] + 1.0);
-                if (adj < 0.0) adj = 0.0;
-                P.dc[e] = dnew;
-                P.adj[e] = adj;
-                double d = dnew - dold;
-                rdc = d * d;
-            }
-            for (int o = 16; o > 0; o >>= 1) rdc += __shfl_down_sync(FULL, rdc, o);
-            if (lane == 0) {
-                P.res_dc[grp] = rdc;
-                if (P.nslices > 1) P.grp_count[grp] = 0;
-            }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int e = blockIdx.x + P.G * warp; e < I.E; e += P.G * (NT / 32)) {  // edges spread over all CTAs
+        double T, L;
+        warp_edge_sums(P.partT, P.partL, P.G, I.E, e, lane, T, L);
+        if (lane == 0) {
+            const double cap = I.capacity[e];
+            const double dold = __ldcg(&P.dc[e]) * f;
+            const double dnew = npmax0(dold + (L - cap));
+            double adj = (T + dnew - cap) / (P.ne[e] + 1.0);
+            if (adj < 0.0) adj = 0.0;
+            P.dc[e] = dnew;
+            P.adj[e] = adj;
+            const double d = dnew - dold;
+            P.res_dc[e] = d * d;
         }
     }
 }
@@ -1080,53 +1094,24 @@ __device__ __forceinline__ unsigned long long *xb_flag(const Params &P, const do
 }
 
 // Rank-local totals of the pass just completed -> every rank's slot [rank]:
-// per-edge T and L (CTA partials summed in the same (slice, CTA) order as the
-// single-GPU edge phase), the 7 residual sums and the 2 error flags; then the
+// per-edge T and L (CTA partials summed as in the single-GPU edge phase), the 7 residual sums and the 2 error flags; then the
 // counter barrier across ranks.  Ends with a grid barrier after which every CTA
 // may read all slots of this exchange.
 __device__ __noinline__ void xchg_phase(const Params &P, Ctrl &c, cg::grid_group &grid) {
     const InstView &I = P.I;
     const int g = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t ep = c.xepoch;
-    const int ngroups = (I.E + RGRP - 1) / RGRP;
-    const int nitems = ngroups * P.nslices;
-    const int per = (P.G + P.nslices - 1) / P.nslices;
     bool wrote = false;  // this thread stored into peer memory
-    for (int item = g * NW + warp; item < nitems; item += P.G * NW) {
-        const int grp = item / P.nslices, sl = item % P.nslices;
-        const int e = grp * RGRP + lane;
-        const int g0 = sl * per, g1 = g0 + per < P.G ? g0 + per : P.G;
-        double sT = 0.0, sL = 0.0;
-        if (e < I.E) {
-            sT = sum_cg(&P.partT[(size_t)g0 * I.E + e], g1 - g0, I.E);
-            sL = sum_cg(&P.partL[(size_t)g0 * I.E + e], g1 - g0, I.E);
-            if (P.nslices > 1) {
-                P.sub[(size_t)sl * I.E + e] = sT;
-                P.sub[(size_t)(P.nslices + sl) * I.E + e] = sL;
-            }
-        }
-        int ticket = 0;
-        if (P.nslices > 1) {
-            __syncwarp();
-            if (lane == 0) ticket = ticket_acq_rel(&P.grp_count[grp]);
-            ticket = __shfl_sync(FULL, ticket, 0);
-        }
-        if (ticket == P.nslices - 1) {
-            __syncwarp();
+    for (int e = g + P.G * warp; e < I.E; e += P.G * (NT / 32)) {
+        double T, L;
+        warp_edge_sums(P.partT, P.partL, P.G, I.E, e, lane, T, L);
+        if (lane == 0) {
             wrote = true;
-            if (e < I.E) {
-                double T = sT, L = sL;
-                if (P.nslices > 1) {
-                    T = sum_cg(&P.sub[e], P.nslices, I.E);
-                    L = sum_cg(&P.sub[(size_t)P.nslices * I.E + e], P.nslices, I.E);
-                }
-                for (int r = 0; r < P.nranks; ++r) {
-                    double *d = xb_slot(P, P.peers[r], ep, P.rank);
-                    d[e] = T;
-                    d[I.E + e] = L;
-                }
+            for (int r = 0; r < P.nranks; ++r) {
+                double *d = xb_slot(P, P.peers[r], ep, P.rank);
+                d[e] = T;
+                d[I.E + e] = L;
             }
-            if (lane == 0 && P.nslices > 1) P.grp_count[grp] = 0;
         }
     }
     if (g == 0 && threadIdx.x < 32) {  // residual sums over the CTAs, error flags
@@ -1193,7 +1178,6 @@ __device__ __noinline__ void xchg_edge_apply(const Params &P, const Ctrl &c, dou
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int grp = blockIdx.x * NW + warp; grp < ngroups; grp += P.G * NW) {
         const int e = grp * RGRP + lane;
-        double rdc = 0.0;
         if (e < I.E) {
             const double T = xsum(P, ep, e), L = xsum(P, ep, I.E + e);
             const double cap = I.capacity[e];
@@ -1204,31 +1188,24 @@ __device__ __noinline__ void xchg_edge_apply(const Params &P, const Ctrl &c, dou
             P.dc[e] = dnew;
             P.adj[e] = adj;
             const double d = dnew - dold;
-            rdc = d * d;
+            P.res_dc[e] = d * d;
         }
-        for (int o = 16; o > 0; o >>= 1) rdc += __shfl_down_sync(FULL, rdc, o);
-        if (lane == 0) P.res_dc[grp] = rdc;
     }
 }
 
 // controller_eval from the exchanged residual sums (every CTA, same result)
 __device__ void xchg_controller_eval(const Params &P, Ctrl &c) {
-    if (threadIdx.x < 32) {
+    const double dcs = dcs_block(P.res_dc, P.I.E);
+    if (threadIdx.x == 0) {
         const uint64_t ep = c.xepoch - 1;
         const int64_t b = 2 * (int64_t)P.I.E;
         const int par = (int)(c.iteration & 1);
-        const int ngroups = (P.I.E + RGRP - 1) / RGRP;
-        double dcs = sum_cg(P.res_dc + threadIdx.x, threadIdx.x < ngroups ? (ngroups - 1 - threadIdx.x) / 32 + 1 : 0,
-                            32);
-        for (int o = 16; o > 0; o >>= 1) dcs += __shfl_down_sync(FULL, dcs, o);
-        if (threadIdx.x == 0) {
-            const double dx = xsum(P, ep, b + 0), rdd = xsum(P, ep, b + 1 + 3 * par),
-                         rdcon = xsum(P, ep, b + 2 + 3 * par), rdn = xsum(P, ep, b + 3 + 3 * par);
-            const bool fc = xsum(P, ep, b + 7) > 0.0, fr = xsum(P, ep, b + 8) > 0.0;
-            const int32_t ec = fc ? (__ldcg(&P.err[0]) != INT_MAX ? __ldcg(&P.err[0]) : -1) : INT_MAX;
-            const int32_t er = fr ? (__ldcg(&P.err[1]) != INT_MAX ? __ldcg(&P.err[1]) : -1) : INT_MAX;
-            if (!c.status) controller_step(P, c, sqrt(dx), sqrt(((rdd + dcs) + rdcon) + rdn), ec, er);
-        }
+        const double dx = xsum(P, ep, b + 0), rdd = xsum(P, ep, b + 1 + 3 * par),
+                     rdcon = xsum(P, ep, b + 2 + 3 * par), rdn = xsum(P, ep, b + 3 + 3 * par);
+        const bool fc = xsum(P, ep, b + 7) > 0.0, fr = xsum(P, ep, b + 8) > 0.0;
+        const int32_t ec = fc ? (__ldcg(&P.err[0]) != INT_MAX ? __ldcg(&P.err[0]) : -1) : INT_MAX;
+        const int32_t er = fr ? (__ldcg(&P.err[1]) != INT_MAX ? __ldcg(&P.err[1]) : -1) : INT_MAX;
+        if (!c.status) controller_step(P, c, sqrt(dx), sqrt(((rdd + dcs) + rdcon) + rdn), ec, er);
     }
     __syncthreads();
 }
@@ -1351,30 +1328,43 @@ __global__ void __launch_bounds__(NT, 2) k_pass(const __grid_constant__ Params P
     pass_tiles<MODE>(P, c, smem_raw, cs, seq);
 }
 
-// CTA partials -> rank totals in a fixed order: tot[0:E] = T, tot[E:2E] = L,
-// tot[2E + 0..6] = residual slots summed over CTAs, tot[2E + 7/8] = error flags.
-__global__ void k_local_reduce(const __grid_constant__ Params P) {
+// CTA partials -> rank totals in the single-GPU association (one warp per
+// edge): tot[0:E] = T, tot[E:2E] = L, tot[2E + 0..6] = residual slots summed
+// over the CTAs (lane-strided, shuffle tree: controller_eval's order),
+// tot[2E + 7/8] = error flags.
+__global__ void __launch_bounds__(NT) k_local_reduce(const __grid_constant__ Params P) {
     const int E = P.I.E;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
-        P.tot[e] = sum_cg(&P.partT[e], P.G, E);
-        P.tot[E + e] = sum_cg(&P.partL[e], P.G, E);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int e = blockIdx.x + gridDim.x * warp; e < E; e += gridDim.x * (NT / 32)) {
+        double T, L;
+        warp_edge_sums(P.partT, P.partL, P.G, E, e, lane, T, L);
+        if (lane == 0) {
+            P.tot[e] = T;
+            P.tot[E + e] = L;
+        }
     }
-    if (blockIdx.x == 0 && threadIdx.x < 7) {
-        double r = 0.0;
-        for (int g = 0; g < P.G; ++g) r += __ldcg(&P.res[g * 8 + threadIdx.x]);
-        P.tot[2 * E + threadIdx.x] = r;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 7) {
-        P.tot[2 * E + 7] = __ldcg(&P.err[0]) != INT_MAX ? 1.0 : 0.0;
-        P.tot[2 * E + 8] = __ldcg(&P.err[1]) != INT_MAX ? 1.0 : 0.0;
+    if (blockIdx.x == 0 && warp == 0) {
+        double acc[7];
+        const int off[7] = {0, 1, 2, 3, 4, 5, 6};
+        res_sums<7>(P.res, P.G, lane, off, acc);
+        for (int j = 0; j < 7; ++j)
+            for (int o = 16; o > 0; o >>= 1) acc[j] += __shfl_down_sync(FULL, acc[j], o);
+        if (lane == 0) {
+            for (int j = 0; j < 7; ++j) P.tot[2 * E + j] = acc[j];
+            P.tot[2 * E + 7] = __ldcg(&P.err[0]) != INT_MAX ? 1.0 : 0.0;
+            P.tot[2 * E + 8] = __ldcg(&P.err[1]) != INT_MAX ? 1.0 : 0.0;
+        }
     }
 }
 
 // controller step from the allreduced totals (one thread).  Inside the
 // per-run CUDA graph it also sets the graph's conditions: run the rollback
 // branch, continue the iteration loop.
-__global__ void k_ctrl_dist(const __grid_constant__ Params P, cudaGraphConditionalHandle h_loop,
-                            cudaGraphConditionalHandle h_rb, int in_graph) {
+__global__ void __launch_bounds__(NT) k_ctrl_dist(const __grid_constant__ Params P,
+                                                  cudaGraphConditionalHandle h_loop, cudaGraphConditionalHandle h_rb,
+                                                  int in_graph) {
+    // dual_capacity is replicated: its residual is rank-local and identical
+    const double dcs = dcs_block(P.res_dc, P.I.E);  // the whole CTA
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     Ctrl c = *P.ctrl;
     c.iteration += 1;
@@ -1385,9 +1375,6 @@ __global__ void k_ctrl_dist(const __grid_constant__ Params P, cudaGraphCondition
     const int E = P.I.E;
     const int par = (int)(c.iteration & 1);
     const double *t = P.tot + 2 * E;
-    double dcs = 0.0;  // dual_capacity is replicated: its residual is rank-local and identical
-    const int ngroups = (E + RGRP - 1) / RGRP;
-    for (int g = 0; g < ngroups; ++g) dcs += P.res_dc[g];
     const int32_t ec = t[7] > 0.0 ? (P.err[0] != INT_MAX ? P.err[0] : -1) : INT_MAX;
     const int32_t er = t[8] > 0.0 ? (P.err[1] != INT_MAX ? P.err[1] : -1) : INT_MAX;
     controller_step(P, c, sqrt(t[0]), sqrt(((t[1 + 3 * par] + dcs) + t[2 + 3 * par]) + t[3 + 3 * par]), ec, er);
@@ -1400,13 +1387,11 @@ __global__ void k_ctrl_dist(const __grid_constant__ Params P, cudaGraphCondition
     }
 }
 
-// kernels.py:212 and :94-96 from the allreduced per-edge totals (one warp per 32 edges)
+// kernels.py:212 and :94-96 from the allreduced per-edge totals (one thread per edge)
 __global__ void k_edge_dist(const __grid_constant__ Params P) {
     const int E = P.I.E;
-    const int grp = blockIdx.x;
-    const int e = grp * RGRP + threadIdx.x;
+    const int e = blockIdx.x * RGRP + threadIdx.x;
     const double f = P.ctrl->f;
-    double rdc = 0.0;
     if (e < E) {
         const double T = P.tot[e], L = P.tot[E + e];
         const double cap = P.I.capacity[e];
@@ -1417,10 +1402,8 @@ __global__ void k_edge_dist(const __grid_constant__ Params P) {
         P.dc[e] = dnew;
         P.adj[e] = adj;
         const double d = dnew - dold;
-        rdc = d * d;
+        P.res_dc[e] = d * d;
     }
-    for (int o = 16; o > 0; o >>= 1) rdc += __shfl_down_sync(FULL, rdc, o);
-    if (threadIdx.x == 0) P.res_dc[grp] = rdc;
 }
 
 enum { CU_AFTER_A1 = 0, CU_AFTER_EDGE = 1 };
@@ -1515,11 +1498,13 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         }
     }
     {  // small instances: smaller tiles so that the tiles fill the grid (per-tile latency
-       // bounds an iteration when every CTA holds one tile)
+       // bounds an iteration when every CTA holds one tile).  Measured plateau:
+       // NP / (3 SMs) pairs per tile, at least 512 (cfg1 15.8 us/iteration at 512,
+       // 17.3 at 256; the 630k-pair 150-node instance 29.6-30.2 us at 1,280-1,664)
         int sms = 148;
         PF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, inst->device()));
-        const int64_t fill = (I.NP / (2 * (int64_t)sms) + 63) / 64 * 64;
-        tps_min = std::min<int64_t>(tps_min, std::max<int64_t>(256, fill));
+        const int64_t fill = (I.NP / (3 * (int64_t)sms) + 63) / 64 * 64;
+        tps_min = std::min<int64_t>(tps_min, std::max<int64_t>(512, fill));
     }
     if (const char *v = getenv("PF_FAST_TPS")) tps_min = std::max(256, atoi(v)) / 64 * 64;
     const int64_t tps = std::max<int64_t>(tps_min, (max_com_pairs + 63) / 64 * 64);
@@ -1648,11 +1633,11 @@ struct FastSolver {
     const pf_instance *inst;
     pf_config cfg;
     std::shared_ptr<TileLayout> L;
-    int G = 0, nslices = 1, nbuf = 1;
+    int G = 0, nbuf = 1;
     size_t smem = 0;
     DevBuf<double> dcon[2], dn[2], dd[2], x[2];
-    DevBuf<double> D, dc, adj, ne, tot, partT, partL, sub, res, res_dc, root_sums;
-    DevBuf<int32_t> grp_count, err, cta_ptr, cta_tiles;
+    DevBuf<double> D, dc, adj, ne, tot, partT, partL, res, res_dc, root_sums;
+    DevBuf<int32_t> err, cta_ptr, cta_tiles;
     DevBuf<Ctrl> ctrl;
     Params P{};
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -1762,14 +1747,6 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     int G = prop.multiProcessorCount * per_sm;
     G = std::max(1, std::min(G, F->L->ntiles));
     F->G = G;
-    int ngroups = (int)((I.E + RGRP - 1) / RGRP);
-    int warps = G * NW;
-    // edge phase: each group's CTA partials are summed in up to 32 slices by
-    // different warps, then combined by the last slice (PF_FAST_NSLICES=1: one
-    // warp per group sums all partials -- measured equal at cfg1, 3% slower at cfg2)
-    F->nslices = std::max(1, std::min({G, 32, warps / std::max(ngroups, 1)}));
-    if (const char *v = getenv("PF_FAST_NSLICES"))
-        F->nslices = std::max(1, std::min({atoi(v), G, 32, std::max(1, warps / std::max(ngroups, 1))}));
     int64_t E = I.E ? I.E : 1;
     for (int b = 0; b < 2; ++b) {
         F->dcon[b].alloc(F->L->nslots + SLOT_ALIGN);
@@ -1809,21 +1786,17 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     }
     F->partT.alloc((size_t)G * E);
     F->partL.alloc((size_t)G * E);
-    F->sub.alloc((size_t)2 * F->nslices * E);
     F->res.alloc((size_t)G * 8);
-    F->res_dc.alloc(ngroups ? ngroups : 1);
-    F->grp_count.alloc(ngroups ? ngroups : 1);
+    F->res_dc.alloc(E);
     F->err.alloc(2);
     F->ctrl.alloc(1);
     if (cfg.trace) F->root_sums.alloc(I.C ? I.C : 1);
-    PF_CUDA(cudaMemsetAsync(F->grp_count.p, 0, sizeof(int32_t) * (ngroups ? ngroups : 1), s));
     PF_CUDA(cudaEventCreate(&F->e0));
     PF_CUDA(cudaEventCreate(&F->e1));
     Params &P = F->P;
     P.I = inst->view();
     P.ntiles = F->L->ntiles;
     P.G = G;
-    P.nslices = F->nslices;
     P.tps = F->L->tps;
     P.nbuf = F->nbuf;
     P.kspan = F->L->kspan;
@@ -1854,10 +1827,8 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     P.tot = F->tot.p;
     P.partT = F->partT.p;
     P.partL = F->partL.p;
-    P.sub = F->sub.p;
     P.res = F->res.p;
     P.res_dc = F->res_dc.p;
-    P.grp_count = F->grp_count.p;
     P.root_sums = cfg.trace ? F->root_sums.p : nullptr;
     P.ctrl = F->ctrl.p;
     P.err = F->err.p;
@@ -1909,7 +1880,7 @@ void fast_set_comm(FastSolver *F, const CommOps *ops) {
 static bool build_dist_graph(FastSolver *F, cudaStream_t s) {
     const Index &I = *F->inst->idx;
     const int64_t E = I.E;
-    const int nred = (int)std::max<int64_t>(1, (E + 255) / 256);
+    const int nred = (int)std::max<int64_t>(1, std::min<int64_t>((E + NT / 32 - 1) / (NT / 32), 1184));
     const int ngroups = (int)((E + RGRP - 1) / RGRP);
     auto ok = [](cudaError_t e) { return e == cudaSuccess; };
     cudaGraph_t top = nullptr;
@@ -1931,9 +1902,9 @@ static bool build_dist_graph(FastSolver *F, cudaStream_t s) {
         // itself and k_ctrl_dist rewrites f and need_edge)
         if (ngroups) k_edge_dist<<<ngroups, RGRP, 0, s>>>(F->P);
         k_pass<MODE_M><<<F->G, NT, F->smem, s>>>(F->P);
-        k_local_reduce<<<nred, 256, 0, s>>>(F->P);
+        k_local_reduce<<<nred, NT, 0, s>>>(F->P);
         F->comm->allreduce_sum(F->comm->ctx, F->tot.p, 2 * E + 16, s);
-        k_ctrl_dist<<<1, 32, 0, s>>>(F->P, h_loop, h_rb, 1);
+        k_ctrl_dist<<<1, NT, 0, s>>>(F->P, h_loop, h_rb, 1);
         cudaStreamCaptureStatus cst;
         cudaGraph_t capg = nullptr;
         const cudaGraphNode_t *deps = nullptr;
@@ -1951,7 +1922,7 @@ static bool build_dist_graph(FastSolver *F, cudaStream_t s) {
         cudaGraph_t rbody = ip.conditional.phGraph_out[0];
         if (!ok(cudaStreamBeginCaptureToGraph(s, rbody, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed))) break;
         k_pass<MODE_RB><<<F->G, NT, F->smem, s>>>(F->P);
-        k_local_reduce<<<nred, 256, 0, s>>>(F->P);
+        k_local_reduce<<<nred, NT, 0, s>>>(F->P);
         F->comm->allreduce_sum(F->comm->ctx, F->tot.p, 2 * E + 16, s);
         if (!ok(cudaStreamEndCapture(s, &tmp))) break;
         if (!ok(cudaGraphInstantiate(&F->dexec, top, 0))) break;
@@ -1979,7 +1950,7 @@ static bool build_dist_graph(FastSolver *F, cudaStream_t s) {
 static int64_t fast_run_dist(FastSolver *F, int64_t max_steps, cudaStream_t s, float *ms) {
     const Index &I = *F->inst->idx;
     const int64_t E = I.E;
-    const int nred = (int)std::max<int64_t>(1, (E + 255) / 256);
+    const int nred = (int)std::max<int64_t>(1, std::min<int64_t>((E + NT / 32 - 1) / (NT / 32), 1184));
     const int ngroups = (int)((E + RGRP - 1) / RGRP);
     auto read = [&]() {
         Ctrl c;
@@ -1988,7 +1959,7 @@ static int64_t fast_run_dist(FastSolver *F, int64_t max_steps, cudaStream_t s, f
         return c;
     };
     auto reduce_allreduce = [&]() {
-        k_local_reduce<<<nred, 256, 0, s>>>(F->P);
+        k_local_reduce<<<nred, NT, 0, s>>>(F->P);
         PF_CHECK_LAUNCH();
         F->comm->allreduce_sum(F->comm->ctx, F->tot.p, 2 * E + 16, s);
     };
@@ -2027,7 +1998,7 @@ static int64_t fast_run_dist(FastSolver *F, int64_t max_steps, cudaStream_t s, f
         k_pass<MODE_M><<<F->G, NT, F->smem, s>>>(F->P);
         PF_CHECK_LAUNCH();
         reduce_allreduce();
-        k_ctrl_dist<<<1, 32, 0, s>>>(F->P, 0, 0, 0);
+        k_ctrl_dist<<<1, NT, 0, s>>>(F->P, 0, 0, 0);
         PF_CHECK_LAUNCH();
         F->launches += 5;
         c = read();
