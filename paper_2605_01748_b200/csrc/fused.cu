@@ -394,43 +394,24 @@ __device__ __forceinline__ double fast_commodity_term(double S, double D, double
     return gain - npmax0(S - (D - dd));
 }
 
-// Sequential sum v = p[0] + p[st] + ... + p[(n-1) st] in index order (the same
-// association as the plain loop, so bitwise the same), with the L2 loads issued
-// 8 ahead: a runtime-trip-count loop would otherwise pay one L2 round trip per term.
-__device__ __forceinline__ double sum_cg(const double *p, int n, size_t st, double v = 0.0) {
-    int k = 0;
-    for (; k + 8 <= n; k += 8) {
-        double b[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) b[u] = __ldcg(p + (size_t)(k + u) * st);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v += b[u];
-    }
-    for (; k < n; ++k) v += __ldcg(p + (size_t)k * st);
-    return v;
-}
-
 // Lane-strided sums of NV fields of the CTAs' residual records (res[g * 8 + off[j]]
 // for g = lane, lane + 32, ...), each in index order (bitwise the plain loop),
-// the loads of 4 CTAs issued ahead.
+// in predicated chunks of 4 CTAs per lane: one L2 round trip per 128 CTAs.
 template <int NV>
 __device__ __forceinline__ void res_sums(const double *res, int G, int lane, const int (&off)[NV], double (&acc)[NV]) {
     for (int j = 0; j < NV; ++j) acc[j] = 0.0;
-    int g = lane;
-    for (; g + 96 < G; g += 128) {
+    for (int g = lane; g < G; g += 128) {
         double b[4][NV];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int j = 0; j < NV; ++j) b[u][j] = __ldcg(&res[(g + 32 * u) * 8 + off[j]]);
+            for (int j = 0; j < NV; ++j) b[u][j] = g + 32 * u < G ? __ldcg(&res[(g + 32 * u) * 8 + off[j]]) : 0.0;
 #pragma unroll
         for (int u = 0; u < 4; ++u)
+            if (g + 32 * u < G)
 #pragma unroll
-            for (int j = 0; j < NV; ++j) acc[j] += b[u][j];
+                for (int j = 0; j < NV; ++j) acc[j] += b[u][j];
     }
-    for (; g < G; g += 32)
-#pragma unroll
-        for (int j = 0; j < NV; ++j) acc[j] += __ldcg(&res[g * 8 + off[j]]);
 }
 
 // Per-edge total of the CTA partials by one warp: lane j sums CTAs j, j + 32,
@@ -441,23 +422,20 @@ __device__ __forceinline__ void res_sums(const double *res, int G, int lane, con
 __device__ __forceinline__ void warp_edge_sums(const double *pT, const double *pL, int G, int E, int e, int lane,
                                                double &T, double &L) {
     double t = 0.0, l = 0.0;
-    int g = lane;
-    for (; g + 96 < G; g += 128) {
+    for (int g = lane; g < G; g += 128) {  // predicated chunks of 4 CTAs: one round trip per 128 CTAs
         double bt[4], bl[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            bt[u] = __ldcg(pT + (size_t)(g + 32 * u) * E + e);
-            bl[u] = __ldcg(pL + (size_t)(g + 32 * u) * E + e);
+            const bool in = g + 32 * u < G;
+            bt[u] = in ? __ldcg(pT + (size_t)(g + 32 * u) * E + e) : 0.0;
+            bl[u] = in ? __ldcg(pL + (size_t)(g + 32 * u) * E + e) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            t += bt[u];
-            l += bl[u];
-        }
-    }
-    for (; g < G; g += 32) {
-        t += __ldcg(pT + (size_t)g * E + e);
-        l += __ldcg(pL + (size_t)g * E + e);
+        for (int u = 0; u < 4; ++u)
+            if (g + 32 * u < G) {
+                t += bt[u];
+                l += bl[u];
+            }
     }
     for (int o = 16; o > 0; o >>= 1) {
         t += __shfl_down_sync(FULL, t, o);
@@ -473,15 +451,14 @@ __device__ __forceinline__ void warp_edge_sums(const double *pT, const double *p
 __device__ double dcs_block(const double *res_dc, int E) {
     __shared__ double wred[NT / 32];
     double v = 0.0;
-    int e = threadIdx.x;
-    for (; e + 3 * NT < E; e += 4 * NT) {
+    for (int e = threadIdx.x; e < E; e += 4 * NT) {  // predicated chunks of 4
         double b[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) b[u] = __ldcg(res_dc + e + u * NT);
+        for (int u = 0; u < 4; ++u) b[u] = e + u * NT < E ? __ldcg(res_dc + e + u * NT) : 0.0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v += b[u];
+        for (int u = 0; u < 4; ++u)
+            if (e + u * NT < E) v += b[u];
     }
-    for (; e < E; e += NT) v += __ldcg(res_dc + e);
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(FULL, v, o);
     __syncthreads();
     if ((threadIdx.x & 31) == 0) wred[threadIdx.x >> 5] = v;
