@@ -587,12 +587,24 @@ int pf_validate_allocation(const pf_instance *inst, const double *rates, double 
         DeviceGuard g(inst->device());
         const Index &I = *inst->idx;
         cudaStream_t s = inst->stream;
-        DevBuf<double> r(I.P + 1), ov(I.E + 1), ex(I.C + 1);
-        h2d(r.p, rates, I.P, s);
-        TraceScratch ts;
-        violation_stats(inst->view(), r.p, tol, ov.p, ex.p, ts, rep, s);
-        if (edge_overload) d2h(edge_overload, ov.p, I.E, s);
-        if (commodity_excess) d2h(commodity_excess, ex.p, I.C, s);
+        // scratch cached on the instance (no per-call cudaMalloc / cudaFree)
+        struct ValWS {
+            DevBuf<double> r, ov, ex;
+            TraceScratch ts;
+        };
+        std::lock_guard<std::mutex> lk(inst->ws_mu);
+        if (!inst->val_ws) {
+            auto w = std::make_shared<ValWS>();
+            w->r.alloc(I.P + 1);
+            w->ov.alloc(I.E + 1);
+            w->ex.alloc(I.C + 1);
+            inst->val_ws = w;
+        }
+        ValWS &w = *static_cast<ValWS *>(inst->val_ws.get());
+        h2d(w.r.p, rates, I.P, s);
+        violation_stats(inst->view(), w.r.p, tol, w.ov.p, w.ex.p, w.ts, rep, s);
+        if (edge_overload) d2h(edge_overload, w.ov.p, I.E, s);
+        if (commodity_excess) d2h(commodity_excess, w.ex.p, I.C, s);
         PF_CUDA(cudaStreamSynchronize(s));
     });
 }

@@ -112,6 +112,12 @@ __global__ void k_gather_edge_major(InstView I, const double *__restrict__ pv, d
     if (t < I.NP) vals[t] = pv[I.edge_pairs[t]];
 }
 
+// edge-major copy of the per-path rates through the incidence: vals[t] = x[pair_path[edge_pairs[t]]]
+__global__ void k_gather_rates_em_pairs(InstView I, const double *__restrict__ x, double *__restrict__ vals) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < I.NP) vals[t] = x[I.pair_path[I.edge_pairs[t]]];
+}
+
 // edge-major copy of the per-path rates: vals[t] = x[pair_path[edge_pairs[t]]]
 __global__ void k_gather_rates_edge_major(int64_t NP, const int32_t *__restrict__ epath,
                                           const double *__restrict__ x, double *__restrict__ vals) {
@@ -328,6 +334,25 @@ __global__ void k_reset_flags(Flags *f) {
 // ---------------- trace / validation helpers
 
 // numpy pairwise_sum (PW_BLOCKSIZE 128) -- np.sum/np.mean order.
+// np_pairwise's leaf branches (n <= 128): no recursion, no stack
+__device__ __forceinline__ double np_pairwise_leaf(const double *a, int64_t n) {
+    if (n < 8) {
+        double res = 0.0;
+        for (int64_t i = 0; i < n; ++i) res += a[i];
+        return res;
+    }
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int64_t i;
+    for (i = 8; i < n - (n % 8); i += 8)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += a[i];
+    return res;
+}
+
 __device__ double np_pairwise(const double *a, int64_t n) {
     if (n < 8) {
         double res = 0.0;
@@ -348,68 +373,166 @@ __device__ double np_pairwise(const double *a, int64_t n) {
     return np_pairwise(a, n2) + np_pairwise(a + n2, n - n2);
 }
 
-// np_pairwise(a, n) by one CTA, bitwise the same: thread 0 enumerates the
-// tree's leaves (<= 128 elements, >= 64 unless n <= 128) left to right, the
-// block sums the leaves in parallel, thread 0 adds them up the same tree.
-// Both traversals are iterative over one small stack (depth <= 27 for
-// n < 2^32).  leaf_lo and leaf_sum hold n / 32 + 8 entries.  Every thread gets
+// np_pairwise's split of a node of m > 128 elements: the left child's size.
+__device__ __forceinline__ int32_t np_split(int32_t m) {
+    int32_t n2 = m / 2;
+    return n2 - n2 % 8;
+}
+
+constexpr int NPW_DEPTH = 5;  // the top of the tree expanded by thread 0 (<= 32 subtrees)
+
+// np_pairwise(a, n) by one CTA, bitwise the same.
+//  1. thread 0 expands the top NPW_DEPTH levels of numpy's split tree, in order:
+//     <= 32 frontier nodes (subtrees, or leaves above that depth);
+//  2. lane j of warp 0 counts its subtree's leaves (<= 128 elements, >= 64
+//     unless n <= 128), a warp scan places them, lane j enumerates them;
+//  3. the block sums the leaves in parallel (np_pairwise's leaf branch);
+//  4. lane j adds its subtree up numpy's tree (post-order), thread 0 adds the
+//     frontier values up the top levels.
+// leaf_lo and leaf_sum hold n / 32 + 8 entries; n < 2^31.  Every thread gets
 // the result.
-__device__ double cta_np_pairwise(const double *a, int64_t n, int64_t *leaf_lo, double *leaf_sum) {
-    __shared__ int64_t s_L;
-    __shared__ double s_res;
-    if (threadIdx.x == 0) {
-        int64_t stk[64];  // enumeration: (lo, m) pairs; combine: m to visit / ~m to add
-        int sp = 0;
-        int64_t L = 0;
+__device__ double cta_np_pairwise(const double *a, int64_t n64, int64_t *leaf_lo, double *leaf_sum) {
+    __shared__ int32_t f_lo[2][32], f_n[2][32];
+    __shared__ int32_t f_cnt, f_off[33];
+    __shared__ double f_val[32], s_res;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int32_t n = (int32_t)n64;
+    if (tid == 0) {
+        int cnt = 0, cur = 0;
         if (n > 0) {
-            stk[0] = 0;
-            stk[1] = n;
-            sp = 2;
-        }
-        while (sp) {
-            sp -= 2;
-            const int64_t lo = stk[sp], m = stk[sp + 1];
-            if (m <= 128) {
-                leaf_lo[L++] = lo;
-            } else {
-                int64_t n2 = m / 2;
-                n2 -= n2 % 8;
-                stk[sp] = lo + n2;  // right, visited after the left
-                stk[sp + 1] = m - n2;
-                stk[sp + 2] = lo;
-                stk[sp + 3] = n2;
-                sp += 4;
+            f_lo[0][0] = 0;
+            f_n[0][0] = n;
+            cnt = 1;
+            for (int d = 0; d < NPW_DEPTH; ++d) {  // in-order expansion, level by level
+                int k = 0;
+                for (int i = 0; i < cnt; ++i) {
+                    const int32_t lo = f_lo[cur][i], m = f_n[cur][i];
+                    if (m > 128) {
+                        const int32_t n2 = np_split(m);
+                        f_lo[cur ^ 1][k] = lo;
+                        f_n[cur ^ 1][k++] = n2;
+                        f_lo[cur ^ 1][k] = lo + n2;
+                        f_n[cur ^ 1][k++] = m - n2;
+                    } else {
+                        f_lo[cur ^ 1][k] = lo;
+                        f_n[cur ^ 1][k++] = m;
+                    }
+                }
+                cur ^= 1;
+                cnt = k;
             }
         }
-        leaf_lo[L] = n;
-        s_L = L;
+        if (cur) {
+            for (int i = 0; i < cnt; ++i) {
+                f_lo[0][i] = f_lo[1][i];
+                f_n[0][i] = f_n[1][i];
+            }
+        }
+        f_cnt = cnt;
     }
     __syncthreads();
-    const int64_t L = s_L;
-    for (int64_t l = threadIdx.x; l < L; l += blockDim.x)
-        leaf_sum[l] = np_pairwise(a + leaf_lo[l], leaf_lo[l + 1] - leaf_lo[l]);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double res = 0.0;
-        if (n > 0) {
-            int64_t stk[64];
-            double val[32];
-            int sp = 0, vp = 0;
-            int64_t i = 0;
-            stk[sp++] = n;
+    const int F = f_cnt;
+    if (tid < 32) {  // leaves per frontier node, placed by a warp scan, enumerated in order
+        int32_t stk[64];
+        int32_t c = 0;
+        if (lane < F) {
+            int sp = 0;
+            stk[sp++] = f_n[0][lane];
             while (sp) {
-                const int64_t m = stk[--sp];
-                if (m < 0) {  // both children done: left + right (np_pairwise's order)
-                    const double b = val[--vp], c = val[--vp];
-                    val[vp++] = c + b;
-                } else if (m <= 128) {
-                    val[vp++] = leaf_sum[i++];
+                const int32_t mm = stk[--sp];
+                if (mm <= 128) {
+                    ++c;
                 } else {
-                    int64_t n2 = m / 2;
-                    n2 -= n2 % 8;
-                    stk[sp++] = ~m;
-                    stk[sp++] = m - n2;
+                    const int32_t n2 = np_split(mm);
+                    stk[sp++] = mm - n2;
                     stk[sp++] = n2;
+                }
+            }
+        }
+        int32_t incl = c;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        f_off[lane] = incl - c;
+        if (lane == 31) f_off[32] = incl;
+        if (lane < F) {
+            int64_t L = incl - c;
+            int sp = 0;
+            stk[sp++] = f_lo[0][lane];
+            stk[sp++] = f_n[0][lane];
+            while (sp) {
+                sp -= 2;
+                const int32_t lo = stk[sp], mm = stk[sp + 1];
+                if (mm <= 128) {
+                    leaf_lo[L++] = lo;
+                } else {
+                    const int32_t n2 = np_split(mm);
+                    stk[sp] = lo + n2;
+                    stk[sp + 1] = mm - n2;
+                    stk[sp + 2] = lo;
+                    stk[sp + 3] = n2;
+                    sp += 4;
+                }
+            }
+        }
+        const int32_t total = __shfl_sync(0xffffffffu, incl, 31);  // (f_off[32] is not yet visible to lane 0)
+        if (lane == 0) leaf_lo[total] = n;
+    }
+    __syncthreads();
+    const int64_t L = f_off[32];
+    for (int64_t l = tid; l < L; l += blockDim.x)
+        leaf_sum[l] = np_pairwise_leaf(a + leaf_lo[l], leaf_lo[l + 1] - leaf_lo[l]);
+    __syncthreads();
+    if (tid < 32 && lane < F) {  // each frontier subtree added up numpy's tree
+        int32_t stk[64];
+        double val[32];
+        int sp = 0, vp = 0;
+        int64_t i = f_off[lane];
+        stk[sp++] = f_n[0][lane];
+        while (sp) {
+            const int32_t mm = stk[--sp];
+            if (mm < 0) {
+                const double b = val[--vp], c2 = val[--vp];
+                val[vp++] = c2 + b;
+            } else if (mm <= 128) {
+                val[vp++] = leaf_sum[i++];
+            } else {
+                const int32_t n2 = np_split(mm);
+                stk[sp++] = ~mm;
+                stk[sp++] = mm - n2;
+                stk[sp++] = n2;
+            }
+        }
+        f_val[lane] = val[0];
+    }
+    __syncthreads();
+    if (tid == 0) {  // the top levels: a node at depth NPW_DEPTH or a leaf is a frontier value
+        double res = 0.0;
+        if (F > 0) {
+            int32_t stk[2 * NPW_DEPTH + 4];
+            int32_t dep[2 * NPW_DEPTH + 4];
+            double val[NPW_DEPTH + 2];
+            int sp = 0, vp = 0, fi = 0;
+            stk[sp] = n;
+            dep[sp++] = 0;
+            while (sp) {
+                --sp;
+                const int32_t mm = stk[sp];
+                const int d = dep[sp];
+                if (mm < 0) {
+                    const double b = val[--vp], c2 = val[--vp];
+                    val[vp++] = c2 + b;
+                } else if (mm <= 128 || d == NPW_DEPTH) {
+                    val[vp++] = f_val[fi++];
+                } else {
+                    const int32_t n2 = np_split(mm);
+                    stk[sp] = ~mm;
+                    dep[sp++] = d;
+                    stk[sp] = mm - n2;
+                    dep[sp++] = d + 1;
+                    stk[sp] = n2;
+                    dep[sp++] = d + 1;
                 }
             }
             res = val[0];
@@ -480,28 +603,41 @@ __global__ void k_worst_negative(int32_t P, const double *x, double tol, double 
 __global__ void __launch_bounds__(1024) k_compact_mean(const double *rel_e, int32_t E, const double *rel_c,
                                                        int32_t C, double *tmp, double *out, int64_t *leaf_lo,
                                                        double *leaf_sum) {
+    constexpr int PER = 8;  // contiguous elements per thread per block step
     __shared__ int32_t wcnt[32];
     __shared__ int64_t s_base;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
     const int64_t N = (int64_t)E + C;
     if (tid == 0) s_base = 0;
     __syncthreads();
-    for (int64_t c0 = 0; c0 < N; c0 += blockDim.x) {
-        const int64_t i = c0 + tid;
-        const double v = i < E ? rel_e[i] : (i < N ? rel_c[i - E] : CUDART_NAN);
-        const bool keep = !isnan(v);
-        const unsigned bal = __ballot_sync(0xffffffffu, keep);
-        if (lane == 0) wcnt[warp] = __popc(bal);
+    for (int64_t c0 = 0; c0 < N; c0 += (int64_t)PER * blockDim.x) {
+        const int64_t i0 = c0 + (int64_t)PER * tid;
+        double v[PER];
+        int32_t cnt = 0;
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int64_t i = i0 + u;
+            v[u] = i < E ? rel_e[i] : (i < N ? rel_c[i - E] : CUDART_NAN);
+            cnt += !isnan(v[u]);
+        }
+        int32_t incl = cnt;  // warp inclusive scan of the per-thread counts
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) wcnt[warp] = incl;
         __syncthreads();
         int32_t before = 0, total = 0;
         for (int w = 0; w < nw; ++w) {
             before += w < warp ? wcnt[w] : 0;
             total += wcnt[w];
         }
-        const int64_t base = s_base;
-        if (keep) tmp[base + before + __popc(bal & ((1u << lane) - 1u))] = v;
+        int64_t pos = s_base + before + (incl - cnt);
+#pragma unroll
+        for (int u = 0; u < PER; ++u)
+            if (!isnan(v[u])) tmp[pos++] = v[u];
         __syncthreads();
-        if (tid == 0) s_base = base + total;
+        if (tid == 0) s_base += total;
     }
     __syncthreads();
     const int64_t n = s_base;
@@ -626,6 +762,7 @@ static void ensure_trace_scratch(const InstView &I, TraceScratch &ts) {
     if (ts.leaf_lo.n < nleaf) ts.leaf_lo.alloc(nleaf);
     if (ts.cnt.n < 4) ts.cnt.alloc(4);
     if (ts.out.n < 8) ts.out.alloc(8);
+    if (ts.em.n < (size_t)I.NP + 1) ts.em.alloc(I.NP + 1);
 }
 
 // controller.py:173-194 _trace_row: objective + pct_violated + mean_relative_violation.
@@ -653,7 +790,15 @@ void trace_stats(const InstView &I, const double *x, const double *root_sums, in
 void violation_stats(const InstView &I, const double *x, double tol, double *d_overload, double *d_excess,
                      TraceScratch &ts, pf_violation *rep, cudaStream_t s) {
     ensure_trace_scratch(I, ts);
-    exact_edge_loads_of_rates(I, x, ts.loads.p, s);
+    // exact-order edge loads through an edge-major copy (same association as
+    // exact_edge_loads_of_rates, one parallel gather instead of per-lane chains)
+    if (I.NP && I.E) {
+        k_gather_rates_em_pairs<<<ceil_div(I.NP, 256), 256, 0, s>>>(I, x, ts.em.p);
+        k_edge_blk_contig<<<ceil_div((int64_t)I.E * 32, 128), 128, 0, s>>>(I, ts.em.p, ts.loads.p);
+        PF_CHECK_LAUNCH();
+    } else {
+        exact_edge_loads_of_rates(I, x, ts.loads.p, s);
+    }
     exact_commodity_sums(I, x, ts.sums.p, s);
     PF_CUDA(cudaMemsetAsync(ts.cnt.p, 0, sizeof(int32_t) * 4, s));
     int32_t n = I.E > I.C ? I.E : I.C;

@@ -158,6 +158,7 @@ struct pf_instance {
     cudaStream_t stream = nullptr;
     mutable std::mutex ws_mu;
     mutable std::shared_ptr<void> proj_ws;  // projection scratch (projection.cu)
+    mutable std::shared_ptr<void> val_ws;   // validate_allocation scratch (capi.cu), under ws_mu
     // one idle fast-mode solver kept for the next solve on this instance (fused.cu):
     // its device buffers are reused instead of re-allocated per solve
     mutable void *fast_pool = nullptr;
@@ -246,6 +247,7 @@ void reset_flags(Flags *f, cudaStream_t s);
 // Trace helpers (model.py:335-369, kernels.py:47-66 summed with numpy pairwise order).
 struct TraceScratch {
     DevBuf<double> loads, sums, rel, tmp, leaf_sum;
+    DevBuf<double> em;  // [NP] edge-major copy of the rates (exact-order edge loads)
     DevBuf<int64_t> leaf_lo;
     DevBuf<int32_t> cnt;
     DevBuf<double> out;  // [4]: objective, pct, mean_rel, n_viol
