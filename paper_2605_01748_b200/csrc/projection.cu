@@ -486,6 +486,7 @@ __global__ void __launch_bounds__(CL_NT, 1) k_edge_trim_cluster(InstView I, cons
     const int32_t nviol = *nviol_p;
     long long st_trimmed = 0, st_passes = 0;
     int ph = 0;
+    cl.sync();  // every CTA of the cluster is running before any DSMEM access
     // every edge is gathered anyway, so its load is always the fresh sum of the
     // gathered rates (the reference re-sums each edge at its turn,
     // projection.py:84-88); no dirty-edge bookkeeping
