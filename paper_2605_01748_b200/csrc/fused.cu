@@ -937,9 +937,12 @@ __device__ PassIO pass_io(const Params &P, const Ctrl &c) {
 }
 
 // Per-CTA persistent shared state.
+constexpr int DL = 64;  // tile descriptors of a CTA's first DL tiles kept in shared memory
+
 struct CtaShared {
     uint64_t bar[2];
     TileDesc sd[2];
+    TileDesc dl[DL];  // this pass's tiles in walk order (thread 0 reads them on the tile boundary)
     PassIO io;
     Tail tails[NW];
     double red[NW];
@@ -965,6 +968,9 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
     const int t0 = P.cta_ptr[g], my = P.cta_ptr[g + 1] - t0;
     const bool rev = (c.iteration & 1) != 0;
     auto tile_of = [&](int k) { return P.cta_tiles[t0 + (rev ? my - 1 - k : k)]; };
+    // the next tile's descriptor from shared memory: no dependent global loads
+    // on thread 0's path between two tiles (its TMA issue and L2 prefetch)
+    auto desc_of = [&](int k) -> TileDesc { return k < DL ? cs.dl[k] : P.desc[tile_of(k)]; };
     const bool dbl = P.nbuf == 2;
     if (tid == 0) {
         cs.io = pass_io<MODE>(P, c);
@@ -975,6 +981,7 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
             issue_tile<MODE>(P, cs.io, cs.sd[b], base, sp, b, &cs.bar[b]);
         }
     }
+    for (int i = tid; i < my && i < DL; i += NT) cs.dl[i] = P.desc[tile_of(i)];  // visible after the barrier below
     for (int e = tid; e < E; e += NT) {
         if (P.acc_smem) {
             A.acc[e] = make_double2(0.0, 0.0);
@@ -999,10 +1006,10 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
         if (tid == 0 && k + 1 < my) {
             if (dbl) {  // prefetch the next tile into the other stage
                 const int nb = b ^ 1;
-                cs.sd[nb] = P.desc[tile_of(k + 1)];
+                cs.sd[nb] = desc_of(k + 1);
                 issue_tile<MODE>(P, io, cs.sd[nb], base, sp, nb, &cs.bar[nb]);
             } else if (k + P.pf_dist < my) {  // single stage: warm L2 with a later tile's pair data
-                const TileDesc dn_ = P.desc[tile_of(k + P.pf_dist)];
+                const TileDesc dn_ = desc_of(k + P.pf_dist);
                 prefetch_l2(io.dcon_in + dn_.sb, 8u * even(dn_.np));
                 prefetch_l2(P.meta + (size_t)dn_.mb16 * 16,
                             (uint32_t)meta_off(dn_.np, dn_.p1 - dn_.p0, dn_.c1 - dn_.c0).bytes);
@@ -1013,11 +1020,11 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
         const StageView st = stage_view(base, sp, b, d);
         tile_compute<MODE>(P, c, io, d, st, A, cs.tails, fx, r_x, r_dd, r_dcon, r_dn);
         __syncthreads();  // the stage is free for the next TMA (its generic writes were proxy-fenced)
-        apply_fix<MODE>(fx, cs.tails, A);
-        if (!dbl && tid == 0 && k + 1 < my) {
-            cs.sd[0] = P.desc[tile_of(k + 1)];
+        if (!dbl && tid == 0 && k + 1 < my) {  // before the fix-ups (they do not touch the stage)
+            cs.sd[0] = desc_of(k + 1);
             issue_tile<MODE>(P, io, cs.sd[0], base, sp, 0, &cs.bar[0]);
         }
+        apply_fix<MODE>(fx, cs.tails, A);
     }
     __syncthreads();  // last tile's fix-ups
     for (int e = tid; e < E; e += NT) {
@@ -1449,7 +1456,7 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         int per_sm = 0, reserved = 0;
         PF_CUDA(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, inst->device()));
         PF_CUDA(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, inst->device()));
-        const int64_t budget = per_sm / 2 - reserved - 1024;
+        const int64_t budget = per_sm / 2 - reserved - 3072;  // static shared memory (CtaShared, ...)
         if (smem_plan(1024, (int)I.E, 1).total > budget || getenv("PF_FAST_LARGE_E")) {
             // large E: the shared-memory edge tables rule out two CTAs per SM; the
             // adjustment table is read through L1 (one CTA per SM, large tiles), or
@@ -1466,7 +1473,7 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
                 while (tps_min > 512 && smem_plan((int)tps_min, (int)I.E, 1, false, false).total > budget)
                     tps_min -= 256;
             } else {
-                const int64_t budget1 = per_sm - reserved - 1024;
+                const int64_t budget1 = per_sm - reserved - 3072;
                 while (tps_min > 512 && smem_plan((int)tps_min, (int)I.E, 1, false).total > budget1)
                     tps_min -= 256;
             }
