@@ -942,7 +942,8 @@ constexpr int DL = 64;  // tile descriptors of a CTA's first DL tiles kept in sh
 struct CtaShared {
     uint64_t bar[2];
     TileDesc sd[2];
-    TileDesc dl[DL];  // this pass's tiles in walk order (thread 0 reads them on the tile boundary)
+    TileDesc dl[DL];  // this CTA's tiles (thread 0 reads them on the tile boundaries)
+    int32_t dl_rev;   // walk direction dl[] is stored in; -1 = not filled (a CTA owns <= DL tiles: kept)
     PassIO io;
     Tail tails[NW];
     double red[NW];
@@ -969,19 +970,24 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
     const bool rev = (c.iteration & 1) != 0;
     auto tile_of = [&](int k) { return P.cta_tiles[t0 + (rev ? my - 1 - k : k)]; };
     // the next tile's descriptor from shared memory: no dependent global loads
-    // on thread 0's path between two tiles (its TMA issue and L2 prefetch)
-    auto desc_of = [&](int k) -> TileDesc { return k < DL ? cs.dl[k] : P.desc[tile_of(k)]; };
+    // on thread 0's path between two tiles (its TMA issue and L2 prefetch).  A
+    // CTA's tile set is fixed for the launch: with <= DL tiles, dl[] is filled by
+    // the first pass and read in either walk direction afterwards.
+    const bool keep = my <= DL && cs.dl_rev >= 0;
+    const bool flip = keep && cs.dl_rev != (rev ? 1 : 0);
+    auto desc_of = [&](int k) -> TileDesc { return k < DL ? cs.dl[flip ? my - 1 - k : k] : P.desc[tile_of(k)]; };
     const bool dbl = P.nbuf == 2;
     if (tid == 0) {
         cs.io = pass_io<MODE>(P, c);
         fence_proxy_async();  // this pass's inputs were written by generic stores after a grid barrier
         if (my > 0) {
             const int b = dbl ? (seq & 1) : 0;
-            cs.sd[b] = P.desc[tile_of(0)];
+            cs.sd[b] = keep ? desc_of(0) : P.desc[tile_of(0)];
             issue_tile<MODE>(P, cs.io, cs.sd[b], base, sp, b, &cs.bar[b]);
         }
     }
-    for (int i = tid; i < my && i < DL; i += NT) cs.dl[i] = P.desc[tile_of(i)];  // visible after the barrier below
+    if (!keep)
+        for (int i = tid; i < my && i < DL; i += NT) cs.dl[i] = P.desc[tile_of(i)];  // visible after the barrier below
     for (int e = tid; e < E; e += NT) {
         if (P.acc_smem) {
             A.acc[e] = make_double2(0.0, 0.0);
@@ -996,6 +1002,7 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
     // so no stale L1 line survives
     if (!P.adj_smem) asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
     __syncthreads();
+    if (tid == 0 && !keep && my <= DL) cs.dl_rev = rev ? 1 : 0;  // every thread read dl_rev before the barrier
     const PassIO &io = cs.io;
     double r_x = 0.0, r_dd = 0.0, r_dcon = 0.0, r_dn = 0.0;
     Fix fx;
@@ -1051,6 +1058,7 @@ __device__ __forceinline__ void cta_init(CtaShared &cs) {
     if (threadIdx.x == 0) {
         mbar_init(&cs.bar[0], 1);
         mbar_init(&cs.bar[1], 1);
+        cs.dl_rev = -1;
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
