@@ -182,7 +182,7 @@ struct Params {
     double *dc, *adj;
     const double *ne;       // [E] paths per edge (global across ranks when sharded)
     double *tot;            // [2E + 16] rank totals (multi-GPU): T, L, residual sums, error counts
-    double *partT, *partL;  // [G][E]
+    double *partT, *partL;  // [E][G]: edge-major, so one edge's CTA partials are contiguous
     double *res;            // [G][8]: 0 dx | 1..3 (dd, dcon, dn) parity 0 | 4..6 parity 1
     double *res_dc;         // [E] squared dual_capacity change per edge
     double *root_sums;      // [C] or null
@@ -427,8 +427,8 @@ __device__ __forceinline__ void warp_edge_sums(const double *pT, const double *p
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const bool in = g + 32 * u < G;
-            bt[u] = in ? __ldcg(pT + (size_t)(g + 32 * u) * E + e) : 0.0;
-            bl[u] = in ? __ldcg(pL + (size_t)(g + 32 * u) * E + e) : 0.0;
+            bt[u] = in ? __ldcg(pT + (size_t)e * G + g + 32 * u) : 0.0;  // coalesced: [E][G]
+            bl[u] = in ? __ldcg(pL + (size_t)e * G + g + 32 * u) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -588,7 +588,8 @@ struct Tail {
 struct Acc {
     double *adj, *y;
     double2 *acc;      // per edge {T, L} in shared memory, or
-    double *gT, *gL;   // this CTA's partial rows (large E)
+    double *gT, *gL;   // this CTA's partials (large E): edge e at gT[e * gs]
+    int gs;
 };
 
 template <int MODE>
@@ -599,8 +600,9 @@ __device__ __forceinline__ void acc_add(const Acc &A, int e, double T, double L)
         if (MODE != MODE_RB) v.y += L;
         A.acc[e] = v;
     } else {  // L2-resident CTA-private rows (bypass L1: it holds the adjustment table)
-        __stcg(&A.gT[e], __ldcg(&A.gT[e]) + T);
-        if (MODE != MODE_RB) __stcg(&A.gL[e], __ldcg(&A.gL[e]) + L);
+        const size_t o = (size_t)e * A.gs;
+        __stcg(&A.gT[o], __ldcg(&A.gT[o]) + T);
+        if (MODE != MODE_RB) __stcg(&A.gL[o], __ldcg(&A.gL[o]) + L);
     }
 }
 
@@ -963,8 +965,9 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
     Acc A;
     A.adj = P.adj_smem ? (double *)(base + sp.adj) : P.adj;
     A.acc = P.acc_smem ? (double2 *)(base + sp.acc) : nullptr;
-    A.gT = P.partT + (size_t)g * E;
-    A.gL = P.partL + (size_t)g * E;
+    A.gT = P.partT + g;  // column g of the edge-major partials
+    A.gL = P.partL + g;
+    A.gs = P.G;
     A.y = (double *)(base + sp.y);
     const int t0 = P.cta_ptr[g], my = P.cta_ptr[g + 1] - t0;
     const bool rev = (c.iteration & 1) != 0;
@@ -988,14 +991,25 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
     }
     if (!keep)
         for (int i = tid; i < my && i < DL; i += NT) cs.dl[i] = P.desc[tile_of(i)];  // visible after the barrier below
-    for (int e = tid; e < E; e += NT) {
-        if (P.acc_smem) {
-            A.acc[e] = make_double2(0.0, 0.0);
-        } else {
-            __stcg(&A.gT[e], 0.0);
-            if (MODE != MODE_RB) __stcg(&A.gL[e], 0.0);
+    for (int e0 = tid; e0 < E; e0 += 4 * NT) {  // the adjustment loads of 4 edges in flight
+        double av[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * NT;
+            av[u] = P.adj_smem && MODE != MODE_A1 && e < E ? __ldcg(&P.adj[e]) : 0.0;
         }
-        if (P.adj_smem) A.adj[e] = MODE == MODE_A1 ? 0.0 : __ldcg(&P.adj[e]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * NT;
+            if (e >= E) break;
+            if (P.acc_smem) {
+                A.acc[e] = make_double2(0.0, 0.0);
+            } else {
+                __stcg(&A.gT[(size_t)e * A.gs], 0.0);
+                if (MODE != MODE_RB) __stcg(&A.gL[(size_t)e * A.gs], 0.0);
+            }
+            if (P.adj_smem) A.adj[e] = av[u];
+        }
     }
     // without the shared table adj is read through L1 (ld.global.ca); it was
     // rewritten by the edge phase before the grid barrier: acquire at gpu scope
@@ -1037,8 +1051,8 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
     for (int e = tid; e < E; e += NT) {
         if (!P.acc_smem) break;  // the rows are the partials already
         const double2 v = A.acc[e];
-        P.partT[(size_t)g * E + e] = v.x;
-        if (MODE != MODE_RB) P.partL[(size_t)g * E + e] = v.y;
+        P.partT[(size_t)e * P.G + g] = v.x;
+        if (MODE != MODE_RB) P.partL[(size_t)e * P.G + g] = v.y;
     }
     double *r = P.res + g * 8;
     double v4[4] = {r_x, r_dd, r_dcon, r_dn};
