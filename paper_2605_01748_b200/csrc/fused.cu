@@ -68,7 +68,8 @@ constexpr int GPATH = 32;         // max paths per group (one lane per path)
 constexpr int TPATH = NW * GPATH; // max paths per tile
 constexpr int TCOM = TPATH;       // max commodities per tile
 static_assert(TPATH <= 256, "tile-local path / commodity indices are u8");
-constexpr int TPS_MIN = 2560;     // default max pairs per tile
+constexpr int TPS_MIN = 2560;     // default max pairs per tile (large-E layouts)
+constexpr int TPS_CAP = 4096;     // upper bound of the shared-memory fit (two CTAs per SM)
 constexpr int SLOT_ALIGN = 16;    // tile start alignment in the per-pair arrays (128 B)
 constexpr int RGRP = 32;          // edges per reduction group (one lane per edge)
 constexpr unsigned FULL = 0xffffffffu;
@@ -1500,7 +1501,11 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
                     tps_min -= 256;
             }
         } else {
-            while (tps_min > 1024 && smem_plan((int)tps_min, (int)I.E, 1).total > budget) tps_min -= 256;
+            // the largest tile that keeps two CTAs per SM: fewer, larger tiles cut
+            // the per-tile fixed costs (config 2: 2,560 pairs 307 us/iteration,
+            // 2,816 pairs 302 us; one more pair-row and only one CTA fits)
+            tps_min = TPS_CAP;
+            while (tps_min > 1024 && smem_plan((int)tps_min, (int)I.E, 1).total > budget) tps_min -= 64;
         }
     }
     {  // small instances: smaller tiles so that the tiles fill the grid (per-tile latency
