@@ -320,6 +320,14 @@ def config45(name, device=0):
                              "optimality_vs_cold_resolve": pf.optimality_from_sums(warm.sums, fresh.sums, theta)},
             "cold_resolve": {"iterations": int(fresh.iterations), "converged": bool(fresh.converged),
                              "ms": 1e3 * fresh.runtime_s}}
+    # the stale allocation carried into the failed state (oracles.py:262-297,
+    # bitwise the reference's): wall time of the GPU carry, host buffers
+    pf.dao_carry_rates(cold.rates, failed)  # warm (workspace)
+    t0 = time.perf_counter()
+    carried = pf.dao_carry_rates(cold.rates, failed)
+    dao_ms = 1e3 * (time.perf_counter() - t0)
+    out4["dao_carry"] = {"ms": dao_ms, "feasible": bool(pf.validate_allocation(failed, carried).feasible),
+                         "dao_evaluate_vs_cold_resolve": pf.dao_evaluate(cold, failed, fresh, theta)}
     out5 = []
     for at in (0, 1, 2, 3, 4, None):
         r = pf.solve(inst, pf.SolverConfig(mode="fast", alpha_target=at))

@@ -25,6 +25,7 @@
  *   pf_det_diff_norm            _reduce.py:118-128 det_diff_norm
  *   pf_score_paths              projection.py:22-32 score_paths
  *   pf_project                  projection.py:51-107 project
+ *   pf_dao_carry_rates          oracles.py:262-287 dao_carry_rates (drift carry)
  *   pf_solve                    controller.py:197-284 solve
  *   pf_solver_*                 controller.py:197-284, split so the device loop can
  *                               be timed / sharded (no reference equivalent)
@@ -168,6 +169,11 @@ int pf_solve_sum_equation(double w_sum, double beta, double q, int64_t alpha, do
 /* ---- projection ---- */
 int pf_score_paths(const pf_instance *inst, const double *rates, int64_t alpha, double *scores);
 int pf_project(const pf_instance *inst, const double *rates, int64_t alpha, double *out);
+
+/* ---- drift carry (oracles.py:262-287): a stale allocation applied to the
+ * instance's current conditions; bitwise equal to the reference.  `passes`
+ * (nullable) = edge passes that scaled. ---- */
+int pf_dao_carry_rates(const pf_instance *inst, const double *rates, double tol, double *out, int64_t *passes);
 
 /* ---- full solve (controller.py:197-284) ---- */
 int pf_solve(const pf_instance *inst, const pf_config *cfg, const double *warm_start /*nullable P*/,

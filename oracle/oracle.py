@@ -352,6 +352,32 @@ def violation_stats(I: FlatInstance, rates, tol=1e-9):
 # --------------------------------------------------------------------- controller
 
 
+def dao_carry_rates(I: FlatInstance, rates, tol=1e-9) -> np.ndarray:
+    """oracles.py:262-287: a stale allocation applied to drifted conditions
+    (I carries the drifted capacity / demand).  Commodity sums above the new
+    demand scale down by D / S; then the most overloaded edge (first index on
+    ties) scales its paths (each once) by cap / (over + cap), at most 4 E + 4
+    times.  Sums and loads are the exact-order C kernels."""
+    x = np.ascontiguousarray(rates, np.float64).copy()
+    sums = commodity_sums(I, x)
+    for c in np.flatnonzero(sums > I.demand + tol):
+        lo, hi = int(I.com_path_ptr[c]), int(I.com_path_ptr[c + 1])
+        x[lo:hi] *= I.demand[c] / sums[c]
+    if I.num_edges == 0:
+        return x
+    for _ in range(4 * I.num_edges + 4):
+        over = edge_loads(I, x) - I.capacity
+        e = int(np.argmax(over))
+        if over[e] <= tol:
+            break
+        load = over[e] + I.capacity[e]
+        factor = I.capacity[e] / load
+        lo, hi = int(I.edge_pair_ptr[e]), int(I.edge_pair_ptr[e + 1])
+        paths = np.unique(I.pair_path[I.edge_pairs[lo:hi]])
+        x[paths] *= factor
+    return x
+
+
 def make_config(alpha_target=None, gamma=1e-3, beta0=1.0, residual_ratio=10.0, beta_scale=2.0,
                 max_iterations=5000, beta_min=1e-6, beta_max=1e6, adapt=True, trace=False) -> Config:
     """controller.py:29-61 SolverConfig defaults."""

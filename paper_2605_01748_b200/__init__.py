@@ -11,7 +11,7 @@ from .controller import (IterationTrace, Residuals, SolveResult, Solver, SolverC
 from .harness import gravity_demands, gravity_table, k_shortest_paths, random_topology
 from .kernels import (KernelError, SolverState, det_diff_norm, solve_commodity_sums, solve_sum_equation,
                       update_duals, update_rate_suggestions, update_rates, update_slacks, utility)
-from .metrics import default_theta, optimality_from_sums
+from .metrics import dao_carry_rates, dao_evaluate, default_theta, optimality_from_sums
 from .model import (FEAS_TOL, Commodity, CommodityTable, FlatPathSet, InputError, Instance, PathSet, Topology,
                     ViolationReport, build_instance, build_instance_flat, build_instance_raw, build_topology, commodity_sums,
                     edge_loads, edge_loads_from_pairs, validate_allocation, with_conditions)
@@ -26,4 +26,5 @@ __all__ = [
     "initialize_state", "k_shortest_paths", "optimality_from_sums", "project", "random_topology", "score_paths",
     "solve", "solve_commodity_sums", "solve_sum_equation", "update_duals", "update_rate_suggestions",
     "update_rates", "update_slacks", "utility", "validate_allocation", "with_conditions",
+    "dao_carry_rates", "dao_evaluate",
 ]

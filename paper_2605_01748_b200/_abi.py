@@ -70,6 +70,7 @@ SIGNATURES = {
     "pf_solve_sum_equation": (C.c_int, [f64, f64, f64, i64, f64p]),
     "pf_score_paths": (C.c_int, [vp, f64p, i64, f64p]),
     "pf_project": (C.c_int, [vp, f64p, i64, f64p]),
+    "pf_dao_carry_rates": (C.c_int, [vp, f64p, C.c_double, f64p, C.POINTER(C.c_int64)]),
     "pf_solve": (C.c_int, [vp, C.POINTER(Config), f64p, f64p, f64p, C.POINTER(Result), C.POINTER(TraceRow),
                            i64, i64p]),
     "pf_solver_create": (C.c_int, [vp, C.POINTER(Config), C.POINTER(vp)]),

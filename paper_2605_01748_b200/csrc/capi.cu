@@ -745,6 +745,21 @@ int pf_score_paths(const pf_instance *inst, const double *rates, int64_t alpha, 
     });
 }
 
+int pf_dao_carry_rates(const pf_instance *inst, const double *rates, double tol, double *out, int64_t *passes) {
+    return guard([&] {
+        require(inst && rates && out, "null argument");
+        DeviceGuard g(inst->device());
+        const Index &I = *inst->idx;
+        cudaStream_t s = inst->stream;
+        DevBuf<double> x(I.P + 1);
+        h2d(x.p, rates, I.P, s);
+        const int64_t n = dao_carry_device(inst, x.p, tol, s);
+        d2h(out, x.p, I.P, s);
+        PF_CUDA(cudaStreamSynchronize(s));
+        if (passes) *passes = n;
+    });
+}
+
 int pf_project(const pf_instance *inst, const double *rates, int64_t alpha, double *out) {
     return guard([&] {
         require(inst && rates && out, "null argument");

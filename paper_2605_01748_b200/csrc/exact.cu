@@ -674,6 +674,18 @@ void exact_edge_loads_of_rates_em(const InstView &I, const double *rates, const 
     PF_CHECK_LAUNCH();
 }
 
+void exact_edge_loads_of_rates_em_pairs(const InstView &I, const double *rates, double *scratch, double *out,
+                                        cudaStream_t s) {
+    if (!I.E) return;
+    if (!I.NP) {
+        exact_edge_loads_of_rates(I, rates, out, s);
+        return;
+    }
+    k_gather_rates_em_pairs<<<ceil_div(I.NP, 256), 256, 0, s>>>(I, rates, scratch);
+    k_edge_blk_contig<<<ceil_div((int64_t)I.E * 32, 128), 128, 0, s>>>(I, scratch, out);
+    PF_CHECK_LAUNCH();
+}
+
 void exact_update_duals(const InstView &I, const StatePtrs &st, double *sums, double *loads, double *dd, double *dc,
                         double *dcon, double *dn, cudaStream_t s, double *scratch) {
     exact_commodity_sums(I, st.x, sums, s);

@@ -220,6 +220,12 @@ struct Flags {
 void exact_commodity_sums(const InstView &I, const double *x, double *out, cudaStream_t s);
 void exact_edge_loads_from_pairs(const InstView &I, const double *pair_vals, double *out, cudaStream_t s);
 void exact_edge_loads_of_rates(const InstView &I, const double *rates, double *out, cudaStream_t s);
+// Same sums through an edge-major copy gathered via the incidence (scratch: NP doubles).
+void exact_edge_loads_of_rates_em_pairs(const InstView &I, const double *rates, double *scratch, double *out,
+                                        cudaStream_t s);
+// oracles.py:262-287 dao_carry_rates on the device rates x (in place); returns
+// the number of edge passes that scaled (dao.cu).
+int64_t dao_carry_device(const pf_instance *inst, double *x, double tol, cudaStream_t s);
 // Same sums (same association) through an edge-major copy: epath[t] =
 // pair_path[edge_pairs[t]], scratch holds NP doubles.
 void exact_edge_loads_of_rates_em(const InstView &I, const double *rates, const int32_t *epath, double *scratch,

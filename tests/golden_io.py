@@ -53,3 +53,15 @@ def kernel_seed(tag):
     if tag.startswith("small/"):
         return 100 + len(tag.split("/", 1)[1])
     return 5
+
+
+@functools.lru_cache(maxsize=1)
+def dao():
+    """Drift-carry vectors (tests/golden/make_golden_dao.py): {tag: {case: arrays}}."""
+    z = dict(np.load(os.path.join(GOLDEN, "golden_dao.npz")))
+    out = {}
+    for k, v in z.items():
+        _, rest = k.split("/", 1)
+        tag, case, field = rest.rsplit("/", 2)
+        out.setdefault(tag, {}).setdefault(case, {})[field] = v
+    return out

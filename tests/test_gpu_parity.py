@@ -9,6 +9,8 @@ Bars:
     decisions, converged sorted sums within 1e-4 relative, feasible output.
 """
 
+import types
+
 import numpy as np
 import pytest
 
@@ -492,6 +494,45 @@ def test_fast_projection_cluster_variants(ncl):
     assert out["infeasible_before"] and out["max_edge_paths"] > 2048
     assert out["feasible"] and out["deterministic"]
     assert out["sums_rel"] <= 1e-6, out
+
+
+def test_dao_carry_bitwise_vs_reference():
+    """oracles.py:262-297 on the GPU: dao_carry_rates bitwise equal to the
+    reference on every golden drift case (zero drift, 5% link cuts, mixed
+    capacity / demand drift), dao_evaluate equal to the reference's value."""
+    for tag, cases in G.dao().items():
+        base = golden_instance(tag)
+        for case, a in cases.items():
+            drifted = pf.with_conditions(base, capacity=a["capacity"], demand=a["demand"])
+            out = pf.dao_carry_rates(a["rates_in"], drifted)
+            assert np.array_equal(out, a["rates_out"]), (tag, case)
+            if "dao_evaluate" in a:
+                alloc = types.SimpleNamespace(rates=a["rates_in"])
+                ref = types.SimpleNamespace(sums=a["ref_sums"])
+                got = pf.dao_evaluate(alloc, drifted, ref, float(a["theta"][0]))
+                assert got == float(a["dao_evaluate"][0]), (tag, got)
+
+
+def test_dao_carry_generated_matches_oracle():
+    """A 447k-pair generated instance (max 5k pairs per edge) with 5% of the
+    links cut and drifted demands: GPU carry bitwise equal to the oracle's, and
+    the carried allocation feasible."""
+    from b200_helpers import generated
+    from oracle import oracle as O
+    topo, tab, ps = generated(90, 8, 1.5)
+    inst = pf.build_instance(topo, tab, ps, device=0)
+    rates = pf.solve(inst, pf.SolverConfig(max_iterations=100)).rates
+    rng = np.random.default_rng(7)
+    cap = np.asarray(inst.capacity, float).copy()
+    cap[rng.choice(inst.num_edges, round(0.05 * inst.num_edges), replace=False)] = 0.0
+    dem = np.asarray(inst.demand, float) * rng.uniform(0.7, 1.1, inst.num_commodities)
+    drifted = pf.with_conditions(inst, capacity=cap, demand=dem)
+    out = pf.dao_carry_rates(rates, drifted)
+    flat = O.build_instance(topo.capacity, tab.demand, ps.com_path_ptr, ps.path_edge_ptr, ps.path_edges)
+    want = O.dao_carry_rates(flat.with_conditions(capacity=cap, demand=dem), rates)
+    assert np.array_equal(out, want)
+    assert pf.validate_allocation(drifted, out).feasible
+    assert np.array_equal(pf.dao_carry_rates(rates, inst), rates)  # zero drift: bit-identical
 
 
 @pytest.mark.parametrize("scale", [1e300, 1e308])

@@ -203,3 +203,17 @@ def test_projection_of_raw_iterates(kk, alpha):
     pct, _, nv = O.violation_stats(I, out)
     assert nv == 0
     assert np.array_equal(O.project(I, out, alpha), out)
+
+
+def test_dao_carry_oracle_matches_reference():
+    """oracles.py:262-287 restated in oracle/ (exact-order sums): bitwise equal
+    to the reference's dao_carry_rates on every golden drift case."""
+    from b200_helpers import oracle_instance
+    for tag, cases in G.dao().items():
+        base = oracle_instance(tag)
+        for case, a in cases.items():
+            inst = base.with_conditions(capacity=a["capacity"], demand=a["demand"])
+            out = O.dao_carry_rates(inst, a["rates_in"])
+            assert np.array_equal(out, a["rates_out"]), (tag, case)
+            if case == "zero_drift":
+                assert np.array_equal(out, a["rates_in"])
