@@ -1544,17 +1544,44 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         }
         gstart.push_back((int32_t)I.C);
     }
-    // tiles
+    // tiles: up to NW groups and tps pairs each.  Tile t goes to CTA t mod G, so
+    // with n0 greedy tiles the busiest CTA holds ceil(n0 / G) of them; packing
+    // T = ceil(n0 / G) * G tiles instead (group caps spread evenly) gives every
+    // CTA the same count of smaller tiles: its load drops from
+    // ceil(n0 / G) * NP / n0 to NP / G pairs (config 2: 7,835 -> 7,992 tiles)
+    const int64_t ng = (int64_t)gstart.size() - 1;
+    auto tile_end = [&](int64_t gi, int64_t cap) {
+        const int32_t c0 = gstart[gi];
+        int64_t gj = gi;
+        while (gj < ng && gj - gi < cap) {
+            const int64_t npair = pptr[cpp[gstart[gj + 1]]] - pptr[cpp[c0]];
+            if (gj > gi && npair > tps) break;
+            ++gj;
+        }
+        return gj;
+    };
+    int64_t target = 0;
+    {
+        int64_t n0 = 0;
+        for (int64_t gi = 0; gi < ng; gi = tile_end(gi, NW)) ++n0;
+        int sms = 148;
+        PF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, inst->device()));
+        const int64_t ctas = (int64_t)sms * (L->acc_smem ? 2 : 1);  // CTAs per SM of this layout
+        // only with several tiles per CTA (measured: 500-node k=4, 13.2 -> 14 tiles
+        // per CTA, 163.7 -> 161.4 us; config 2 unchanged; 1.6 -> 2 per CTA no gain)
+        if (n0 >= 4 * ctas && !getenv("PF_FAST_NO_BALANCE")) target = (n0 + ctas - 1) / ctas * ctas;
+    }
     std::vector<TileDesc> tiles;
     std::vector<std::array<int32_t, NW + 1>> tgroups;  // group commodity boundaries per tile
     int64_t slot = 0, mb = 0;
     {
-        const int64_t ng = (int64_t)gstart.size() - 1;
         int64_t gi = 0;
         while (gi < ng) {
             const int32_t c0 = gstart[gi];
+            const int64_t left = target - (int64_t)tiles.size();
+            const int64_t cap = target && left > 0 ? std::min<int64_t>(NW, (ng - gi + left - 1) / left) : NW;
             int64_t gj = gi;
-            while (gj < ng && gj - gi < NW) {
+            while (gj < ng && gj - gi < cap) {
                 const int64_t npair = pptr[cpp[gstart[gj + 1]]] - pptr[cpp[c0]];
                 if (gj > gi && npair > tps) break;
                 ++gj;
