@@ -98,6 +98,8 @@ struct pf_solver {
     int64_t bad_commodity = -1;
     bool initialized = false, finished = false;
     DevBuf<double> rates_out, sums_out, trace_proj, trace_sums;
+    DevBuf<double> trace_rows;                  // traced fast runs: a batch of device rows
+    cudaEvent_t tev[64] = {};                   // per-launch timing of a traced batch
     pf_comm *comm = nullptr;
     int64_t global_C = 0;
 
@@ -368,7 +370,64 @@ static int64_t solver_run(pf_solver *S, int64_t max_steps) {
         S->loop_ms += ms;
         return done;
     }
-    // fast mode with trace: one device iteration at a time, stats on the fresh x
+    // fast mode with trace, single GPU, no optimality column: batches of
+    // iterations with their rows computed on the device (controller fields,
+    // objective, % violated, mean relative violation), one host read per batch
+    if (S->ref_sums.empty() && !S->comm) {
+        constexpr int RB = 32, RW = 12;
+        cudaStream_t st = S->stream;
+        if (S->trace_rows.n < (size_t)RB * RW) S->trace_rows.alloc((size_t)RB * RW);
+        if (!S->tev[0])
+            for (cudaEvent_t &e : S->tev) PF_CUDA(cudaEventCreate(&e));
+        const InstView I = S->inst->view();
+        std::vector<double> h((size_t)RB * RW);
+        int64_t last = fast_status(S->fast, st).iteration;
+        bool stop = false;
+        while (done < max_steps && !stop) {
+            const int B = (int)std::min<int64_t>(RB, max_steps - done);
+            for (int i = 0; i < B; ++i) {
+                double *row = S->trace_rows.p + (size_t)i * RW;
+                PF_CUDA(cudaEventRecord(S->tev[2 * i], st));
+                fast_launch_one(S->fast, st);
+                PF_CUDA(cudaEventRecord(S->tev[2 * i + 1], st));
+                fast_ctrl_row(S->fast, row, st);
+                double *xcur = fast_scratch(S->fast, 1);  // free until finish()
+                fast_copy_x(S->fast, xcur, st);
+                trace_stats_dev(I, xcur, fast_root_sums(S->fast), fast_alpha_used_dev(S->fast), S->ts, 1e-9, row + 7,
+                                st);
+            }
+            d2h(h.data(), S->trace_rows.p, (size_t)B * RW, st);
+            PF_CUDA(cudaStreamSynchronize(st));
+            bool progressed = false;
+            for (int i = 0; i < B && !stop; ++i) {
+                const double *r = &h[(size_t)i * RW];
+                const int64_t it = (int64_t)r[0];
+                if (it > last) {  // a stopped controller leaves its iteration unchanged
+                    float ms = 0.f;
+                    PF_CUDA(cudaEventElapsedTime(&ms, S->tev[2 * i], S->tev[2 * i + 1]));
+                    S->loop_ms += ms;
+                    pf_trace_row row;
+                    row.iteration = it;
+                    row.alpha = (int64_t)r[1];
+                    row.beta = r[2];
+                    row.s = r[3];
+                    row.r = r[4];
+                    row.objective = r[7];
+                    row.pct_violated = r[8];
+                    row.mean_relative_violation = r[9];
+                    row.optimality = NAN;
+                    S->trace.push_back(row);
+                    last = it;
+                    ++done;
+                    progressed = true;
+                }
+                if (r[5] != 0.0 || it >= S->cfg.max_iterations) stop = true;
+            }
+            if (!progressed) break;
+        }
+        return done;
+    }
+    // with the optimality column (a projection per row): one iteration at a time
     while (done < max_steps) {
         float ms = 0.f;
         int64_t k = fast_run(S->fast, 1, S->stream, &ms);
@@ -508,6 +567,8 @@ static void solver_destroy(pf_solver *S) {
     if (S->fast) fast_release(S->fast);
     if (S->ev0) cudaEventDestroy(S->ev0);
     if (S->ev1) cudaEventDestroy(S->ev1);
+    for (cudaEvent_t e : S->tev)
+        if (e) cudaEventDestroy(e);
     if (S->stream) cudaStreamDestroy(S->stream);
     delete S;
 }

@@ -562,6 +562,28 @@ __global__ void k_utility(int32_t C, const double *sums, int64_t alpha, double *
         u[c] = (pow(s, 1.0 - (double)alpha) - 1.0) / (1.0 - (double)alpha);
 }
 
+// k_utility with alpha read from the device controller (traced runs)
+__global__ void k_utility_dev(int32_t C, const double *sums, const int64_t *alpha_p, double *u) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    const int64_t alpha = *alpha_p;
+    double s = sums[c] > 1e-12 ? sums[c] : 1e-12;
+    if (alpha == 0)
+        u[c] = s - 1.0;
+    else if (alpha == 1)
+        u[c] = log(s);
+    else
+        u[c] = (pow(s, 1.0 - (double)alpha) - 1.0) / (1.0 - (double)alpha);
+}
+
+// the host's pct_violated / n_violated arithmetic (violation_stats) on the device
+__global__ void k_row_pct(const int32_t *cnt, int64_t total, double *row_pct, double *row_nv) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int64_t nv = (int64_t)cnt[0] + cnt[1] + cnt[2];
+    *row_pct = total ? 100.0 * (double)nv / (double)total : 0.0;
+    *row_nv = (double)nv;
+}
+
 // model.py:346-362: overload / excess, violation flags and relative violations.
 __global__ void k_violations(InstView I, const double *x, const double *loads, const double *sums, double tol,
                              double *overload, double *excess, double *rel_e, double *rel_c, int32_t *cnt) {
@@ -796,6 +818,37 @@ void trace_stats(const InstView &I, const double *x, const double *root_sums, in
     host_out4[1] = rep.pct_violated;
     host_out4[2] = rep.mean_relative_violation;
     host_out4[3] = (double)rep.n_violated;
+}
+
+// trace_stats without a host round trip (traced fast runs): row[0] objective,
+// row[1] pct_violated, row[2] mean_relative_violation, row[3] n_violated, all
+// on the device; alpha from the device controller
+void trace_stats_dev(const InstView &I, const double *x, const double *root_sums, const int64_t *d_alpha,
+                     TraceScratch &ts, double tol, double *row, cudaStream_t s) {
+    ensure_trace_scratch(I, ts);
+    if (I.C) {
+        k_utility_dev<<<ceil_div(I.C, TB), TB, 0, s>>>(I.C, root_sums, d_alpha, ts.tmp.p);
+        k_np_sum<<<1, 1024, 0, s>>>(ts.tmp.p, I.C, row + 0, ts.leaf_lo.p, ts.leaf_sum.p);
+    } else {
+        PF_CUDA(cudaMemsetAsync(row, 0, sizeof(double), s));
+    }
+    if (I.NP && I.E) {
+        k_gather_rates_em_pairs<<<ceil_div(I.NP, 256), 256, 0, s>>>(I, x, ts.em.p);
+        k_edge_blk_contig<<<ceil_div((int64_t)I.E * 32, 128), 128, 0, s>>>(I, ts.em.p, ts.loads.p);
+    } else {
+        exact_edge_loads_of_rates(I, x, ts.loads.p, s);
+    }
+    exact_commodity_sums(I, x, ts.sums.p, s);
+    PF_CUDA(cudaMemsetAsync(ts.cnt.p, 0, sizeof(int32_t) * 4, s));
+    int32_t n = I.E > I.C ? I.E : I.C;
+    n = n > I.P ? n : I.P;
+    if (n)
+        k_violations<<<ceil_div(n, TB), TB, 0, s>>>(I, x, ts.loads.p, ts.sums.p, tol, nullptr, nullptr, ts.rel.p,
+                                                     ts.rel.p + I.E, ts.cnt.p);
+    k_compact_mean<<<1, 1024, 0, s>>>(ts.rel.p, I.E, ts.rel.p + I.E, I.C, ts.tmp.p, row + 2, ts.leaf_lo.p,
+                                      ts.leaf_sum.p);
+    k_row_pct<<<1, 32, 0, s>>>(ts.cnt.p, (int64_t)I.E + I.C + I.P, row + 1, row + 3);
+    PF_CHECK_LAUNCH();
 }
 
 // model.py:335-369 validate_allocation

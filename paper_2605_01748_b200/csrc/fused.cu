@@ -2092,6 +2092,59 @@ void fast_init(FastSolver *F, const double *d_x0, int64_t alpha0, double beta0, 
     PF_CUDA(cudaStreamSynchronize(s));
 }
 
+// Traced runs (capi.cu): one iteration per launch with no host round trip.  The
+// run target is set on the device (one past the current iteration), so a
+// stopped controller just leaves its iteration unchanged.
+__global__ void k_ctrl_next(Ctrl *c) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) c->target = c->iteration + 1;
+}
+
+// row[0..6] = iteration, alpha_used, beta_used, s, r, stopped-or-failed, status
+__global__ void k_ctrl_row(const Ctrl *c, double *row) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    row[0] = (double)c->iteration;
+    row[1] = (double)c->alpha_used;
+    row[2] = c->beta_used;
+    row[3] = c->s;
+    row[4] = c->r;
+    row[5] = (c->stopped || c->status) ? 1.0 : 0.0;
+    row[6] = (double)c->status;
+}
+
+void fast_launch_one(FastSolver *F, cudaStream_t s) {
+    require(!F->comm && !F->nranks, "traced multi-GPU runs are not supported");
+    k_ctrl_next<<<1, 32, 0, s>>>(F->ctrl.p);
+    PF_CHECK_LAUNCH();
+    void *args[] = {(void *)&F->P};
+    PF_CUDA(cudaLaunchCooperativeKernel((const void *)k_fused<false>, dim3(F->G), dim3(NT), args, F->smem, s));
+    PF_CHECK_LAUNCH();
+    ++F->launches;
+}
+
+void fast_ctrl_row(FastSolver *F, double *row7, cudaStream_t s) {
+    k_ctrl_row<<<1, 32, 0, s>>>(F->ctrl.p, row7);
+    PF_CHECK_LAUNCH();
+}
+
+// dst = the current rates x[ctrl.xc], the buffer chosen on the device
+__global__ void k_copy_current_x(const Ctrl *c, const double *x0, const double *x1, int64_t n, double *dst) {
+    const double *x = c->xc ? x1 : x0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = x[i];
+}
+
+void fast_copy_x(FastSolver *F, double *dst, cudaStream_t s) {
+    const int64_t P = F->inst->idx->P;
+    if (!P) return;
+    k_copy_current_x<<<(int)std::min<int64_t>(ceil_div(P, 256), 1184), 256, 0, s>>>(F->ctrl.p, F->x[0].p, F->x[1].p,
+                                                                                    P, dst);
+    PF_CHECK_LAUNCH();
+}
+
+const int64_t *fast_alpha_used_dev(FastSolver *F) {
+    return (const int64_t *)((const char *)F->ctrl.p + offsetof(Ctrl, alpha_used));
+}
+
 int64_t fast_run(FastSolver *F, int64_t max_steps, cudaStream_t s, float *ms) {
     if (F->comm) return fast_run_dist(F, max_steps, s, ms);
     Ctrl c;

@@ -30,6 +30,15 @@ void fast_init(FastSolver *f, const double *d_x0, int64_t alpha0, double beta0, 
 // Runs up to max_steps iterations (fewer if the controller stops); returns the count.
 int64_t fast_run(FastSolver *f, int64_t max_steps, cudaStream_t s, float *ms);
 FastStatus fast_status(FastSolver *f, cudaStream_t s);
+// Traced runs without host round trips: one iteration launched asynchronously
+// (single GPU), the controller's row fields copied to a device row
+// (iteration, alpha_used, beta_used, s, r, stopped-or-failed, status), and the
+// device address of alpha_used.
+void fast_launch_one(FastSolver *f, cudaStream_t s);
+void fast_ctrl_row(FastSolver *f, double *row7, cudaStream_t s);
+const int64_t *fast_alpha_used_dev(FastSolver *f);
+// dst [P] = the current rates (buffer chosen on the device: no host read)
+void fast_copy_x(FastSolver *f, double *dst, cudaStream_t s);
 const double *fast_x(FastSolver *f);
 const double *fast_root_sums(FastSolver *f);
 void fast_export_state(FastSolver *f, double *x, double *y, double *dd, double *dc, double *dcon, double *dn,

@@ -496,6 +496,26 @@ def test_fast_projection_cluster_variants(ncl):
     assert out["sums_rel"] <= 1e-6, out
 
 
+def test_fast_trace_batched_rows_equal_per_row_path():
+    """Traced fast runs without an optimality column compute their rows on the
+    device in batches (no host round trip per iteration); with reference sums
+    every row is computed after its own launch.  Every shared column is
+    bitwise equal between the two, across the alpha / beta changes."""
+    tag = "cfg1_v0.3"
+    inst = golden_instance(tag)
+    batched = pf.solve(inst, pf.SolverConfig(mode="fast", trace=True, max_iterations=900))
+    ref = G.arrays()[f"{tag}/sums"]
+    per_row = pf.solve(inst, pf.SolverConfig(mode="fast", trace=True, max_iterations=900, reference_sums=ref))
+    assert len(batched.trace) == len(per_row.trace) == batched.iterations == per_row.iterations
+    cols = ("iteration", "alpha", "beta", "s", "r", "objective", "pct_violated", "mean_relative_violation")
+    a = np.array([[getattr(t, c) for c in cols] for t in batched.trace])
+    b = np.array([[getattr(t, c) for c in cols] for t in per_row.trace])
+    assert np.array_equal(a, b)
+    assert len({t.alpha for t in batched.trace}) > 1  # the run crosses alpha changes
+    assert all(t.optimality is None for t in batched.trace)
+    assert np.array_equal(batched.rates, per_row.rates)
+
+
 def test_dao_carry_bitwise_vs_reference():
     """oracles.py:262-297 on the GPU: dao_carry_rates bitwise equal to the
     reference on every golden drift case (zero drift, 5% link cuts, mixed
