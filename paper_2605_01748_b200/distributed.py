@@ -126,31 +126,60 @@ class ShardedSolver:
         # transport: "ipc" = the fused kernel exchanges edge totals over NVLink peer
         # memory (CUDA IPC buffers, no host round trip); "nccl" = split kernels
         # around one ncclAllReduce per iteration, run as a CUDA graph
-        self.transport = transport or os.environ.get("PF_DIST_TRANSPORT", "ipc")
+        requested = transport or os.environ.get("PF_DIST_TRANSPORT")
+        self.transport = requested or "ipc"
+        self.comm = None
         if self.transport == "ipc":
-            self.comm = None
-            self._connect_ipc(group)
-        elif self.transport == "nccl":
+            err = self._connect_ipc(group)
+            if err is not None:
+                if requested == "ipc":
+                    raise RuntimeError(f"peer-memory exchange unavailable: {err}")
+                import warnings
+                warnings.warn(f"peer-memory exchange unavailable ({err}); using NCCL", RuntimeWarning)
+                self.solver = Solver(self.instance, self.config)  # no half-connected exchange state
+                self.transport = "nccl"
+        if self.transport == "nccl":
             self.comm = Comm(rank, world, device, group)
             n_kept = int(np.sum((np.asarray(table.demand) > 0) & (np.diff(flat.com_path_ptr) > 0)))
             check(lib().pf_solver_attach_comm(self.solver._h, self.comm.handle, n_kept))
-        else:
+        elif self.transport != "ipc":
             raise ValueError(f"unknown transport {self.transport!r}")
 
     def _connect_ipc(self, group=None):
+        """Exchange CUDA-IPC handles and open every peer's buffer.  Every rank
+        takes part in every collective whatever happens locally, and the ranks
+        agree on the outcome: returns None, or the (first) error on any rank."""
         import torch
         import torch.distributed as dist
+        err = None
         h = C.create_string_buffer(64)
-        check(lib().pf_solver_xchg_create(self.solver._h, self.rank, self.world, h))
+        try:
+            if os.environ.get("PF_DIST_IPC_FAIL") == "1":  # test hook: exercise the fallback
+                raise RuntimeError("PF_DIST_IPC_FAIL=1")
+            check(lib().pf_solver_xchg_create(self.solver._h, self.rank, self.world, h))
+            mine = bytes(h.raw)
+        except Exception as exc:  # noqa: BLE001
+            err, mine = exc, b""
         parts = [None] * self.world
-        dist.all_gather_object(parts, bytes(h.raw), group=group)
-        allh = C.create_string_buffer(b"".join(parts), 64 * self.world)
-        check(lib().pf_solver_xchg_connect(self.solver._h, allh))
+        dist.all_gather_object(parts, mine, group=group)
+        if err is None and all(len(p) == 64 for p in parts):
+            try:
+                allh = C.create_string_buffer(b"".join(parts), 64 * self.world)
+                check(lib().pf_solver_xchg_connect(self.solver._h, allh))
+            except Exception as exc:  # noqa: BLE001
+                err = exc
+        elif err is None:
+            err = RuntimeError("another rank could not create its exchange buffer")
+        bad = torch.tensor([0.0 if err is None else 1.0], dtype=torch.float64)
+        dist.all_reduce(bad, group=group)
+        if bad.item() > 0:
+            return err if err is not None else RuntimeError("another rank could not open the exchange")
         # n_e of kernels.py:94 counts the paths of every shard
         ne = torch.tensor(np.asarray(self.instance.edge_path_count, np.float64))
         dist.all_reduce(ne, group=group)
         ne = np.ascontiguousarray(ne.numpy(), np.float64)
         check(lib().pf_solver_set_edge_counts(self.solver._h, ne.ctypes.data_as(C.POINTER(C.c_double))))
+        return None
 
     def init(self, warm_start=None):
         if warm_start is not None:

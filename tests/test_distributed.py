@@ -261,3 +261,38 @@ def test_ipc_multirank_on_one_gpu(world):
     xg, xs = res[0][4], res[0][5]
     assert xg.shape == xs.shape
     assert float(np.max(np.abs(xg - xs))) <= 1e-6 * float(np.max(np.abs(xs)))
+
+
+@pytest.mark.gpu
+def test_ipc_failure_falls_back_to_nccl(monkeypatch):
+    """When the peer-memory exchange cannot be set up on some rank, all ranks
+    agree and continue over NCCL (default transport); an explicit transport="ipc"
+    request raises instead."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.distributed as dist
+
+    import paper_2605_01748_b200 as pf
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1)
+    try:
+        topo = pf.random_topology(40, seed=40)
+        tab = pf.gravity_table(topo, 0.3 * float(topo.capacity.sum()))
+        flat = pf.k_shortest_paths(topo, tab, 4)
+        cfg = pf.SolverConfig(mode="fast", gamma=1e-12, max_iterations=10 ** 6)
+        monkeypatch.delenv("PF_DIST_TRANSPORT", raising=False)
+        monkeypatch.setenv("PF_DIST_IPC_FAIL", "1")
+        with pytest.warns(RuntimeWarning, match="peer-memory exchange unavailable"):
+            fb = D.ShardedSolver(topo, tab, flat, cfg, 0, 1, 0)
+        assert fb.transport == "nccl"
+        with pytest.raises(RuntimeError, match="peer-memory exchange unavailable"):
+            D.ShardedSolver(topo, tab, flat, cfg, 0, 1, 0, transport="ipc")
+        monkeypatch.delenv("PF_DIST_IPC_FAIL")
+        nc = D.ShardedSolver(topo, tab, flat, cfg, 0, 1, 0, transport="nccl")
+        fb.init()
+        nc.init()
+        fb.run(50)
+        nc.run(50)
+        assert np.array_equal(fb.gather_x(), nc.gather_x())
+    finally:
+        dist.destroy_process_group()
