@@ -62,6 +62,25 @@ def last_error() -> str:
     return buf.value.decode(errors="replace")
 
 
+_INPUT_ERROR = None
+
+
+def _input_error_type():
+    """PF_ERR_INPUT is the reference's InputError (model.py:20); the type is
+    also a NativeError so callers catching either keep working."""
+    global _INPUT_ERROR
+    if _INPUT_ERROR is None:
+        from .topology import InputError
+
+        class NativeInputError(InputError, NativeError):
+            pass
+        _INPUT_ERROR = NativeInputError
+    return _INPUT_ERROR
+
+
 def check(status: int) -> None:
     if status != 0:
-        raise NativeError(f"pf status {status}: {last_error()}")
+        msg = f"pf status {status}: {last_error()}"
+        if status == 1:  # PF_ERR_INPUT
+            raise _input_error_type()(msg)
+        raise NativeError(msg)

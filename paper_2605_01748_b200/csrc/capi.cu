@@ -520,6 +520,17 @@ static void solver_finish(pf_solver *S, double *rates, double *sums) {
     S->finished = true;
 }
 
+// the fused-kernel entry points need a fast solver; name the layout limit when
+// the instance fell back to the exact-order kernels
+static void require_fast(const pf_solver *S, const char *what) {
+    require(S != nullptr, "null solver");
+    if (S->fast) return;
+    std::string why;
+    fast_supported(S->inst, &why);
+    throw Error(PF_ERR_INPUT, std::string(what) + " needs the fused fast-mode kernel" +
+                                  (why.empty() ? std::string(" (PF_MODE_FAST)") : ": this instance has " + why));
+}
+
 static pf_solver *solver_create(const pf_instance *inst, const pf_config *cfg) {
     require(inst && cfg, "null argument");
     validate_config(*cfg);
@@ -540,7 +551,11 @@ static pf_solver *solver_create(const pf_instance *inst, const pf_config *cfg) {
         d2h(S->h_demand.data(), inst->demand.p, I.C, S->stream);
         PF_CUDA(cudaStreamSynchronize(S->stream));
     }
-    if (cfg->mode == PF_MODE_EXACT) {
+    // fast mode on an instance outside the fused kernel's layout limits (more
+    // than 65535 edges, 32 paths or 16384 pairs per commodity): the exact-order
+    // kernels run instead -- the reference's own arithmetic, on the GPU
+    if (cfg->mode == PF_MODE_FAST && !fast_supported(inst, nullptr)) S->cfg.mode = PF_MODE_EXACT;
+    if (S->cfg.mode == PF_MODE_EXACT) {
         S->cur.alloc(I);
         S->nxt.alloc(I);
         S->sums_tmp.alloc(I.C + 1);
@@ -558,19 +573,24 @@ static pf_solver *solver_create(const pf_instance *inst, const pf_config *cfg) {
     } else {
         S->fast = fast_create(inst, *cfg, S->stream);
     }
+    inst->refs.fetch_add(1);  // released by solver_destroy
     return S.release();
 }
 
 static void solver_destroy(pf_solver *S) {
     if (!S) return;
-    DeviceGuard g(S->inst->device());
-    if (S->fast) fast_release(S->fast);
-    if (S->ev0) cudaEventDestroy(S->ev0);
-    if (S->ev1) cudaEventDestroy(S->ev1);
-    for (cudaEvent_t e : S->tev)
-        if (e) cudaEventDestroy(e);
-    if (S->stream) cudaStreamDestroy(S->stream);
-    delete S;
+    const pf_instance *inst = S->inst;
+    {
+        DeviceGuard g(inst->device());
+        if (S->fast) fast_release(S->fast);
+        if (S->ev0) cudaEventDestroy(S->ev0);
+        if (S->ev1) cudaEventDestroy(S->ev1);
+        for (cudaEvent_t e : S->tev)
+            if (e) cudaEventDestroy(e);
+        if (S->stream) cudaStreamDestroy(S->stream);
+        delete S;
+    }
+    instance_release(inst);  // the solver's reference
 }
 
 // ---------------------------------------------------------------- kernel-level helpers
@@ -914,7 +934,7 @@ int pf_solver_time_loop(pf_solver *S, int64_t iterations, float *ms_total, float
     return guard([&] {
         require(S != nullptr, "null solver");
         DeviceGuard g(S->inst->device());
-        require(S->cfg.mode == PF_MODE_FAST, "time_loop requires PF_MODE_FAST");
+        require_fast(S, "time_loop");
         float ms = 0.f;
         int64_t done = fast_run(S->fast, iterations, S->stream, &ms);
         S->loop_ms += ms;
@@ -936,8 +956,7 @@ int pf_solver_kernel_stats(pf_solver *S, int64_t *launches, int64_t *tiles, int6
 
 int pf_solver_attach_comm(pf_solver *S, pf_comm *c, int64_t global_commodities) {
     return guard([&] {
-        require(S != nullptr, "null solver");
-        require(S->cfg.mode == PF_MODE_FAST, "multi-GPU solves run in PF_MODE_FAST");
+        require_fast(S, "a multi-GPU solve");
         S->comm = c;
         S->global_C = global_commodities;
         fast_set_comm(S->fast, comm_ops(c));
@@ -946,8 +965,8 @@ int pf_solver_attach_comm(pf_solver *S, pf_comm *c, int64_t global_commodities) 
 
 int pf_solver_xchg_create(pf_solver *S, int rank, int nranks, void *handle64) {
     return guard([&] {
-        require(S != nullptr && handle64 != nullptr, "null argument");
-        require(S->cfg.mode == PF_MODE_FAST, "multi-GPU solves run in PF_MODE_FAST");
+        require(handle64 != nullptr, "null argument");
+        require_fast(S, "a multi-GPU solve");
         DeviceGuard g(S->inst->device());
         fast_xchg_create(S->fast, rank, nranks, handle64);
     });
@@ -957,6 +976,7 @@ int pf_solver_xchg_connect(pf_solver *S, const void *handles) {
     return guard([&] {
         require(S != nullptr && handles != nullptr, "null argument");
         DeviceGuard g(S->inst->device());
+        require_fast(S, "a multi-GPU solve");
         fast_xchg_connect(S->fast, handles);
     });
 }
@@ -964,7 +984,7 @@ int pf_solver_xchg_connect(pf_solver *S, const void *handles) {
 int pf_solver_set_edge_counts(pf_solver *S, const double *counts) {
     return guard([&] {
         require(S != nullptr && counts != nullptr, "null argument");
-        require(S->cfg.mode == PF_MODE_FAST, "edge counts apply to PF_MODE_FAST");
+        require_fast(S, "edge counts");
         DeviceGuard g(S->inst->device());
         fast_set_edge_counts(S->fast, counts);
     });

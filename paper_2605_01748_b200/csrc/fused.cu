@@ -1457,6 +1457,34 @@ __global__ void k_scaled_copy(const double *a, int64_t n, const Ctrl *ctrl, doub
 
 // Pack commodities into groups (<= GPATH paths, one warp) and groups into tiles
 // (<= NW groups, <= tps pairs), then write each tile's metadata block.
+bool fast_supported(const pf_instance *inst, std::string *why) {
+    std::lock_guard<std::mutex> lk(inst->ws_mu);
+    if (inst->fast_ok < 0) {
+        const Index &I = *inst->idx;
+        std::string w;
+        if (I.E > 65535) {
+            w = "more than 65535 edges (u16 edge ids)";
+        } else if (I.NP >= ((int64_t)1 << 30)) {
+            w = "more than 2^30 demand-path pairs";
+        } else {
+            std::vector<int32_t> cpp(I.C + 1), pptr(I.P + 1);
+            d2h(cpp.data(), I.com_path_ptr.p, I.C + 1, inst->stream);
+            d2h(pptr.data(), I.pair_ptr.p, I.P + 1, inst->stream);
+            PF_CUDA(cudaStreamSynchronize(inst->stream));
+            for (int64_t c = 0; c < I.C && w.empty(); ++c) {
+                if (cpp[c + 1] - cpp[c] > GPATH)
+                    w = "commodity " + std::to_string(c) + " has more than " + std::to_string(GPATH) + " paths";
+                else if (pptr[cpp[c + 1]] - pptr[cpp[c]] > 16384)
+                    w = "commodity " + std::to_string(c) + " has more than 16384 demand-path pairs";
+            }
+        }
+        inst->fast_ok = w.empty() ? 1 : 0;
+        inst->fast_why = w;
+    }
+    if (why) *why = inst->fast_why;
+    return inst->fast_ok == 1;
+}
+
 static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStream_t s) {
     const Index &I = *inst->idx;
     std::vector<int32_t> cpp(I.C + 1), pptr(I.P + 1), pedge(I.NP);

@@ -19,6 +19,10 @@ struct FastStatus {
     int64_t bad;
 };
 
+// The fused kernel's layout limits: u16 edge ids (E <= 65535), one warp lane
+// per path (<= 32 paths per commodity), a commodity within one tile (<= 16384
+// pairs).  Cached on the instance; `why` names the first limit that fails.
+bool fast_supported(const pf_instance *inst, std::string *why);
 FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStream_t s);
 void fast_destroy(FastSolver *f);
 // Return a solver to its instance's pool (kept for the next solve), or destroy it.

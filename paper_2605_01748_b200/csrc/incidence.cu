@@ -246,6 +246,16 @@ static pf_instance *build(int device, int64_t C0, int64_t E, const int64_t *h_cp
 
 using namespace pf;
 
+namespace pf {
+void instance_release(const pf_instance *inst) {
+    if (!inst || inst->refs.fetch_sub(1) != 1) return;
+    pf_instance *p = const_cast<pf_instance *>(inst);
+    DeviceGuard g(p->device());
+    if (p->stream) cudaStreamDestroy(p->stream);
+    delete p;
+}
+}  // namespace pf
+
 extern "C" {
 
 int pf_last_error(char *buf, size_t cap) {
@@ -305,12 +315,7 @@ int pf_instance_with_conditions(const pf_instance *base, const double *capacity,
 }
 
 int pf_instance_destroy(pf_instance *inst) {
-    return guard([&] {
-        if (!inst) return;
-        DeviceGuard g(inst->device());
-        if (inst->stream) cudaStreamDestroy(inst->stream);
-        delete inst;
-    });
+    return guard([&] { pf::instance_release(inst); });
 }
 
 int pf_instance_sizes(const pf_instance *inst, int64_t *C, int64_t *P, int64_t *E, int64_t *NP) {

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <memory>
+#include <atomic>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -159,6 +160,12 @@ struct pf_instance {
     mutable std::mutex ws_mu;
     mutable std::shared_ptr<void> proj_ws;  // projection scratch (projection.cu)
     mutable std::shared_ptr<void> val_ws;   // validate_allocation scratch (capi.cu), under ws_mu
+    // the handle plus every solver created from it: the instance is freed with
+    // the last of them (pf_instance_destroy may come first, e.g. from a garbage
+    // collector finalising a cycle in arbitrary order)
+    mutable std::atomic<int> refs{1};
+    mutable int fast_ok = -1;               // the fused kernel's layout limits hold (-1: not checked)
+    mutable std::string fast_why;
     // one idle fast-mode solver kept for the next solve on this instance (fused.cu):
     // its device buffers are reused instead of re-allocated per solve
     mutable void *fast_pool = nullptr;
@@ -219,6 +226,8 @@ struct Flags {
 
 void exact_commodity_sums(const InstView &I, const double *x, double *out, cudaStream_t s);
 void exact_edge_loads_from_pairs(const InstView &I, const double *pair_vals, double *out, cudaStream_t s);
+// drops one reference of the instance (the handle's or a solver's); frees it with the last
+void instance_release(const pf_instance *inst);
 void exact_edge_loads_of_rates(const InstView &I, const double *rates, double *out, cudaStream_t s);
 // Same sums through an edge-major copy gathered via the incidence (scratch: NP doubles).
 void exact_edge_loads_of_rates_em_pairs(const InstView &I, const double *rates, double *scratch, double *out,

@@ -142,6 +142,9 @@ class ShardedSolver:
             self.comm = Comm(rank, world, device, group)
             n_kept = int(np.sum((np.asarray(table.demand) > 0) & (np.diff(flat.com_path_ptr) > 0)))
             check(lib().pf_solver_attach_comm(self.solver._h, self.comm.handle, n_kept))
+            # the native solver (and the CUDA graph capturing its allreduce) must be
+            # destroyed before the communicator: the solver keeps it alive
+            self.solver._comm_keepalive = self.comm
         elif self.transport != "ipc":
             raise ValueError(f"unknown transport {self.transport!r}")
 

@@ -516,6 +516,23 @@ def test_fast_trace_batched_rows_equal_per_row_path():
     assert np.array_equal(batched.rates, per_row.rates)
 
 
+def test_fast_mode_outside_fused_limits_runs_exact():
+    """More than 32 paths per commodity (one warp lane per path in the fused
+    kernel): a fast-mode solve runs the exact-order kernels instead -- the
+    reference's arithmetic, bitwise -- and the fused-only entry points say why."""
+    topo = pf.random_topology(30, seed=30)
+    tab = pf.gravity_table(topo, 0.3 * float(topo.capacity.sum()))
+    ps = pf.k_shortest_paths(topo, tab, 40)
+    assert int(np.max(np.diff(np.asarray(ps.com_path_ptr)))) > 32
+    inst = pf.build_instance_flat(topo, tab, ps, device=0)
+    fast = pf.solve(inst, pf.SolverConfig(mode="fast", max_iterations=200))
+    exact = pf.solve(inst, pf.SolverConfig(mode="exact", max_iterations=200))
+    assert np.array_equal(fast.rates, exact.rates) and fast.iterations == exact.iterations
+    s = pf.Solver(inst, pf.SolverConfig(mode="fast")).init()
+    with pytest.raises(pf.InputError, match="more than 32 paths"):
+        s.time_loop(5)
+
+
 def test_dao_carry_bitwise_vs_reference():
     """oracles.py:262-297 on the GPU: dao_carry_rates bitwise equal to the
     reference on every golden drift case (zero drift, 5% link cuts, mixed
