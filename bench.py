@@ -71,6 +71,20 @@ def dist_env():
     return rank, world, local
 
 
+def l2_note(device, bytes_per_iter):
+    """say whether the per-GPU working set (the fused pass's
+    compulsory bytes per iteration) fits in L2, with the L2 size queried on the box."""
+    import torch
+    l2 = int(torch.cuda.get_device_properties(device).L2_cache_size)
+    ws = int(bytes_per_iter)
+    if ws > l2:
+        how = "inputs larger than L2 (no flush)"
+    else:
+        how = ("per-GPU working set fits in L2: iterations after the first are L2-resident "
+               "(one persistent launch, no flush between iterations)")
+    return {"l2": how, "l2_bytes": l2, "working_set_bytes_per_gpu": ws}
+
+
 def build_inputs(name):
     """Generate (or load the cached) flat instance with this package's
     generators (pinned to the reference's, tests/test_generators.py)."""
@@ -431,7 +445,7 @@ def run_b200(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "description": CONFIGS[args.config][3], "commodities": C,
                    "paths": P, "pairs": NP, "edges": E, "parallelism": f"dp{world}" if world > 1 else "single",
-                   "l2": "inputs larger than L2 (no flush)", "mode": "fast (fused persistent kernel)"},
+                   **l2_note(local, stats["bytes_per_iter"]), "mode": "fast (fused persistent kernel)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": profile_traffic(args.config), "peak_kind": peak_kind,
                      "bytes_per_iteration_algorithmic": b_iter,

@@ -308,7 +308,7 @@ def bench_main(args, bench):
                                           "over NVLink peer memory (CUDA IPC), counter barrier, rank-order sums"
                                           if sh.transport == "ipc" else
                                           "one ncclAllReduce of 2E+16 fp64 per iteration (CUDA-graph loop)"),
-                           "l2": "inputs larger than L2 (no flush)",
+                           **bench.l2_note(local, st["bytes_per_iter"]),
                            **({"shared_gpus": torch.cuda.device_count()}
                               if os.environ.get("PF_BENCH_SHARE_GPU") == "1" else {})},
                 "roofline": {"bound": "hbm", "achieved": ach, "peak": peak * world, "unit": "GB/s",
