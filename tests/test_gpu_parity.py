@@ -316,6 +316,20 @@ def test_fast_controller_decisions_match_reference():
     np.testing.assert_allclose([t.s for t in res.trace[:3]], want[:3, 3], rtol=1e-9)
 
 
+def test_fast_trace_objective_within_1e4_of_exact():
+    """SURVEY 8(d) fast-mode gate: objective within 1e-4 of the reference's
+    (exact mode, bitwise the reference) on every trace row, over 300
+    iterations with the same alpha / beta decisions."""
+    inst = golden_instance("cfg1_v0.3")
+    fa = pf.solve(inst, pf.SolverConfig(mode="fast", trace=True, max_iterations=300))
+    ex = pf.solve(inst, pf.SolverConfig(mode="exact", trace=True, max_iterations=300))
+    assert len(fa.trace) == len(ex.trace) == 300
+    for a, b in zip(fa.trace, ex.trace):
+        assert (a.iteration, a.alpha, a.beta) == (b.iteration, b.alpha, b.beta)
+        assert abs(a.objective - b.objective) <= 1e-4 * max(1.0, abs(b.objective)), (a.iteration, a.objective,
+                                                                                       b.objective)
+
+
 def test_fast_converged_sums_within_1e4():
     """cfg1, V = 0.3 x capacity: stagnation stop; sorted max-min vector within 1e-4."""
     tag = "cfg1_v0.3"
