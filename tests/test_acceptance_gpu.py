@@ -1,5 +1,5 @@
-"""SPEC acceptance criteria 1, 3, 5, 6, 8 and 9 (reference tests/test_acceptance.py:77-89,
-169-208, 287-328, 368-401) with the GPU solvers swapped in for pathfair.solve: same
+"""SPEC acceptance criteria 1, 3, 4, 5, 6, 8 and 9 (reference tests/test_acceptance.py:77-89,
+169-328, 368-401) with the GPU solvers swapped in for pathfair.solve: same
 instance families, seeds and thresholds.  The single-path max-min reference is
 a progressive-filling oracle restated here (pathfair/oracles.py:56-93:
 raise every unfrozen commodity equally, freeze it at its demand or when its
@@ -174,3 +174,111 @@ def test_criterion_03_projection_feasible_idempotent():
             infeasible += not pf.validate_allocation(inst, out).feasible
             non_idempotent += not np.array_equal(pf.project(inst, out, alpha), out)
     assert checked == 10_000 and infeasible == 0 and non_idempotent == 0, (checked, infeasible, non_idempotent)
+
+
+def _bisect_linear(w, beta, q):
+    """Sign-agnostic bisection for alpha = 0 (tests/test_acceptance.py:211-224)."""
+    lin, c = 1.0 + w, w / beta
+    span = 1.0 + abs(q) + c
+    lo, hi = -span, span
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        if lin * mid - c - q >= 0.0:
+            hi = mid
+        else:
+            lo = mid
+    return 0.5 * (lo + hi)
+
+
+def _bisect_root(w_sum, beta, q, alpha, tol=1e-12):
+    """Pure-bisection root of (1+W)S - (W/beta)S^(-alpha) - Q on (0, inf)
+    (tests/helpers.py:92-112), independent of the Newton path."""
+    lin, c = 1.0 + w_sum, w_sum / beta
+
+    def f(s):
+        return lin * s - c * s ** (-float(alpha)) - q if alpha else lin * s - c - q
+    lo, hi = 1e-300, max(1.0, q / lin)
+    while f(hi) < 0.0:
+        hi *= 2.0
+    for _ in range(20000):
+        mid = 0.5 * (lo + hi)
+        if f(mid) >= 0.0:
+            hi = mid
+        else:
+            lo = mid
+        if hi - lo <= tol * max(1.0, hi):
+            break
+    return 0.5 * (lo + hi)
+
+
+def _rate_block_objective(inst, st, x, alpha):
+    """The x-block objective the rate update minimises (tests/helpers.py:119-131)."""
+    x = np.asarray(x, np.float64)
+    sums = pf.commodity_sums(inst, x)
+    val = -np.sum(pf.utility(sums, alpha)) / st.beta
+    val += 0.5 * np.sum(np.maximum(sums - (np.asarray(inst.demand) - st.dual_demand), 0.0) ** 2)
+    diff = x[np.asarray(inst.pair_path)] - st.y + st.dual_consensus
+    val += 0.5 * np.sum(diff ** 2)
+    val += 0.5 * np.sum(np.maximum(st.dual_nonneg - x, 0.0) ** 2)
+    return float(val)
+
+
+def _random_state(inst, rng, beta, alpha, nonneg_floor=False):
+    import states
+    a = states.random_state(inst.num_commodities, inst.num_paths, inst.num_edges, inst.num_pairs, rng,
+                            nonneg_floor=nonneg_floor)
+    return pf.SolverState(**a, beta=beta, alpha=alpha, iteration=0)
+
+
+def test_criterion_04_kernel_exactness():
+    """Criterion 4 (tests/test_acceptance.py:227-284) on the GPU kernels: 1,000
+    roots (residual and bisection gap <= 1e-8), sum consistency of the rate
+    update (<= 1e-8) and stationarity of the rate block by finite differences
+    (<= 1e-4)."""
+    from b200_helpers import chain, diamond, shared_edge
+    rng = np.random.default_rng(88)
+    worst_f = worst_agree = 0.0
+    for _ in range(1000):
+        w = float(rng.uniform(1e-6, 10.0))
+        beta = float(10 ** rng.uniform(-3, 3))
+        q = float(rng.uniform(-1e3, 1e3))
+        alpha = int(rng.choice([0, 1, 2, 3, 8]))
+        s = pf.solve_sum_equation(w, beta, q, alpha)
+        f = (1 + w) * s - (w / beta) * (s ** (-alpha) if alpha else 1.0) - q
+        worst_f = max(worst_f, abs(f) / max(1.0, abs(q)))
+        ref = _bisect_linear(w, beta, q) if alpha == 0 else _bisect_root(w, beta, q, alpha)
+        worst_agree = max(worst_agree, abs(s - ref) / max(1.0, abs(ref)))
+    assert worst_f <= 1e-8 and worst_agree <= 1e-8, (worst_f, worst_agree)
+
+    worst_sum = 0.0
+    for alpha in (0, 1, 2, 4):
+        for inst in (chain(), diamond(), shared_edge(3)):
+            for _ in range(5):
+                st = _random_state(inst, rng, float(rng.uniform(0.2, 4)), alpha, nonneg_floor=True)
+                sums = pf.solve_commodity_sums(st, inst, alpha)
+                st.x = pf.update_rates(st, inst, sums, alpha)
+                got = pf.commodity_sums(inst, st.x)
+                worst_sum = max(worst_sum, float((np.abs(got - sums) / np.maximum(1.0, np.abs(sums))).max()))
+    assert worst_sum <= 1e-8, worst_sum
+
+    h = 1e-5
+    worst_grad = 0.0
+    insts = (chain(), diamond(), shared_edge(2))
+    for i in range(20):
+        alpha = i % 2
+        inst = insts[i % 3]
+        st = _random_state(inst, rng, float(rng.uniform(0.3, 3)), alpha)
+        dd, dc, dcon, dn = pf.update_duals(st, inst)
+        sd, sc = pf.update_slacks(st, inst)
+        st.dual_demand, st.dual_capacity, st.dual_consensus, st.dual_nonneg = dd, dc, dcon, dn
+        st.slack_demand, st.slack_capacity = sd, sc
+        st.y = pf.update_rate_suggestions(st, inst)
+        sums = pf.solve_commodity_sums(st, inst, alpha)
+        st.x = pf.update_rates(st, inst, sums, alpha)
+        for p in range(inst.num_paths):
+            up, down = st.x.copy(), st.x.copy()
+            up[p] += h
+            down[p] -= h
+            grad = (_rate_block_objective(inst, st, up, alpha) - _rate_block_objective(inst, st, down, alpha)) / (2 * h)
+            worst_grad = max(worst_grad, abs(grad))
+    assert worst_grad <= 1e-4, worst_grad
