@@ -235,7 +235,7 @@ def _ipc_rank_worker(rank, world, port, iters, q):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_ipc_multirank_on_one_gpu(world):
     """Real multi-rank exchange of the peer-memory transport: `world` processes
     on the one B200 (the driver time-slices their cooperative kernels), shards
