@@ -296,3 +296,64 @@ def test_ipc_failure_falls_back_to_nccl(monkeypatch):
         assert np.array_equal(fb.gather_x(), nc.gather_x())
     finally:
         dist.destroy_process_group()
+
+
+def _agree_worker(rank, world, port, fail_rank, fail_at, q):
+    """_connect_ipc with the native calls stubbed: `fail_rank` fails at
+    `fail_at` ("create" / "connect"); every rank must return an error and none
+    may block in a collective."""
+    import types
+
+    import torch.distributed as dist
+
+    from paper_2605_01748_b200 import distributed as DD
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        class FakeLib:
+            def pf_solver_xchg_create(self, h, r, w, buf):
+                if rank == fail_rank and fail_at == "create":
+                    return 1
+                buf.raw = bytes([r + 1]) * 64
+                return 0
+
+            def pf_solver_xchg_connect(self, h, handles):
+                return 1 if rank == fail_rank and fail_at == "connect" else 0
+
+            def pf_solver_set_edge_counts(self, h, p):
+                return 0
+
+            def pf_last_error(self, buf, n):
+                buf.value = b"stubbed failure"
+                return 0
+
+        DD.lib = lambda: FakeLib()
+        import paper_2605_01748_b200._lib as L
+        L.lib = lambda: FakeLib()
+        stub = types.SimpleNamespace(solver=types.SimpleNamespace(_h=None), rank=rank, world=world,
+                                     instance=types.SimpleNamespace(edge_path_count=np.ones(3)))
+        err = DD.ShardedSolver._connect_ipc(stub, None)
+        q.put((rank, None if err is None else str(err)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_at", ["create", "connect", None])
+def test_ipc_setup_failure_on_one_rank_is_agreed(fail_at):
+    """The peer-memory setup protocol (host logic, gloo world size 2 on CPU):
+    a failure on one rank is seen by every rank (so all fall back together)
+    and no rank blocks; without failures every rank connects."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_agree_worker, args=(r, 2, port, 1, fail_at, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in ps)
+    if fail_at is None:
+        assert res == {0: None, 1: None}
+    else:
+        assert res[0] is not None and res[1] is not None, res
