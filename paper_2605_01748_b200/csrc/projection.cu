@@ -133,7 +133,7 @@ __global__ void k_over(int32_t E, const double *loads, const double *cap, double
 // the values are gathered in parallel into shared memory one block at a time,
 // each 32-element chunk is summed sequentially and the chunk partials are added
 // in chunk order by one thread -- the reference's exact association.
-constexpr int RB = 8192;  // gather block (a multiple of the 32-element chunk)
+constexpr int RB = 7936;  // gather block (a multiple of the 32-element chunk; RB + RB / 32 pad slots fit the 8,192-double buffer)
 
 __device__ double cta_edge_resum(const int32_t *epath, const double *x, int32_t lo, int32_t hi, double *buf) {
     __shared__ double s_parts[RB / BLK];
@@ -155,21 +155,38 @@ __device__ double cta_edge_resum(const int32_t *epath, const double *x, int32_t 
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const int32_t j = j0 + u * blockDim.x;
-                if (j < n) buf[j] = v[u];
+                if (j < n) buf[j + (j >> 5)] = v[u];  // one pad slot per chunk: chunk c at 33 c
             }
         }
         __syncthreads();
         const int32_t nch = (n + BLK - 1) / BLK;
         for (int32_t ch = threadIdx.x; ch < nch; ch += blockDim.x) {
             const int32_t cs = ch * BLK, ce = cs + BLK < n ? cs + BLK : n;
+            const double *cb = buf + ch * (BLK + 1);  // the padding keeps a warp's chunks on distinct banks
             double part = 0.0;
-            for (int32_t t = cs; t < ce; ++t) part += buf[t];
+            if (ce - cs == BLK) {  // the loads in flight, the adds in the same order
+                double b[BLK];
+#pragma unroll
+                for (int u = 0; u < BLK; ++u) b[u] = cb[u];
+#pragma unroll
+                for (int u = 0; u < BLK; ++u) part += b[u];
+            } else {
+                for (int32_t t = 0; t < ce - cs; ++t) part += cb[t];
+            }
             s_parts[ch] = part;
         }
         __syncthreads();
         if (threadIdx.x == 0) {
             double total = s_total;
-            for (int32_t ch = 0; ch < nch; ++ch) total += s_parts[ch];
+            int32_t ch = 0;
+            for (; ch + 8 <= nch; ch += 8) {  // 8 partials loaded ahead, added in order
+                double b[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) b[u] = s_parts[ch + u];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) total += b[u];
+            }
+            for (; ch < nch; ++ch) total += s_parts[ch];
             s_total = total;
         }
         __syncthreads();
