@@ -71,26 +71,18 @@ def dist_env():
     return rank, world, local
 
 
-def l2_note(device, bytes_per_iter):
-    """say whether the per-GPU working set (the fused pass's
-    compulsory bytes per iteration) fits in L2, with the L2 size queried on the box."""
-    import torch
-    l2 = int(torch.cuda.get_device_properties(device).L2_cache_size)
-    ws = int(bytes_per_iter)
-    if ws > l2:
-        how = "inputs larger than L2 (no flush)"
-    else:
-        how = ("per-GPU working set fits in L2: iterations after the first are L2-resident "
-               "(one persistent launch, no flush between iterations)")
-    return {"l2": how, "l2_bytes": l2, "working_set_bytes_per_gpu": ws}
+def cache_path(name):
+    return os.path.join(ROOT, "data", f"{name}.npz")
 
 
 def build_inputs(name):
-    """Generate (or load the cached) flat instance with this package's
-    generators (pinned to the reference's, tests/test_generators.py)."""
+    """(topology, commodity table, flat path set) for a config, from this
+    package's generators (pinned to the reference's: tests/test_generators.py,
+    tests/golden/golden_ksp.json); paths cached under data/."""
     import paper_2605_01748_b200 as pf
+    from paper_2605_01748_b200 import gen
     n, k, vol, _ = CONFIGS[name]
-    cache = os.path.join(ROOT, "data", f"{name}.npz")
+    cache = cache_path(name)
     topo = pf.random_topology(n, seed=n)
     tab = pf.gravity_table(topo, vol * float(topo.capacity.sum()))
     if os.path.exists(cache):
@@ -101,13 +93,51 @@ def build_inputs(name):
         flat = pf.k_shortest_paths(topo, tab, k)
         log(f"[bench] k_shortest_paths({name}) {time.perf_counter() - t:.1f}s (native, {os.cpu_count()} threads)")
         try:
-            os.makedirs(os.path.dirname(cache), exist_ok=True)
-            tmp = f"{cache}.{os.getpid()}.tmp.npz"  # atomic: ranks may race on the cache
-            np.savez(tmp, cpp=flat.com_path_ptr, pep=flat.path_edge_ptr, pe=flat.path_edges)
-            os.replace(tmp, cache)
+            gen.write(cache, n, k, vol, topo, tab, flat)
         except OSError:
             pass
     return topo, tab, flat
+
+
+def reference_inputs(name):
+    """The same inputs for the reference arm WITHOUT loading this package's
+    solver: a cached file, else the generator step (paper_2605_01748_b200.gen,
+    host-only libpf_gen.so) run as a separate process."""
+    n, k, vol, _ = CONFIGS[name]
+    cache = cache_path(name)
+    z = np.load(cache) if os.path.exists(cache) else None
+    if z is None or "capacity" not in z:
+        subprocess.run([sys.executable, "-m", "paper_2605_01748_b200.gen", "--nodes", str(n), "--k", str(k),
+                        "--volume", str(vol), "--out", cache], check=True, cwd=ROOT)
+        z = np.load(cache)
+    return z["capacity"], z["demand"], z["cpp"], z["pep"], z["pe"]
+
+
+def algorithmic_bytes(C, P, NP, E):
+    """SURVEY 8(d) B_iter: bytes one iteration must move with y stored (fp64
+    state, int32 indices): 36/pair + 40/path + 32/commodity + 32/edge."""
+    return 36 * NP + 40 * P + 32 * C + 32 * E
+
+
+B200_L2_BYTES = 132644864  # queried on the pool's B200s (cudaDevAttrL2CacheSize)
+
+
+def workload_config(name, C, P, NP, E, world):
+    """The `config` object -- identical in both arms (same workload, same keys)."""
+    try:
+        import torch
+        l2 = int(torch.cuda.get_device_properties(0).L2_cache_size) if torch.cuda.is_available() else B200_L2_BYTES
+    except Exception:  # noqa: BLE001
+        l2 = B200_L2_BYTES
+    ws = algorithmic_bytes(C, P, NP, E) // max(world, 1)
+    if ws > l2:
+        how = "inputs larger than L2 (no flush)"
+    else:
+        how = ("per-GPU working set fits in L2: iterations after the first are L2-resident "
+               "(one persistent launch, no flush between iterations)")
+    return {"workload": name, "description": CONFIGS[name][3], "commodities": int(C), "paths": int(P),
+            "pairs": int(NP), "edges": int(E), "parallelism": f"dp{world}" if world > 1 else "single",
+            "l2": how, "l2_bytes": l2, "working_set_bytes_per_gpu": int(ws)}
 
 
 class ClockSampler:
@@ -222,24 +252,49 @@ def cpu_baseline(flat, tab, topo, budget_s=15.0):
             "sample": f"{n} iterations of the full instance (C oracle, exact reference op order)"}
 
 
-def time_to_quality(name, device=0, cpu=True, chunk=None):
-    """Time to within 1% of the reference algorithm's own fixed point.
+def oracle_fixed_point(name):
+    """The reference algorithm's own fixed point for a ttq instance, computed
+    once by the oracle (tests/golden/make_golden_fixed_points.py, committed):
+    (meta, post-projection commodity sums) or None."""
+    pj = os.path.join(ROOT, "tests", "golden", "golden_fixed_points.json")
+    pz = os.path.join(ROOT, "tests", "golden", "golden_fixed_points.npz")
+    if not (os.path.exists(pj) and os.path.exists(pz)):
+        return None
+    with open(pj) as fh:
+        meta = json.load(fh)
+    if name not in meta:
+        return None
+    return meta[name], np.load(pz)[f"{name}/opt_sums"]
 
-    OPT_ref = post-projection sums of a full solve (stagnation stop, or the
-    reference's 5,000-iteration cap, flagged).  k* = first iteration whose
-    post-projection optimality_from_sums(S_k, OPT_ref, default_theta) >= 0.99.
-    The timed figure is the device time of k* fused iterations (one launch) plus
-    one GPU projection.  The CPU column runs the C oracle (exact reference order)
-    for the same k* iterations plus one projection (measured when cheap, else
+
+def time_to_quality(name, device=0, cpu=True, chunk=None):
+    """Time to within 1% of the reference algorithm's fixed point.
+
+    OPT_ref = the post-projection commodity sums of the reference algorithm's
+    own solve (the exact-order oracle run to its stagnation stop or the
+    5,000-iteration cap; committed fixture), or -- when no fixture exists for the
+    instance -- the fast solver's own end point (flagged).  k* = first iteration
+    whose post-projection optimality_from_sums(S_k, OPT_ref, default_theta) >=
+    0.99 (oracles.py:51-53, 244-254).  The timed figure is the device time of k*
+    fused iterations (one launch) plus one GPU projection.  The reference
+    trajectory's own k* comes with the fixture; the CPU column times the C oracle
+    for that many iterations plus one projection (measured when cheap, else
     extrapolated from a bounded sample and marked so)."""
     import paper_2605_01748_b200 as pf
     topo, tab, flat = build_inputs(name)
     inst = pf.build_instance_flat(topo, tab, flat, device=device)
+    fp = oracle_fixed_point(name)
     s = pf.Solver(inst, pf.SolverConfig(mode="fast", max_iterations=5000)).init()
     s.run(5000)
     r = s.result()
-    _, opt = s.finish()
+    _, own = s.finish()
     theta = pf.default_theta(inst)
+    if fp is not None:
+        meta, opt = fp
+        opt_kind = "reference algorithm's fixed point (exact-order oracle, tests/golden/golden_fixed_points.npz)"
+    else:
+        meta, opt = None, own
+        opt_kind = "fast solver's own end point (no oracle fixture for this instance)"
 
     def quality(k):
         q = pf.Solver(inst, pf.SolverConfig(mode="fast", max_iterations=5000)).init()
@@ -261,33 +316,40 @@ def time_to_quality(name, device=0, cpu=True, chunk=None):
             hi = k
             break
         lo = k
+    reached = hi is not None
     if hi is None:
         hi = n
-    while hi - lo > 1:  # quality is monotone in practice; bisect inside the chunk
+    while reached and hi - lo > 1:  # quality is monotone in practice; bisect inside the chunk
         mid = (lo + hi) // 2
         if quality(mid) >= 0.99:
             hi = mid
         else:
             lo = mid
-    kstar = hi
+    kstar = hi if reached else None
     t = pf.Solver(inst, pf.SolverConfig(mode="fast", max_iterations=5000)).init()
-    ms_loop, _ = t.time_loop(kstar)
+    ms_loop, _ = t.time_loop(hi)
     t.finish()
     ms_proj = t.result().projection_ms
-    out = {"config": name, "k_star": kstar, "opt_ref_iterations": n, "opt_ref_cap_limited": not bool(r.converged),
-           "opt_ref_alpha": int(r.alpha), "gpu_ms": ms_loop + ms_proj, "gpu_loop_ms": ms_loop,
-           "gpu_projection_ms": ms_proj, "pairs": inst.num_pairs, "mode": "fast"}
-    if cpu:
+    out = {"config": name, "k_star": kstar, "opt_ref": opt_kind,
+           "end_optimality_vs_opt_ref": pf.optimality_from_sums(own, opt, theta),
+           "fast_stop": {"iterations": n, "alpha": int(r.alpha), "converged": bool(r.converged)},
+           "gpu_ms": ms_loop + ms_proj, "gpu_loop_ms": ms_loop, "gpu_projection_ms": ms_proj,
+           "pairs": inst.num_pairs, "mode": "fast"}
+    if meta is not None:
+        out["reference"] = {"k_star": meta["k_star"], "iterations": meta["iterations"], "alpha": meta["alpha"],
+                            "converged": meta["converged"]}
+    k_cpu = meta["k_star"] if meta is not None and meta["k_star"] else kstar
+    if cpu and k_cpu:
         from oracle import oracle as O
         I = O.build_instance(topo.capacity, tab.demand, flat.com_path_ptr, flat.path_edge_ptr, flat.path_edges)
         loop = O.Loop(I, O.make_config(max_iterations=5000))
         t0 = time.perf_counter()
         loop.step(1)
         t1 = time.perf_counter() - t0
-        if t1 * kstar < 60.0:
+        if t1 * k_cpu < 60.0:
             t0 = time.perf_counter()
             loop2 = O.Loop(I, O.make_config(max_iterations=5000))
-            loop2.step(kstar)
+            loop2.step(k_cpu)
             st = loop2.state()
             O.project(I, st.x, st.alpha)
             out["cpu_ms"] = 1e3 * (time.perf_counter() - t0)
@@ -299,8 +361,9 @@ def time_to_quality(name, device=0, cpu=True, chunk=None):
             t0 = time.perf_counter()
             O.project(I, st.x, st.alpha)
             pj = time.perf_counter() - t0
-            out["cpu_ms"] = 1e3 * (per * kstar + pj)
+            out["cpu_ms"] = 1e3 * (per * k_cpu + pj)
             out["cpu_kind"] = "extrapolated from 3 iterations + 1 projection"
+        out["cpu_iterations"] = int(k_cpu)
         out["cpu_cores"] = O.num_threads()
     return out
 
@@ -353,13 +416,17 @@ def config45(name, device=0):
 
 
 def run_reference(args):
+    """--impl reference: the reference algorithm's CPU implementation (the
+    exact-order C oracle, all host threads) on the same workload; rank 0 only.
+    This process never loads the B200 solver library: inputs come from the
+    generator step (a separate process) or its cached file."""
     rank, world, local = dist_env()
     if rank != 0:
         return 0
-    import paper_2605_01748_b200  # noqa: F401  (generators only)
     from oracle import oracle as O
-    topo, tab, flat = build_inputs(args.config)
-    I = O.build_instance(topo.capacity, tab.demand, flat.com_path_ptr, flat.path_edge_ptr, flat.path_edges)
+    name = resolve_config(args, world)
+    cap, dem, cpp, pep, pe = reference_inputs(name)
+    I = O.build_instance(cap, dem, cpp, pep, pe)
     loop = O.Loop(I, O.make_config(gamma=1e-12, max_iterations=10 ** 7))
     # each step = one iteration; bound the run to a few minutes
     t0 = time.perf_counter()
@@ -372,19 +439,52 @@ def run_reference(args):
     t = time.perf_counter()
     loop.step(steps)
     dt = time.perf_counter() - t
+    assert loop.state().iteration == 1 + warm + steps
     v = steps / dt
     line = {"metric": METRIC, "value": v, "unit": "iterations/s", "n_gpus": world, "steps": steps,
-            "warmup": warm, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": warm, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "description": CONFIGS[args.config][3],
-                       "commodities": I.num_commodities, "paths": I.num_paths, "pairs": I.num_pairs,
-                       "edges": I.num_edges},
+            "config": workload_config(name, I.num_commodities, I.num_paths, I.num_pairs, I.num_edges, world),
             "impl": "reference",
             "cpu_baseline": {"value": v, "unit": "iterations/s", "cores": O.num_threads(), "kind": "port",
-                             "sample": f"{steps} iterations of the full instance"},
+                             "sample": f"{steps} iterations of the full instance (C oracle, exact reference "
+                                       f"op order, OpenMP)"},
             "e2e": {"value": v, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def resolve_config(args, world):
+    """Default workload: config 2 on one GPU (BASELINE's single-B200 config),
+    config 3 when sharded over N > 1 GPUs (BASELINE's multi-GPU config)."""
+    return args.config or ("cfg2" if world == 1 else "cfg3")
+
+
+def single_gpu_rate(name, device, steps=20, warmup=3):
+    """Fused-loop iterations/s of one workload on one GPU (the N=1 point of a
+    sharded config's scaling curve)."""
+    import torch
+
+    import paper_2605_01748_b200 as pf
+    t0 = time.perf_counter()
+    topo, tab, flat = build_inputs(name)
+    t_gen = time.perf_counter() - t0
+    inst = pf.build_instance_flat(topo, tab, flat, device=device)
+    t_build = time.perf_counter() - t0 - t_gen
+    s = pf.Solver(inst, pf.SolverConfig(mode="fast", gamma=1e-12, max_iterations=10 ** 9)).init()
+    s.time_loop(warmup)
+    it0 = int(s.result().iterations)
+    ms, _ = s.time_loop(steps)
+    torch.cuda.synchronize()
+    assert int(s.result().iterations) - it0 == steps, "the controller stopped inside the timed region"
+    C, P, E, NP = inst.num_commodities, inst.num_paths, inst.num_edges, inst.num_pairs
+    b = algorithmic_bytes(C, P, NP, E)
+    peak, _ = measured_peaks()
+    out = {"workload": name, "n_gpus": 1, "value": steps / (ms / 1e3), "unit": "iterations/s",
+           "ms_per_step": ms / steps, "steps": steps, "pairs": NP, "edges": E,
+           "roofline_frac": b * steps / (ms / 1e3) / 1e9 / peak, "inputs_s": t_gen, "instance_build_s": t_build}
+    del s, inst
+    return out
 
 
 def run_b200(args):
@@ -392,6 +492,7 @@ def run_b200(args):
 
     import paper_2605_01748_b200 as pf
     rank, world, local = dist_env()
+    args.config = resolve_config(args, world)
     if world > 1:
         from paper_2605_01748_b200 import distributed as D
         return D.bench_main(args, sys.modules[__name__])
@@ -404,16 +505,20 @@ def run_b200(args):
     # warm-up (W iterations, untimed)
     solver.time_loop(max(args.warmup, 3))
     torch.cuda.synchronize()
+    it0 = int(solver.result().iterations)
     clocks = ClockSampler(local).start()
     t_wall = time.perf_counter()
     ms, ms_it = solver.time_loop(args.steps)  # CUDA events around exactly K iterations (one launch)
     torch.cuda.synchronize()
     t_wall = time.perf_counter() - t_wall
     clk = clocks.stop()
+    done = int(solver.result().iterations) - it0
+    if done != args.steps:
+        raise RuntimeError(f"timed region ran {done} iterations, expected {args.steps}")
     value = args.steps / (ms / 1e3)
 
     # roofline: algorithmic bytes per launch / launch duration
-    b_iter = 36 * NP + 40 * P + 32 * C + 32 * E
+    b_iter = algorithmic_bytes(C, P, NP, E)
     peak, peak_kind = measured_peaks()
     achieved = b_iter * args.steps / (ms / 1e3) / 1e9
     stats = solver.kernel_stats()
@@ -428,8 +533,11 @@ def run_b200(args):
     t = time.perf_counter()
     res = pf.solve(inst, e2e_cfg, warm_start=warm)
     e2e_s = time.perf_counter() - t
+    if res.iterations != args.steps:
+        raise RuntimeError(f"e2e solve ran {res.iterations} iterations, expected {args.steps}")
     e2e = {"value": args.steps / e2e_s, "unit": "iterations/s", "h2d_bytes_per_step": 8 * P / args.steps,
            "d2h_bytes_per_step": 8 * (P + C) / args.steps, "projection_ms": res.projection_ms,
+           "loop_ms": res.loop_ms, "wall_ms": 1e3 * e2e_s,
            "call": "pf_solve (pinned host warm start -> K iterations -> GPU projection -> host rates/sums)"}
 
     cpu = cpu_baseline(flat, tab, topo) if (rank == 0 and not args.no_cpu_baseline) else None
@@ -439,13 +547,15 @@ def run_b200(args):
     cfg4 = cfg5 = None
     if rank == 0 and not args.no_extras:
         cfg4, cfg5 = config45(args.extras_config, device=local)
+    del solver
+    sharded_n1 = None
+    if rank == 0 and args.sharded_config and args.sharded_config != args.config:
+        sharded_n1 = single_gpu_rate(args.sharded_config, local)
     line = {
         "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "description": CONFIGS[args.config][3], "commodities": C,
-                   "paths": P, "pairs": NP, "edges": E, "parallelism": f"dp{world}" if world > 1 else "single",
-                   **l2_note(local, stats["bytes_per_iter"]), "mode": "fast (fused persistent kernel)"},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args.config, C, P, NP, E, world),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": profile_traffic(args.config), "peak_kind": peak_kind,
                      "bytes_per_iteration_algorithmic": b_iter,
@@ -455,29 +565,53 @@ def run_b200(args):
         "time_to_1pct": ttq,
         "config4_link_failure_resolve": cfg4,
         "config5_alpha_sweep": cfg5,
+        "sharded_config_n1": sharded_n1,
         "clocks": clk,
         "gpu_launches": 1,
         "wall_s_timed_region": t_wall,
-        "kernel": {"grid": stats["grid"], "tiles": stats["tiles"], "launches_total": stats["launches"]},
+        "kernel": {"name": "pf::k_fused (cooperative persistent kernel)", "grid": stats["grid"],
+                   "tiles": stats["tiles"], "launches_total": stats["launches"]},
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
 
 
+def spawn_ranks(argv, n):
+    """`bench.py --gpus N` outside torchrun: launch N ranks (one per GPU) the
+    way the driver does and return their exit status."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *argv]
+    return subprocess.run(cmd).returncode
+
+
 def main(argv=None):
+    argv = list(sys.argv[1:] if argv is None else argv)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="workload (default: cfg2 on one GPU, cfg3 sharded over N > 1)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ttq", action="store_true", help="skip the time-to-within-1%% measurement")
     ap.add_argument("--ttq", default="cfg1_v0.3,cfg2_v0.3,target_k4_v0.3", help="configs for time-to-within-1%%")
     ap.add_argument("--no-extras", action="store_true", help="skip the config 4 / config 5 measurements")
     ap.add_argument("--extras-config", default="cfg2_v0.3", help="instance for the config 4 / 5 measurements")
+    ap.add_argument("--sharded-config", default="cfg3",
+                    help="at N=1 also time this workload on one GPU (the N=1 point of the sharded curve; '' skips)")
     args = ap.parse_args(argv)
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if args.gpus > 1 and world == 0:
+        return spawn_ranks(argv, args.gpus)
+    if world and world != args.gpus and os.environ.get("PF_BENCH_SHARE_GPU") != "1":
+        log(f"[bench] --gpus {args.gpus} but WORLD_SIZE={world}")
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     return run_b200(args)

@@ -29,7 +29,9 @@
  *   pf_solve                    controller.py:197-284 solve
  *   pf_solver_*                 controller.py:197-284, split so the device loop can
  *                               be timed / sharded (no reference equivalent)
- *   pf_ksp_*                    harness.py:138-176 k_shortest_paths (host, OpenMP)
+ *
+ * Input generation (k shortest paths, path validation) is host-only code in a
+ * separate library, libpf_gen.so (include/pf_gen.h).
  */
 #ifndef PF_B200_H
 #define PF_B200_H
@@ -122,6 +124,10 @@ typedef struct {
     double runtime_s;      /* init .. projection, wall clock (controller.py:204,281) */
     double loop_ms;        /* device time of the iteration loop (CUDA events) */
     double projection_ms;  /* device time of the projection */
+    int32_t exact_fallback; /* 1: mode FAST was requested outside the fused layout limits (more than 32
+                               paths or 16,384 pairs per commodity, or 65,535 edges) and the exact-order
+                               kernels ran instead */
+    int32_t reserved;
 } pf_result;
 
 typedef struct {
@@ -191,6 +197,9 @@ int pf_solver_get_state(pf_solver *s, double *x, double *y, double *dd, double *
                         double *beta, int64_t *alpha, int64_t *iteration);
 int pf_solver_time_loop(pf_solver *s, int64_t iterations, float *ms_total, float *ms_kernel_per_iter);
 int pf_solver_kernel_stats(pf_solver *s, int64_t *launches, int64_t *tiles, int64_t *grid, int64_t *bytes_per_iter);
+/* The IterationTrace rows recorded so far (controller.py:173-194): copies min(cap, total) rows,
+ * *total = the number recorded (lets a caller size its buffer by the actual run, not max_iterations). */
+int pf_solver_trace(pf_solver *s, pf_trace_row *rows /*nullable when cap == 0*/, int64_t cap, int64_t *total);
 int pf_solver_destroy(pf_solver *s);
 
 /* ---- multi-GPU: one process per GPU, NCCL over NVLink (dlopen'ed libnccl) ---- */
@@ -207,19 +216,6 @@ int pf_solver_attach_comm(pf_solver *s, pf_comm *c, int64_t global_commodities);
 int pf_solver_xchg_create(pf_solver *s, int rank, int nranks, void *handle64);
 int pf_solver_xchg_connect(pf_solver *s, const void *handles);
 int pf_solver_set_edge_counts(pf_solver *s, const double *counts);
-
-/* ---- host input preparation: k shortest paths (harness.py:138-176) ---- */
-void *pf_ksp_run(int32_t n_nodes, int64_t n_edges, const int64_t *edge_src, const int64_t *edge_dst,
-                 const double *weight, const double *capacity, int64_t n_coms, const int64_t *com_src,
-                 const int64_t *com_dst, int32_t k, int32_t n_threads);
-void pf_ksp_sizes(void *h, int64_t *n_paths, int64_t *n_pairs);
-void pf_ksp_export(void *h, int64_t *com_path_ptr, int64_t *path_edge_ptr, int64_t *path_edges);
-void pf_ksp_free(void *h);
-/* model.py:183-203 _check_path over every path (host, OpenMP): first bad path
- * in commodity-major order, or -1 (build_instance's validation) */
-int64_t pf_validate_paths(int64_t n_commodities, const int64_t *com_path_ptr, const int64_t *path_edge_ptr,
-                          const int64_t *path_edges, int64_t n_edges, const int64_t *edge_src,
-                          const int64_t *edge_dst, const int64_t *com_src, const int64_t *com_dst);
 
 #ifdef __cplusplus
 }

@@ -39,7 +39,7 @@ class TraceRow(C.Structure):
 class Result(C.Structure):
     _fields_ = [("iterations", i64), ("alpha", i64), ("converged", i32), ("status", i32),
                 ("bad_commodity", i64), ("beta", f64), ("runtime_s", f64), ("loop_ms", f64),
-                ("projection_ms", f64)]
+                ("projection_ms", f64), ("exact_fallback", i32), ("reserved", i32)]
 
 
 class Violation(C.Structure):
@@ -82,6 +82,7 @@ SIGNATURES = {
     "pf_solver_get_state": (C.c_int, [vp, f64p, f64p, f64p, f64p, f64p, f64p, f64p, i64p, i64p]),
     "pf_solver_time_loop": (C.c_int, [vp, i64, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "pf_solver_kernel_stats": (C.c_int, [vp, i64p, i64p, i64p, i64p]),
+    "pf_solver_trace": (C.c_int, [vp, vp, i64, i64p]),
     "pf_solver_destroy": (C.c_int, [vp]),
     "pf_comm_unique_id": (C.c_int, [vp]),
     "pf_comm_create": (C.c_int, [C.c_int, C.c_int, vp, C.c_int, C.POINTER(vp)]),

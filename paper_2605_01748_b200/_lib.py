@@ -43,7 +43,27 @@ _i64p = C.POINTER(C.c_int64)
 _f64p = C.POINTER(C.c_double)
 
 
-def _declare(L):
+_gen = None
+
+
+def gen_lib():
+    """libpf_gen.so (include/pf_gen.h): host-only input generation."""
+    global _gen
+    if _gen is None:
+        with _lock:
+            if _gen is None:
+                if not os.path.exists(_build.GEN_LIB):
+                    try:
+                        _build.build_gen()
+                    except Exception as exc:  # noqa: BLE001
+                        raise NativeError(f"{_build.GEN_LIB} is missing and could not be built: {exc}") from exc
+                L = C.CDLL(_build.GEN_LIB)
+                _declare_gen(L)
+                _gen = L
+    return _gen
+
+
+def _declare_gen(L):
     L.pf_ksp_run.restype = C.c_void_p
     L.pf_ksp_run.argtypes = [C.c_int32, C.c_int64, _i64p, _i64p, _f64p, _f64p, C.c_int64, _i64p, _i64p,
                              C.c_int32, C.c_int32]
@@ -52,6 +72,9 @@ def _declare(L):
     L.pf_ksp_free.argtypes = [C.c_void_p]
     L.pf_validate_paths.restype = C.c_int64
     L.pf_validate_paths.argtypes = [C.c_int64, _i64p, _i64p, _i64p, C.c_int64, _i64p, _i64p, _i64p, _i64p]
+
+
+def _declare(L):
     from . import _abi
     _abi.declare(L)
 

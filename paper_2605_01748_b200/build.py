@@ -24,6 +24,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_build")
 LIB = os.path.join(OUT_DIR, "libpf_b200.so")
+GEN_LIB = os.path.join(OUT_DIR, "libpf_gen.so")  # host-only input generation (include/pf_gen.h)
+GEN_SOURCES = ("ksp.cpp",)
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC,-fopenmp",
@@ -38,7 +40,28 @@ def _nvcc() -> str:
 
 
 def sources():
-    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cpp")))
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)
+                  if f.endswith((".cu", ".cpp")) and f not in GEN_SOURCES)
+
+
+def build_gen(force: bool = False, verbose: bool = False) -> str:
+    """libpf_gen.so: the CPU-only input generators (k shortest paths, path
+    validation), g++ with OpenMP -- no CUDA, so input preparation never maps
+    the solver library."""
+    os.makedirs(OUT_DIR, exist_ok=True)
+    srcs = [os.path.join(CSRC, f) for f in GEN_SOURCES]
+    hdr = os.path.join(ROOT, "include", "pf_gen.h")
+    if force or _stale(GEN_LIB, srcs + [hdr, __file__]):
+        cxx = shutil.which("g++") or "g++"
+        cmd = [cxx, "-O3", "-std=c++17", "-fPIC", "-shared", "-fopenmp", "-I", os.path.join(ROOT, "include"),
+               *srcs, "-o", GEN_LIB]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        env = dict(os.environ)
+        env.pop("CC", None)
+        env.pop("CXX", None)
+        subprocess.run(cmd, check=True, env=env)
+    return GEN_LIB
 
 
 def headers():
@@ -91,6 +114,8 @@ def main(argv=None):
     ap.add_argument("--variant", default=None, help="tuning variant name (output _build/<variant>/)")
     ap.add_argument("-D", dest="defines", action="append", default=[], help="preprocessor define for a variant")
     a = ap.parse_args(argv)
+    if not a.variant:
+        print(build_gen(force=a.force, verbose=a.verbose))
     print(build(force=a.force, verbose=a.verbose, variant=a.variant, defines=a.defines))
 
 

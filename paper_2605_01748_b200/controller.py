@@ -16,6 +16,8 @@ Both return the GPU-projected, feasible allocation (projection.py:51-107).
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
+import warnings
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -64,9 +66,9 @@ class SolverConfig:
         if self.mode not in _MODES:
             raise InputError(f"mode must be one of {sorted(_MODES)}")
 
-    def to_c(self, project=True, keep=None) -> A.Config:
+    def to_c(self, project=True, keep=None, with_reference=True) -> A.Config:
         ref = None
-        if self.reference_sums is not None:
+        if self.reference_sums is not None and self.trace and with_reference:
             rs = np.ascontiguousarray(self.reference_sums, np.float64)
             if keep is not None:
                 keep.append(rs)
@@ -107,6 +109,7 @@ class SolveResult:
     trace: tuple | None
     loop_ms: float = field(default=0.0, compare=False)
     projection_ms: float = field(default=0.0, compare=False)
+    mode: str = field(default="fast", compare=False)  # the arithmetic that ran: "fast" | "exact"
 
 
 def _p(a):
@@ -147,29 +150,57 @@ def _trace_rows(buf, n):
     return tuple(rows)
 
 
+def _fallback_warning(res):
+    if res.exact_fallback:
+        warnings.warn("mode='fast' requested outside the fused kernel's layout limits (more than 32 paths or "
+                      "16,384 pairs per commodity, or 65,535 edges): the exact-order kernels ran instead "
+                      "(SolveResult.mode == 'exact')", RuntimeWarning, stacklevel=3)
+
+
+def _result(res, rates, sums, trace, config):
+    return SolveResult(rates=rates, sums=sums, iterations=int(res.iterations), alpha=int(res.alpha),
+                       converged=bool(res.converged), runtime_s=float(res.runtime_s), trace=trace,
+                       loop_ms=float(res.loop_ms), projection_ms=float(res.projection_ms),
+                       mode="exact" if (config.mode == "exact" or res.exact_fallback) else "fast")
+
+
 def solve(instance: Instance, config: SolverConfig | None = None, warm_start=None) -> SolveResult:
     """controller.py:197-284: run the loop on the GPU and return a projected, feasible result."""
     config = config if config is not None else SolverConfig()
     warm = _check_warm(instance, warm_start)
+    if config.trace:
+        return _solve_traced(instance, config, warm)
     keep = []
-    cfg = config.to_c(keep=keep)
-    if config.reference_sums is not None and np.asarray(config.reference_sums).shape != (instance.num_commodities,):
-        if warm is not None and not np.all(np.isfinite(warm)):  # the reference checks the warm start first
-            raise InputError("warm start contains non-finite rates")
-        raise InputError("commodity sets differ between allocation and reference")
+    cfg = config.to_c(keep=keep, with_reference=False)  # reference_sums only feed the trace
     rates = np.empty(instance.num_paths)
     sums = np.empty(instance.num_commodities)
     res = A.Result()
-    cap = config.max_iterations if config.trace else 0
-    tbuf = (A.TraceRow * max(cap, 1))()
     tlen = C.c_int64(0)
     rc = lib().pf_solve(instance.handle, C.byref(cfg), _p(warm) if warm is not None else None, _p(rates),
-                        _p(sums), C.byref(res), tbuf, cap, C.byref(tlen))
+                        _p(sums), C.byref(res), None, 0, C.byref(tlen))
     _raise(instance, rc, res.bad_commodity, res.iterations)
-    return SolveResult(rates=rates, sums=sums, iterations=int(res.iterations), alpha=int(res.alpha),
-                       converged=bool(res.converged), runtime_s=float(res.runtime_s),
-                       trace=_trace_rows(tbuf, tlen.value) if config.trace else None,
-                       loop_ms=float(res.loop_ms), projection_ms=float(res.projection_ms))
+    _fallback_warning(res)
+    return _result(res, rates, sums, None, config)
+
+
+def _solve_traced(instance, config, warm):
+    """solve() with trace=True through the device-resident solver, so the rows
+    are copied out by the run's actual length (the reference's trace list grows
+    lazily; a buffer of max_iterations rows would not)."""
+    ref_ok = (config.reference_sums is None
+              or np.asarray(config.reference_sums).shape == (instance.num_commodities,))
+    s = Solver(instance, config if ref_ok else dataclasses.replace(config, reference_sums=None))
+    s.init(warm)
+    if not ref_ok and instance.num_paths:
+        # the reference fails in its first trace row (optimality_from_sums,
+        # controller.py:183), i.e. after iteration 1's kernels: a KernelError there wins
+        s.run(1)
+        raise InputError("commodity sets differ between allocation and reference")
+    s.run(config.max_iterations)
+    rates, sums = s.finish()
+    res = s.result()
+    _fallback_warning(res)
+    return _result(res, rates, sums, s.trace(), config)
 
 
 class Solver:
@@ -179,6 +210,9 @@ class Solver:
     def __init__(self, instance: Instance, config: SolverConfig | None = None):
         self.instance = instance
         self.config = config if config is not None else SolverConfig()
+        rs = self.config.reference_sums
+        if self.config.trace and rs is not None and np.asarray(rs).shape != (instance.num_commodities,):
+            raise InputError("commodity sets differ between allocation and reference")
         self._keep = []
         self._cfg = self.config.to_c(keep=self._keep)
         h = C.c_void_p()
@@ -241,6 +275,14 @@ class Solver:
         tot, per = C.c_float(), C.c_float()
         check(lib().pf_solver_time_loop(self._h, int(iterations), C.byref(tot), C.byref(per)))
         return float(tot.value), float(per.value)
+
+    def trace(self) -> tuple:
+        """The IterationTrace rows recorded so far (pf_solver_trace)."""
+        total = C.c_int64(0)
+        check(lib().pf_solver_trace(self._h, None, 0, C.byref(total)))
+        buf = (A.TraceRow * max(total.value, 1))()
+        check(lib().pf_solver_trace(self._h, buf, total.value, C.byref(total)))
+        return _trace_rows(buf, total.value)
 
     def kernel_stats(self):
         vals = [C.c_int64() for _ in range(4)]

@@ -97,6 +97,7 @@ struct pf_solver {
     int status = PF_OK;
     int64_t bad_commodity = -1;
     bool initialized = false, finished = false;
+    bool exact_fallback = false;                // fast mode requested outside the fused layout limits
     DevBuf<double> rates_out, sums_out, trace_proj, trace_sums;
     DevBuf<double> trace_rows;                  // traced fast runs: a batch of device rows
     cudaEvent_t tev[64] = {};                   // per-launch timing of a traced batch
@@ -463,6 +464,7 @@ static void solver_status(pf_solver *S, pf_result *res) {
     res->status = res->status ? res->status : S->status;
     if (S->bad_commodity >= 0) res->bad_commodity = S->bad_commodity;
     res->runtime_s = wall() - S->t0;
+    res->exact_fallback = S->exact_fallback ? 1 : 0;
     res->loop_ms = S->loop_ms;
     res->projection_ms = S->proj_ms;
 }
@@ -554,7 +556,10 @@ static pf_solver *solver_create(const pf_instance *inst, const pf_config *cfg) {
     // fast mode on an instance outside the fused kernel's layout limits (more
     // than 65535 edges, 32 paths or 16384 pairs per commodity): the exact-order
     // kernels run instead -- the reference's own arithmetic, on the GPU
-    if (cfg->mode == PF_MODE_FAST && !fast_supported(inst, nullptr)) S->cfg.mode = PF_MODE_EXACT;
+    if (cfg->mode == PF_MODE_FAST && !fast_supported(inst, nullptr)) {
+        S->cfg.mode = PF_MODE_EXACT;
+        S->exact_fallback = true;
+    }
     if (S->cfg.mode == PF_MODE_EXACT) {
         S->cur.alloc(I);
         S->nxt.alloc(I);
@@ -987,6 +992,15 @@ int pf_solver_set_edge_counts(pf_solver *S, const double *counts) {
         require_fast(S, "edge counts");
         DeviceGuard g(S->inst->device());
         fast_set_edge_counts(S->fast, counts);
+    });
+}
+
+int pf_solver_trace(pf_solver *S, pf_trace_row *rows, int64_t cap, int64_t *total) {
+    return guard([&] {
+        require(S != nullptr && total != nullptr && (rows != nullptr || cap == 0), "null argument");
+        const int64_t n = (int64_t)S->trace.size();
+        *total = n;
+        if (cap > 0) std::memcpy(rows, S->trace.data(), sizeof(pf_trace_row) * (size_t)(n < cap ? n : cap));
     });
 }
 

@@ -12,6 +12,8 @@
 // reference's `float(sum(weights[e] for e in eids))` computes.  Host code: this
 // is input preparation (a config-3 prerequisite), not the GPU
 // hot path.  Commodities are processed in parallel with OpenMP.
+#include "pf_gen.h"
+
 #include <algorithm>
 #include <cmath>
 #include <cstdint>

@@ -239,7 +239,8 @@ def consistency_check(sh, topo, tab, flat, world, rank):
 
 
 def bench_main(args, bench):
-    """bench.py --gpus N under torchrun: config 2 sharded over N GPUs (strong scaling)."""
+    """bench.py --gpus N under torchrun: one instance (config 3 by default)
+    sharded over N GPUs (fixed total work: strong scaling)."""
     import json
 
     import torch
@@ -248,6 +249,9 @@ def bench_main(args, bench):
     rank, world, local = bench.dist_env()
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
+    if rank == 0:  # one generator run; the other ranks read its cache
+        bench.build_inputs(args.config)
+    dist.barrier()
     topo, tab, flat = bench.build_inputs(args.config)
     cfg = SolverConfig(mode="fast", gamma=1e-12, max_iterations=10 ** 9)
     sh = ShardedSolver(topo, tab, flat, cfg, rank, world, local)
@@ -295,22 +299,22 @@ def bench_main(args, bench):
     if rank == 0:
         C_, P_, E_ = len(tab), int(flat.com_path_ptr[-1]), topo.num_edges
         NPt = int(tn.item())
-        b_iter = 36 * NPt + 40 * P_ + 32 * C_ + 32 * E_
+        b_iter = bench.algorithmic_bytes(C_, P_, NPt, E_)
         peak, kind = bench.measured_peaks()
         ach = b_iter * args.steps / (ms_max / 1e3) / 1e9
         line = {"metric": bench.METRIC, "value": args.steps / (ms_max / 1e3), "unit": "iterations/s",
                 "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
                 "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": args.config, "pairs": NPt, "parallelism": f"dp{world} (commodity shards)",
-                           "transport": sh.transport,
-                           "collective": ("per-iteration exchange of 2E+16 fp64 rank totals inside the fused kernel "
-                                          "over NVLink peer memory (CUDA IPC), counter barrier, rank-order sums"
-                                          if sh.transport == "ipc" else
-                                          "one ncclAllReduce of 2E+16 fp64 per iteration (CUDA-graph loop)"),
-                           **bench.l2_note(local, st["bytes_per_iter"]),
-                           **({"shared_gpus": torch.cuda.device_count()}
-                              if os.environ.get("PF_BENCH_SHARE_GPU") == "1" else {})},
+                "config": bench.workload_config(args.config, C_, P_, NPt, E_, world),
+                "transport": {"kind": sh.transport,
+                              "collective": ("per-iteration exchange of 2E+16 fp64 rank totals inside the fused "
+                                             "kernel over NVLink peer memory (CUDA IPC), counter barrier, "
+                                             "rank-order sums" if sh.transport == "ipc" else
+                                             "one ncclAllReduce of 2E+16 fp64 per iteration (CUDA-graph loop)"),
+                              "sharding": "contiguous commodity ranges, equal pair counts",
+                              **({"shared_gpus": torch.cuda.device_count()}
+                                 if os.environ.get("PF_BENCH_SHARE_GPU") == "1" else {})},
                 "roofline": {"bound": "hbm", "achieved": ach, "peak": peak * world, "unit": "GB/s",
                              "frac": ach / (peak * world), "traffic": None, "peak_kind": kind},
                 "clocks": clk, "gpu_launches": int(st["launches"]), "max_over_ranks_ms": ms_max,

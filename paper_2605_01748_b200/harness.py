@@ -95,14 +95,15 @@ def gravity_demands(topology, total_volume):
 
 def k_shortest_paths(topology, commodities, k=4, threads=None) -> FlatPathSet:
     """Up to k loopless shortest paths per commodity ordered by (weight, edge tuple);
-    unreachable pairs get zero paths (harness.py:138-176).  Native (csrc/ksp.cpp)."""
+    unreachable pairs get zero paths (harness.py:138-176).  Native host code
+    (csrc/ksp.cpp in libpf_gen.so, include/pf_gen.h)."""
     if k < 1:
         raise InputError("k must be >= 1")
-    from ._lib import lib
+    from ._lib import gen_lib
 
     if not isinstance(commodities, CommodityTable):
         commodities = CommodityTable.from_commodities(topology, commodities)
-    L = lib()
+    L = gen_lib()
     es = np.ascontiguousarray(topology.edge_src, np.int64)
     ed = np.ascontiguousarray(topology.edge_dst, np.int64)
     wt = np.ascontiguousarray(topology.weight, np.float64)

@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _abi as A
 from ._lib import NativeError, check, last_error, lib
-from .model import Instance, default_device
+from .model import InputError, Instance, _vec, default_device
 
 
 class KernelError(RuntimeError):
@@ -65,15 +65,17 @@ def _p(a):
 class _View:
     """Keeps contiguous float64 copies alive behind a pf_state_view."""
 
-    def __init__(self, state):
-        self.arrs = [np.ascontiguousarray(getattr(state, f), np.float64) for f in
-                     ("x", "y", "dual_demand", "dual_capacity", "dual_consensus", "dual_nonneg")]
+    def __init__(self, state, instance):
+        n = {"x": instance.num_paths, "y": instance.num_pairs, "dual_demand": instance.num_commodities,
+             "dual_capacity": instance.num_edges, "dual_consensus": instance.num_pairs,
+             "dual_nonneg": instance.num_paths}
+        self.arrs = [_vec(getattr(state, f), m, f"state.{f}") for f, m in n.items()]
         self.view = A.StateView(*(_p(a) for a in self.arrs), float(state.beta), int(state.alpha))
 
 
 def update_duals(state, instance: Instance):
     """kernels.py:206-216: returns (demand, capacity, consensus, nonneg) duals."""
-    v = _View(state)
+    v = _View(state, instance)
     dd, dc = np.empty(instance.num_commodities), np.empty(instance.num_edges)
     dcon, dn = np.empty(instance.num_pairs), np.empty(instance.num_paths)
     check(lib().pf_update_duals(instance.handle, C.byref(v.view), _p(dd), _p(dc), _p(dcon), _p(dn)))
@@ -82,7 +84,7 @@ def update_duals(state, instance: Instance):
 
 def update_slacks(state, instance: Instance):
     """kernels.py:219-232."""
-    v = _View(state)
+    v = _View(state, instance)
     sd, sc = np.empty(instance.num_commodities), np.empty(instance.num_edges)
     check(lib().pf_update_slacks(instance.handle, C.byref(v.view), _p(sd), _p(sc)))
     return sd, sc
@@ -90,7 +92,7 @@ def update_slacks(state, instance: Instance):
 
 def update_rate_suggestions(state, instance: Instance):
     """kernels.py:235-252."""
-    v = _View(state)
+    v = _View(state, instance)
     y = np.empty(instance.num_pairs)
     check(lib().pf_update_rate_suggestions(instance.handle, C.byref(v.view), _p(y)))
     return y
@@ -107,7 +109,7 @@ def _raise_kernel(instance, rc, bad):
 
 def solve_commodity_sums(state, instance: Instance, alpha):
     """kernels.py:267-282: per-commodity sums from the summed stationarity equation."""
-    v = _View(state)
+    v = _View(state, instance)
     out = np.empty(instance.num_commodities)
     bad = C.c_int64(-1)
     rc = lib().pf_solve_commodity_sums(instance.handle, C.byref(v.view), int(alpha), _p(out), C.byref(bad))
@@ -117,8 +119,8 @@ def solve_commodity_sums(state, instance: Instance, alpha):
 
 def update_rates(state, instance: Instance, sums, alpha):
     """kernels.py:285-296."""
-    v = _View(state)
-    s = np.ascontiguousarray(sums, np.float64)
+    v = _View(state, instance)
+    s = _vec(sums, instance.num_commodities, "sums")
     x = np.empty(instance.num_paths)
     check(lib().pf_update_rates(instance.handle, C.byref(v.view), _p(s), int(alpha), _p(x)))
     return x
@@ -135,6 +137,8 @@ def det_diff_norm(a, b, device=None):
     """_reduce.py:118-128 (device, 4096-block / 32-chunk order)."""
     a = np.ascontiguousarray(a, np.float64)
     b = np.ascontiguousarray(b, np.float64)
+    if a.ndim != 1 or a.shape != b.shape:
+        raise InputError(f"det_diff_norm: shapes {a.shape} and {b.shape} differ")
     out = C.c_double()
     dev = default_device() if device is None else device
     check(lib().pf_det_diff_norm(dev, _p(a), _p(b), a.shape[0], C.byref(out)))

@@ -180,12 +180,12 @@ def _validate_paths(topology: Topology, table: CommodityTable, flat: FlatPathSet
         return
     # the native check (OpenMP) finds whether any path is bad; the vectorised
     # code below only runs to name the first bad path with the reference's message
-    from ._lib import lib
+    from ._lib import gen_lib
     i64 = lambda a: np.ascontiguousarray(a, np.int64)  # noqa: E731
     arrs = [i64(cpp), i64(pep), i64(pe), i64(topology.edge_src), i64(topology.edge_dst), i64(table.src),
             i64(table.dst)]
     ptr = [a.ctypes.data_as(C.POINTER(C.c_int64)) for a in arrs]
-    if lib().pf_validate_paths(len(table), ptr[0], ptr[1], ptr[2], topology.num_edges, ptr[3], ptr[4], ptr[5],
+    if gen_lib().pf_validate_paths(len(table), ptr[0], ptr[1], ptr[2], topology.num_edges, ptr[3], ptr[4], ptr[5],
                                ptr[6]) < 0:
         return
     m = topology.num_edges
@@ -329,9 +329,18 @@ def with_conditions(instance: Instance, capacity=None, demand=None) -> Instance:
     return out
 
 
+def _vec(a, n, what) -> np.ndarray:
+    """Contiguous float64 copy of a length-n vector; a wrong length is an
+    InputError (the native side copies exactly n doubles from the host)."""
+    a = _f64(a)
+    if a.shape != (n,):
+        raise InputError(f"{what} length {a.shape} does not match {n}")
+    return a
+
+
 def commodity_sums(instance: Instance, rates) -> np.ndarray:
     """model.py:297-302 (device, reference reduction order)."""
-    rates = _f64(rates)
+    rates = _vec(rates, instance.num_paths, "rates")
     out = np.empty(instance.num_commodities)
     check(lib().pf_commodity_sums(instance.handle, _p(rates), _p(out)))
     return out
@@ -339,7 +348,7 @@ def commodity_sums(instance: Instance, rates) -> np.ndarray:
 
 def edge_loads(instance: Instance, rates) -> np.ndarray:
     """model.py:305-311."""
-    rates = _f64(rates)
+    rates = _vec(rates, instance.num_paths, "rates")
     out = np.empty(instance.num_edges)
     check(lib().pf_edge_loads(instance.handle, _p(rates), _p(out)))
     return out
@@ -347,7 +356,7 @@ def edge_loads(instance: Instance, rates) -> np.ndarray:
 
 def edge_loads_from_pairs(instance: Instance, pair_values) -> np.ndarray:
     """model.py:314-319."""
-    pv = _f64(pair_values)
+    pv = _vec(pair_values, instance.num_pairs, "pair values")
     out = np.empty(instance.num_edges)
     check(lib().pf_edge_loads_from_pairs(instance.handle, _p(pv), _p(out)))
     return out

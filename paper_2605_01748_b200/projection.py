@@ -6,7 +6,7 @@ import numpy as np
 
 from . import _abi as A
 from ._lib import check, lib
-from .model import Instance, InputError
+from .model import Instance, InputError, _vec
 
 
 def _p(a):
@@ -15,7 +15,7 @@ def _p(a):
 
 def score_paths(instance: Instance, rates, alpha):
     """projection.py:22-32: (commodity sum)^alpha x violated-edge count."""
-    r = np.ascontiguousarray(rates, np.float64)
+    r = _vec(rates, instance.num_paths, "rates")
     out = np.empty(instance.num_paths)
     check(lib().pf_score_paths(instance.handle, _p(r), int(alpha), _p(out)))
     return out

@@ -77,3 +77,55 @@ def test_generator_input_errors():
         H.gravity_table(topo, 0.0)
     with pytest.raises(InputError):
         H.k_shortest_paths(topo, H.gravity_demands(topo, 1.0), 0)
+
+
+def _golden_ksp():
+    import json
+    import os
+    p = os.path.join(G.GOLDEN, "golden_ksp.json")
+    if not os.path.exists(p):
+        pytest.skip("golden_ksp.json not generated")
+    with open(p) as fh:
+        return json.load(fh)
+
+
+def _chunk_digests(topo, tab, idx_chunks, k):
+    import hashlib
+    out = []
+    for idx in idx_chunks:
+        sub = CommodityTable(tab.nodes, tab.src[idx], tab.dst[idx], tab.demand[idx])
+        ps = H.k_shortest_paths(topo, sub, k)
+        h = hashlib.sha256()
+        for a in (ps.com_path_ptr, ps.path_edge_ptr, ps.path_edges):
+            h.update(np.ascontiguousarray(a, np.int64).tobytes())
+        out.append(h.hexdigest()[:32])
+    return out
+
+
+def test_ksp_config2_all_commodities_vs_networkx():
+    """SURVEY 8(f)#2 gate: all 249,500 commodities of config 2 (k = 8) give
+    path sets identical to the reference's networkx k_shortest_paths
+    (harness.py:138-176), chunk by chunk (tests/golden/make_golden_ksp.py)."""
+    g = _golden_ksp()
+    topo = H.random_topology(500, seed=500)
+    tab = H.gravity_table(topo, 1.0)
+    C = len(tab)
+    assert C == g["cfg2"]["commodities"]
+    ch = g["chunk"]
+    chunks = [np.arange(s, min(C, s + ch)) for s in range(0, C, ch)]
+    got = _chunk_digests(topo, tab, chunks, g["k"])
+    bad = [i for i, (a, b) in enumerate(zip(got, g["cfg2"]["digests"])) if a != b]
+    assert not bad, f"chunks differing from networkx: {bad[:10]}"
+    full = H.k_shortest_paths(topo, tab, g["k"])
+    assert full.path_edge_ptr.shape[0] - 1 == g["cfg2"]["paths"] and full.path_edges.shape[0] == g["cfg2"]["pairs"]
+
+
+def test_ksp_config3_sample_vs_networkx():
+    """10,000 commodities of config 3 (2000 nodes, 6,000 edges, k = 8)."""
+    g = _golden_ksp()["cfg3_sample"]
+    topo = H.random_topology(2000, seed=2000)
+    tab = H.gravity_table(topo, 1.0)
+    assert len(tab) == g["commodities_total"]
+    pick = np.sort(np.random.default_rng(g["seed"]).choice(len(tab), g["size"], replace=False))
+    chunks = [pick[s:s + g["chunk"]] for s in range(0, pick.size, g["chunk"])]
+    assert _chunk_digests(topo, tab, chunks, 8) == g["digests"]

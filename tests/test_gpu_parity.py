@@ -539,7 +539,9 @@ def test_fast_mode_outside_fused_limits_runs_exact():
     ps = pf.k_shortest_paths(topo, tab, 40)
     assert int(np.max(np.diff(np.asarray(ps.com_path_ptr)))) > 32
     inst = pf.build_instance_flat(topo, tab, ps, device=0)
-    fast = pf.solve(inst, pf.SolverConfig(mode="fast", max_iterations=200))
+    with pytest.warns(RuntimeWarning, match="layout limits"):
+        fast = pf.solve(inst, pf.SolverConfig(mode="fast", max_iterations=200))
+    assert fast.mode == "exact"  # the fallback is reported, not silent
     exact = pf.solve(inst, pf.SolverConfig(mode="exact", max_iterations=200))
     assert np.array_equal(fast.rates, exact.rates) and fast.iterations == exact.iterations
     s = pf.Solver(inst, pf.SolverConfig(mode="fast")).init()
