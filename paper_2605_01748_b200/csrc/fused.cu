@@ -76,24 +76,32 @@ constexpr unsigned FULL = 0xffffffffu;
 
 struct TileDesc {
     int32_t c0, c1, p0, p1, t0, np, sb, mb16;  // mb16: metadata offset / 16
+    int32_t nrun;                              // edge runs: distinct edges of the tile's pairs
+    int32_t nab;                               // runs summed by a warp (low 16 bits), by 8 lanes (high)
 };
+constexpr int RUN_WARP = 64;  // runs of >= RUN_WARP pairs are summed by a whole warp
+constexpr int RUN_OCT = 8;    // runs of >= RUN_OCT pairs by 8 lanes; shorter ones by one lane
 
 __host__ __device__ __forceinline__ int r16(int b) { return (b + 15) & ~15; }
 __host__ __device__ __forceinline__ int even(int n) { return (n + 1) & ~1; }
 
 // Byte offsets of the sections of one tile's metadata block.
 struct MetaOff {
-    int eid, spath, skp, poff, pcom, cpp, gpath, bytes;
+    int eid, spath, sperm, rstart, rord, poff, pcom, cpp, gpath, bytes;
 };
-__host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc) {
+__host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc, int nrun) {
     MetaOff m;
     int o = 0;
     m.eid = o;  // u16 [np] edge id of each pair (path-major)
     o += r16(2 * np);
     m.spath = o;  // u8 [np] tile-local path of each pair
     o += r16(np);
-    m.skp = o;  // u32 [np] (edge << 16) | tile-local pair, for the edge-sorted slots (stable by pair)
-    o += r16(4 * np);
+    m.sperm = o;  // u16 [np] tile-local pairs sorted by (edge, pair): the edge runs, back to back
+    o += r16(2 * np);
+    m.rstart = o;  // u16 [nrun + 1] start of each run in sperm (runs in edge order)
+    o += r16(2 * (nrun + 1));
+    m.rord = o;  // u16 [nrun] runs by decreasing length (work order: balanced over the warps)
+    o += r16(2 * nrun);
     m.poff = o;  // u16 [npath + 1] tile-local pair offset of each path
     o += r16(2 * (npath + 1));
     m.pcom = o;  // u8 [npath] tile-local commodity of each path
@@ -118,7 +126,7 @@ __host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E, int nbuf,
     s.s_dcon = o;
     o += 8 * tps;
     s.s_meta = o;
-    o += meta_off(tps, TPATH, TCOM).bytes;
+    o += meta_off(tps, TPATH, TCOM, tps < E ? tps : E).bytes;  // at most min(pairs, edges) runs
     s.s_xk = o;
     o += 8 * (TPATH + 2);
     s.s_xo = o;
@@ -199,6 +207,22 @@ struct Params {
 // Iteration-phase probe (tuning only, PF_FAST_PROBE): %globaltimer deltas of
 // CTA 0, thread 0, summed into g_probe[phase] (ns).
 __device__ unsigned long long g_probe[8];
+// Tile-phase probe (tuning builds only, -DPF_TPROBE): clock64 deltas of thread 0
+// of every CTA per tile phase, summed over tiles and CTAs into g_tprobe
+// (0 TMA wait, 1 y, 2 K + commodities, 3 dcon + barrier, 4 edge runs, 5 end barrier, 7 tiles).
+__device__ unsigned long long g_tprobe[8];
+#ifdef PF_TPROBE
+#define TP_DECL unsigned long long tp_last = 0;
+#define TP(i)                                                        \
+    if (threadIdx.x == 0) {                                          \
+        const unsigned long long t_ = clock64();                     \
+        if ((i) >= 0) atomicAdd(&g_tprobe[(i) < 0 ? 0 : (i)], t_ - tp_last); \
+        tp_last = t_;                                                \
+    }
+#else
+#define TP_DECL
+#define TP(i)
+#endif
 __device__ unsigned long long g_pmax[3];  // per-phase max over CTAs (reset per launch read)
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -281,7 +305,7 @@ __device__ __forceinline__ void issue_tile(const Params &P, const PassIO &io, co
                                            const SmemPlan &sp, int b, uint64_t *bar) {
     char *s = base + b * sp.stage;
     const int npath = d.p1 - d.p0, nc = d.c1 - d.c0;
-    const MetaOff m = meta_off(d.np, npath, nc);
+    const MetaOff m = meta_off(d.np, npath, nc, d.nrun);
     const int pa = d.p0 & ~1, npa = even(d.p1 - pa);
     const int ca = d.c0 & ~1, nca = even(d.c1 - ca);
     const uint32_t b_dcon = 8u * even(d.np), b_p = 8u * npa, b_c = 8u * nca;
@@ -580,12 +604,6 @@ __device__ __noinline__ void edge_phase(const Params &P, double f) {
 
 // ------------------------------------------------------------------ tile compute
 
-struct Tail {
-    double T, L;
-    int32_t open;  // the warp's whole range continues a run begun in an earlier warp
-    int32_t pad;
-};
-
 struct Acc {
     double *adj, *y;
     double2 *acc;      // per edge {T, L} in shared memory, or
@@ -606,12 +624,6 @@ __device__ __forceinline__ void acc_add(const Acc &A, int e, double T, double L)
         if (MODE != MODE_RB) __stcg(&A.gL[o], __ldcg(&A.gL[o]) + L);
     }
 }
-
-struct Fix {
-    bool on;
-    int key, w;
-    double T, L;
-};
 
 // The per-pair loops as functions with __restrict__ operands: the shared-memory
 // arrays a loop stores to never alias the ones it loads from, so the compiler
@@ -672,11 +684,11 @@ __device__ __forceinline__ double path_k(int lo, int hi, const double *__restric
 // MODE_A1: A(1) with y_0 = x_0[pair_path] (controller.py:118)
 template <int MODE>
 __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, const PassIO &io, const TileDesc &d,
-                                             const StageView &st, const Acc &A, Tail *tails, Fix &fx, double &r_x,
+                                             const StageView &st, const Acc &A, double &r_x,
                                              double &r_dd, double &r_dcon, double &r_dn) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int np = d.np, npath = d.p1 - d.p0, nc = d.c1 - d.c0;
-    const MetaOff m = meta_off(np, npath, nc);
+    const MetaOff m = meta_off(np, npath, nc, d.nrun);
     const uint16_t *eid = (const uint16_t *)(st.meta + m.eid);
     const uint8_t *spath = st.meta + m.spath;
     const uint16_t *poff = (const uint16_t *)(st.meta + m.poff);
@@ -685,6 +697,8 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     const uint16_t *gpath = (const uint16_t *)(st.meta + m.gpath);
     const double *dcon = st.dcon;
     double *ys = A.y;
+    TP_DECL
+    TP(-1)
     const double f = io.f;
     const double inv_beta = 1.0 / c.beta;
     double *const x_out = io.x_out, *const dn_out = io.dn_out, *const dd_out = io.dd_out;
@@ -697,6 +711,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     const double xlane = gp0 + lane < gp1 ? (MODE == MODE_RB ? st.xo[gp0 + lane] : st.xk[gp0 + lane]) : 0.0;
     if (!(P.ablate & 64)) pairs_y<MODE>(l0, l1, gp0, lane, xlane, spath, eid, dcon, A.adj, !P.adj_smem, ys);
     __syncwarp();
+    TP(1)
     // (2) paths (lane = path) and commodities (lane segments)
     double xnew_lane = 0.0;  // x' of this lane's path
     {
@@ -765,6 +780,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
         }
     }
     __syncwarp();
+    TP(2)
     // (3) pairs in path order: dual_consensus' (kernels.py:72) stored coalesced;
     // T = x' + dcon' (kernels.py:91) replaces the consumed dcon in the stage
     // (tv aliases dcon on purpose: every iteration reads dcon[l] before it
@@ -773,127 +789,73 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
                          const_cast<double *>(dcon));
     fence_proxy_async_shared();  // these generic writes precede the TMA that refills the stage
     __syncthreads();
+    TP(3)
 
     }
     if (P.ablate & 2) return;
-    // (4) pairs in edge-sorted order: the per-edge sums T = sum (x' + dcon')
-    // (kernels.py:91) and L = sum y (kernels.py:210).  Warp w owns sorted slots [s0, s1), lane `lane` the
-    // consecutive items [a, b): a sequential segmented sum per lane, one warp
-    // scan of the lane aggregates, then the run totals go to the CTA
-    // accumulators (a run never repeats an edge within a tile: no conflicts).
-    // A run begun in an earlier warp is completed after the barrier from the
-    // warps' tails.
-    const int q = ((np + NW - 1) / NW + 31) & ~31;
-    const int s0 = min(w * q, np), s1 = min(s0 + q, np);
-    const int IT = (s1 - s0 + 31) >> 5;
-    const int a = min(s0 + lane * IT, s1), b = min(a + IT, s1);
-    const uint32_t *skp = (const uint32_t *)(st.meta + m.skp);
-    const int kbefore = a > 0 ? (int)(skp[a - 1] >> 16) : -1;
-    // one sequential pass per lane: the lane's prefix (items continuing the run
-    // open at item a) is summed first; runs that start inside the lane are added
-    // at their end; the prefix and the lane's last run are settled after the
-    // warp scan.
-    double cT = 0.0, cL = 0.0, pT = 0.0, pL = 0.0;
-    const int pkey = kbefore;
-    int s = a;
-    uint32_t kp = s < b ? skp[s] : 0u;  // (edge << 16) | pair of the current item
-    auto item = [&](uint32_t kpv, int s_, double &T, double &L) {
-        const int pl = (int)(kpv & 0xffffu);
-        T += dcon[pl];  // x' + dcon' (written by step 3)
-        if (MODE != MODE_RB) L += ys[pl];
+    // (4) per-edge sums over the tile's edge runs: T = sum (x' + dcon')
+    // (kernels.py:91) and L = sum y (kernels.py:210).  A run is the tile's pairs
+    // on one edge (sperm[rstart[r] .. rstart[r + 1]), in pair order).  Runs are
+    // taken in decreasing length (rord) in three classes -- a warp, 8 lanes or
+    // one lane per run -- so the longest run (a source's out-edge, ~160 pairs
+    // at config 2) is not one serial chain; each run is summed in a fixed order
+    // and added to the CTA accumulator of its edge by one lane.  Runs of one tile have
+    // distinct edges, so no two lanes touch the same accumulator, and tiles are
+    // separated by block barriers: deterministic without atomics.
+    const uint16_t *sperm = (const uint16_t *)(st.meta + m.sperm);
+    const uint16_t *rstart = (const uint16_t *)(st.meta + m.rstart);
+    const uint16_t *rord = (const uint16_t *)(st.meta + m.rord);
+    const double *tv = dcon;  // x' + dcon' per pair (written over dcon by step 3)
+    const int nA = d.nab & 0xffff, nAB = nA + (d.nab >> 16);
+    // one run's items a, a + stp, a + 2 stp, ... < b into T, L (in order)
+    auto run_sum = [&](int a, int b, int stp, double &T, double &L) {
+        T = 0.0;
+        L = 0.0;
+        for (int s = a; s < b; s += stp) {
+            const int u = sperm[s];
+            T += tv[u];
+            if (MODE != MODE_RB) L += ys[u];
+        }
     };
-    while (s < b && (int)(kp >> 16) == kbefore) {
-        const uint32_t cur = kp;
-        if (s + 1 < b) kp = skp[s + 1];
-        item(cur, s, pT, pL);
-        ++s;
-    }
-    const bool pn = s > a;  // the prefix is non-empty
-    const bool hh = s < b;  // the lane holds a run head
-    int pk = hh ? (int)(kp >> 16) : kbefore;
-    for (; s < b; ++s) {
-        const uint32_t cur = kp;
-        if (s + 1 < b) kp = skp[s + 1];  // next item's key in flight while this one computes
-        const int k = (int)(cur >> 16);
-        if (k != pk) {  // run head at s: the previous run ended inside the lane
-            acc_add<MODE>(A, pk, cT, cL);
-            cT = 0.0;
-            cL = 0.0;
-            pk = k;
+    // long runs: a whole warp per run, then a fixed shuffle tree
+    for (int i = w; i < nA; i += NW) {
+        const int r = rord[i];
+        const int a = rstart[r], b = rstart[r + 1];
+        double T, L;
+        run_sum(a + lane, b, 32, T, L);
+        for (int o = 16; o > 0; o >>= 1) {
+            T += __shfl_xor_sync(FULL, T, o);
+            if (MODE != MODE_RB) L += __shfl_xor_sync(FULL, L, o);
         }
-        item(cur, s, cT, cL);
+        if (lane == 0) acc_add<MODE>(A, eid[sperm[a]], T, L);
     }
-    if (!hh) {  // the whole lane continues one run
-        cT = pT;
-        cL = pL;
-    }
-    // warp scan of (head, open-run aggregate): carry into each lane = the sum of
-    // the run that is open at the lane's first item, over the earlier lanes
-    const unsigned hm = __ballot_sync(FULL, hh);
-    double gT = hh ? cT : pT, gL = hh ? cL : pL;
+    // medium runs: 8 lanes per run, four runs per warp at a time (run i on
+    // warp i % NW: the longest medium runs spread over the warps)
     {
-        const unsigned upto = hm & (0xffffffffu >> (31 - lane));
-        const int f = upto ? 31 - __clz(upto) : 0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const double t = __shfl_up_sync(FULL, gT, o);
-            const double u = (MODE != MODE_RB) ? __shfl_up_sync(FULL, gL, o) : 0.0;
-            if (lane - o >= f) {
-                gT += t;
-                gL += u;
+        const int o8 = lane & 7;
+        const unsigned gm = 0xffu << (lane & 24);
+        for (int i = nA + (lane >> 3) * NW + w; i < nAB; i += NW * 4) {
+            const int r = rord[i];
+            const int a = rstart[r], b = rstart[r + 1];
+            double T, L;
+            run_sum(a + o8, b, 8, T, L);
+            for (int o = 4; o > 0; o >>= 1) {
+                T += __shfl_xor_sync(gm, T, o);
+                if (MODE != MODE_RB) L += __shfl_xor_sync(gm, L, o);
             }
+            if (o8 == 0) acc_add<MODE>(A, eid[sperm[a]], T, L);
         }
     }
-    double CT = __shfl_up_sync(FULL, gT, 1), CL = (MODE != MODE_RB) ? __shfl_up_sync(FULL, gL, 1) : 0.0;
-    if (lane == 0) {
-        CT = 0.0;
-        CL = 0.0;
+    TP(6)
+    // short runs: one lane per run
+    for (int i = nAB + lane * NW + w; i < d.nrun; i += NT) {
+        const int r = rord[i];
+        const int a = rstart[r], b = rstart[r + 1];
+        double T, L;
+        run_sum(a, b, 1, T, L);
+        acc_add<MODE>(A, eid[sperm[a]], T, L);
     }
-    const bool copen = (hm & ((1u << lane) - 1u)) == 0u;  // the carried run began before this warp's range
-    if (a < b) {
-        const int knext = b < np ? (int)(skp[b] >> 16) : -3;
-        // prefix run: items [a, first head) continue the carried run
-        if (pn) {
-            const double tT = CT + pT, tL = CL + pL;
-            const bool ends = hh || knext != pkey;  // with a head in the lane the prefix ends before it
-            if (ends) {
-                if (copen) {  // completed by the caller after the end-of-tile barrier
-                    fx.on = true;
-                    fx.key = pkey;
-                    fx.T = tT;
-                    fx.L = tL;
-                    fx.w = w;
-                } else {
-                    acc_add<MODE>(A, pkey, tT, tL);
-                }
-            } else if (b == s1) {
-                tails[w] = Tail{tT, tL, copen ? 1 : 0, 0};
-            }
-        }
-        // last run of a lane with a head: started inside the lane
-        if (hh) {
-            if (knext != pk) {
-                acc_add<MODE>(A, pk, cT, cL);
-            } else if (b == s1) {
-                tails[w] = Tail{cT, cL, 0, 0};
-            }
-        }
-    }
-}
-
-// The warp's first run began in an earlier warp of the same tile: add the
-// carried tails (after the end-of-tile barrier, before the next tile's scan).
-template <int MODE>
-__device__ __forceinline__ void apply_fix(Fix &fx, const Tail *tails, const Acc &A) {
-    if (!fx.on) return;
-    double cT = 0.0, cL = 0.0;
-    for (int ww = fx.w - 1; ww >= 0; --ww) {
-        cT += tails[ww].T;
-        cL += tails[ww].L;
-        if (!tails[ww].open) break;
-    }
-    acc_add<MODE>(A, fx.key, cT + fx.T, cL + fx.L);
-    fx.on = false;
+    TP(4)
 }
 
 template <int MODE>
@@ -948,7 +910,6 @@ struct CtaShared {
     TileDesc dl[DL];  // this CTA's tiles (thread 0 reads them on the tile boundaries)
     int32_t dl_rev;   // walk direction dl[] is stored in; -1 = not filled (a CTA owns <= DL tiles: kept)
     PassIO io;
-    Tail tails[NW];
     double red[NW];
     double red4[NW][4];
 };
@@ -1020,8 +981,6 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
     if (tid == 0 && !keep && my <= DL) cs.dl_rev = rev ? 1 : 0;  // every thread read dl_rev before the barrier
     const PassIO &io = cs.io;
     double r_x = 0.0, r_dd = 0.0, r_dcon = 0.0, r_dn = 0.0;
-    Fix fx;
-    fx.on = false;
     for (int k = 0; k < my; ++k, ++seq) {
         const int b = dbl ? (seq & 1) : 0;
         const uint32_t par = dbl ? ((seq >> 1) & 1) : (seq & 1);
@@ -1034,21 +993,34 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
                 const TileDesc dn_ = desc_of(k + P.pf_dist);
                 prefetch_l2(io.dcon_in + dn_.sb, 8u * even(dn_.np));
                 prefetch_l2(P.meta + (size_t)dn_.mb16 * 16,
-                            (uint32_t)meta_off(dn_.np, dn_.p1 - dn_.p0, dn_.c1 - dn_.c0).bytes);
+                            (uint32_t)meta_off(dn_.np, dn_.p1 - dn_.p0, dn_.c1 - dn_.c0, dn_.nrun).bytes);
             }
         }
+#ifdef PF_TPROBE
+        const unsigned long long tw0 = clock64();
+#endif
         mbar_wait(&cs.bar[b], par);
+#ifdef PF_TPROBE
+        if (tid == 0) {
+            atomicAdd(&g_tprobe[0], clock64() - tw0);
+            atomicAdd(&g_tprobe[7], 1ull);
+        }
+#endif
         const TileDesc d = cs.sd[b];
         const StageView st = stage_view(base, sp, b, d);
-        tile_compute<MODE>(P, c, io, d, st, A, cs.tails, fx, r_x, r_dd, r_dcon, r_dn);
+        tile_compute<MODE>(P, c, io, d, st, A, r_x, r_dd, r_dcon, r_dn);
+#ifdef PF_TPROBE
+        const unsigned long long tb0 = clock64();
+#endif
         __syncthreads();  // the stage is free for the next TMA (its generic writes were proxy-fenced)
+#ifdef PF_TPROBE
+        if (tid == 0) atomicAdd(&g_tprobe[5], clock64() - tb0);
+#endif
         if (!dbl && tid == 0 && k + 1 < my) {  // before the fix-ups (they do not touch the stage)
             cs.sd[0] = desc_of(k + 1);
             issue_tile<MODE>(P, io, cs.sd[0], base, sp, 0, &cs.bar[0]);
         }
-        apply_fix<MODE>(fx, cs.tails, A);
     }
-    __syncthreads();  // last tile's fix-ups
     for (int e = tid; e < E; e += NT) {
         if (!P.acc_smem) break;  // the rows are the partials already
         const double2 v = A.acc[e];
@@ -1602,6 +1574,7 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
     std::vector<TileDesc> tiles;
     std::vector<std::array<int32_t, NW + 1>> tgroups;  // group commodity boundaries per tile
     int64_t slot = 0, mb = 0;
+    std::vector<int32_t> emark(I.E > 0 ? I.E : 1, -1);  // tile stamp per edge: counts a tile's runs
     {
         int64_t gi = 0;
         while (gi < ng) {
@@ -1627,10 +1600,17 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
             d.sb = (int32_t)slot;
             require(mb / 16 < INT_MAX, "fast-mode metadata exceeds 32 GB");
             d.mb16 = (int32_t)(mb / 16);
+            d.nrun = 0;
+            d.nab = 0;
+            for (int32_t t = d.t0; t < d.t0 + d.np; ++t)
+                if (emark[pedge[t]] != (int32_t)tiles.size()) {
+                    emark[pedge[t]] = (int32_t)tiles.size();
+                    ++d.nrun;
+                }
             tiles.push_back(d);
             tgroups.push_back(gb);
             slot += (d.np + SLOT_ALIGN - 1) / SLOT_ALIGN * SLOT_ALIGN;
-            mb += meta_off(d.np, d.p1 - d.p0, d.c1 - d.c0).bytes;
+            mb += meta_off(d.np, d.p1 - d.p0, d.c1 - d.c0, d.nrun).bytes;
             require(slot < INT_MAX, "too many demand-path pairs for fast mode");
             gi = gj;
         }
@@ -1640,11 +1620,12 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
     L->meta_bytes = mb;
     std::vector<uint8_t> meta(mb ? mb : 16, 0);
     std::vector<int32_t> pair_tile(I.NP);
+    std::vector<int32_t> tiles_nab(tiles.size());
 #pragma omp parallel for schedule(dynamic, 16)
     for (int64_t ti = 0; ti < (int64_t)tiles.size(); ++ti) {
         const TileDesc &T = tiles[ti];
         const int np = T.np, npath = T.p1 - T.p0, nc = T.c1 - T.c0;
-        const MetaOff m = meta_off(np, npath, nc);
+        const MetaOff m = meta_off(np, npath, nc, T.nrun);
         uint8_t *blk = meta.data() + (int64_t)T.mb16 * 16;
         uint16_t *eid = (uint16_t *)(blk + m.eid);
         std::vector<uint16_t> perm(np);
@@ -1659,15 +1640,34 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
             pair_tile[T.t0 + l] = (int32_t)ti;
         }
         std::stable_sort(perm.begin(), perm.end(), [&](uint16_t a, uint16_t b) { return eid[a] < eid[b]; });
-        uint32_t *skp = (uint32_t *)(blk + m.skp);
         for (int i = 0; i < npath; ++i) {
             poff[i] = (uint16_t)(pptr[T.p0 + i] - T.t0);
             for (int32_t t = pptr[T.p0 + i]; t < pptr[T.p0 + i + 1]; ++t) spath[t - T.t0] = (uint8_t)i;
         }
         poff[npath] = (uint16_t)np;
+        // edge runs: sperm = pairs sorted by (edge, pair); rstart = run starts;
+        // rord = runs by decreasing length (stable)
+        uint16_t *sperm = (uint16_t *)(blk + m.sperm);
+        uint16_t *rstart = (uint16_t *)(blk + m.rstart);
+        uint16_t *rord = (uint16_t *)(blk + m.rord);
+        int nr = 0;
         for (int sl = 0; sl < np; ++sl) {
-            skp[sl] = ((uint32_t)eid[perm[sl]] << 16) | perm[sl];
+            sperm[sl] = perm[sl];
+            if (sl == 0 || eid[perm[sl]] != eid[perm[sl - 1]]) rstart[nr++] = (uint16_t)sl;
         }
+        require(nr == T.nrun, "fast layout: run count mismatch");
+        rstart[nr] = (uint16_t)np;
+        for (int r = 0; r < nr; ++r) rord[r] = (uint16_t)r;
+        std::stable_sort(rord, rord + nr, [&](uint16_t a, uint16_t b) {
+            return rstart[a + 1] - rstart[a] > rstart[b + 1] - rstart[b];
+        });
+        int na = 0, nb = 0;
+        for (int r = 0; r < nr; ++r) {
+            const int len = rstart[rord[r] + 1] - rstart[rord[r]];
+            na += len >= RUN_WARP;
+            nb += len >= RUN_OCT && len < RUN_WARP;
+        }
+        tiles_nab[ti] = na | (nb << 16);
         for (int j = 0; j < nc; ++j) {
             lcpp[j] = (uint16_t)(cpp[T.c0 + j] - T.p0);
             for (int32_t p = cpp[T.c0 + j]; p < cpp[T.c0 + j + 1]; ++p) pcom[p - T.p0] = (uint8_t)j;
@@ -1675,12 +1675,13 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         lcpp[nc] = (uint16_t)npath;
         for (int k = 0; k <= NW; ++k) gpath[k] = (uint16_t)(cpp[tgroups[ti][k]] - T.p0);
     }
+    for (size_t ti = 0; ti < tiles.size(); ++ti) tiles[ti].nab = tiles_nab[ti];
     // compulsory HBM bytes of one M pass: what the bulk copies read plus what the pass writes
     int64_t bytes = 0;
     for (const TileDesc &d : tiles) {
         const int npath = d.p1 - d.p0, nc = d.c1 - d.c0;
         const int npa = even(d.p1 - (d.p0 & ~1)), nca = even(d.c1 - (d.c0 & ~1));
-        bytes += 8LL * even(d.np) + meta_off(d.np, npath, nc).bytes + 16LL * npa + 16LL * nca;  // reads
+        bytes += 8LL * even(d.np) + meta_off(d.np, npath, nc, d.nrun).bytes + 16LL * npa + 16LL * nca;  // reads
         bytes += 8LL * d.np + 16LL * npath + 8LL * nc;                                            // writes
     }
     L->bytes_per_pass = bytes;
@@ -2213,6 +2214,18 @@ int64_t fast_run(FastSolver *F, int64_t max_steps, cudaStream_t s, float *ms) {
         unsigned long long z[8] = {0};
         PF_CUDA(cudaMemcpyToSymbol(g_probe, z, sizeof(z)));
     }
+#ifdef PF_TPROBE
+    {
+        unsigned long long tp[8];
+        PF_CUDA(cudaMemcpyFromSymbol(tp, g_tprobe, sizeof(tp)));
+        const double nt = (double)std::max<unsigned long long>(1, tp[7]);
+        fprintf(stderr, "[tprobe] cycles per tile (thread 0, %llu tiles): tma-wait %.0f, y %.0f, K+com %.0f, "
+                        "dcon+bar %.0f, runs-long %.0f, runs-short %.0f, end-bar %.0f\n",
+                tp[7], tp[0] / nt, tp[1] / nt, tp[2] / nt, tp[3] / nt, tp[6] / nt, tp[4] / nt, tp[5] / nt);
+        unsigned long long z[8] = {0};
+        PF_CUDA(cudaMemcpyToSymbol(g_tprobe, z, sizeof(z)));
+    }
+#endif
     return c.iteration - start;
 }
 

@@ -81,7 +81,10 @@ __global__ void k_scores(InstView I, const double *x_sums, const uint8_t *viol, 
         i = j;
     }
     double s = npmax0(x_sums[I.path_com[p]]);
-    scores[p] = pow(s, (double)alpha) * total;
+    // np.power(s, 0.0) == 1 and np.power(s, 1.0) == s exactly; CUDA's pow is
+    // only within an ulp of the latter
+    const double sa = alpha == 0 ? 1.0 : alpha == 1 ? s : pow(s, (double)alpha);
+    scores[p] = sa * total;
 }
 
 // projection.py:63-74 + _trim_slice :35-48; one thread per commodity.
