@@ -150,6 +150,9 @@ int pf_instance_with_conditions(const pf_instance *base, const double *capacity 
                                 const double *demand /*nullable*/, pf_instance **out);
 int pf_instance_destroy(pf_instance *inst);
 int pf_instance_sizes(const pf_instance *inst, int64_t *C, int64_t *P, int64_t *E, int64_t *NP);
+/* Whether fast mode's fused kernel can run this instance (at most 32 paths and
+ * 16,384 pairs per commodity, 65,535 edges); otherwise `why` says which limit. */
+int pf_instance_fast_supported(const pf_instance *inst, int *ok, char *why /*nullable*/, size_t why_len);
 int pf_instance_export_index(const pf_instance *inst, int field, int64_t *out);
 int pf_instance_export_values(const pf_instance *inst, int field, double *out);
 

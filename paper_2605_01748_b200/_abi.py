@@ -55,6 +55,7 @@ SIGNATURES = {
     "pf_instance_with_conditions": (C.c_int, [vp, f64p, f64p, C.POINTER(vp)]),
     "pf_instance_destroy": (C.c_int, [vp]),
     "pf_instance_sizes": (C.c_int, [vp, i64p, i64p, i64p, i64p]),
+    "pf_instance_fast_supported": (C.c_int, [vp, C.POINTER(C.c_int), C.c_char_p, C.c_size_t]),
     "pf_instance_export_index": (C.c_int, [vp, C.c_int, i64p]),
     "pf_instance_export_values": (C.c_int, [vp, C.c_int, f64p]),
     "pf_commodity_sums": (C.c_int, [vp, f64p, f64p]),

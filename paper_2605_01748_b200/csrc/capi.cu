@@ -995,6 +995,18 @@ int pf_solver_set_edge_counts(pf_solver *S, const double *counts) {
     });
 }
 
+int pf_instance_fast_supported(const pf_instance *inst, int *ok, char *why, size_t why_len) {
+    return guard([&] {
+        require(inst != nullptr && ok != nullptr, "null argument");
+        DeviceGuard g(inst->device());
+        std::string w;
+        *ok = fast_supported(inst, &w) ? 1 : 0;
+        if (why && why_len) {
+            std::snprintf(why, why_len, "%s", w.c_str());
+        }
+    });
+}
+
 int pf_solver_trace(pf_solver *S, pf_trace_row *rows, int64_t cap, int64_t *total) {
     return guard([&] {
         require(S != nullptr && total != nullptr && (rows != nullptr || cap == 0), "null argument");

@@ -87,15 +87,13 @@ __host__ __device__ __forceinline__ int even(int n) { return (n + 1) & ~1; }
 
 // Byte offsets of the sections of one tile's metadata block.
 struct MetaOff {
-    int eid, spath, sperm, rstart, rord, poff, pcom, cpp, gpath, bytes;
+    int eid, sperm, rstart, rord, poff, pcom, cpp, gpath, bytes;
 };
 __host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc, int nrun) {
     MetaOff m;
     int o = 0;
-    m.eid = o;  // u16 [np] edge id of each pair (path-major)
+    m.eid = o;  // u16 [np] edge id of each pair (hop-major within each group)
     o += r16(2 * np);
-    m.spath = o;  // u8 [np] tile-local path of each pair
-    o += r16(np);
     m.sperm = o;  // u16 [np] tile-local pairs sorted by (edge, pair): the edge runs, back to back
     o += r16(2 * np);
     m.rstart = o;  // u16 [nrun + 1] start of each run in sperm (runs in edge order)
@@ -156,7 +154,7 @@ struct TileLayout {
     int64_t nslots = 0, meta_bytes = 0;
     DevBuf<TileDesc> desc;      // per tile
     DevBuf<uint8_t> meta;       // per-tile metadata blocks
-    DevBuf<int32_t> pair_tile;  // [NP] tile of pair t (export only)
+    DevBuf<int32_t> pair_slot;  // [NP] fast-layout slot of reference pair t (export only)
     std::vector<TileDesc> h_desc;
     int64_t bytes_per_pass = 0;  // compulsory HBM bytes of one M pass over the tiles
 };
@@ -625,36 +623,46 @@ __device__ __forceinline__ void acc_add(const Acc &A, int e, double T, double L)
     }
 }
 
-// The per-pair loops as functions with __restrict__ operands: the shared-memory
-// arrays a loop stores to never alias the ones it loads from, so the compiler
-// may overlap the dependent loads of consecutive iterations.
+// Per-pair loops over one commodity group in its hop-major order: lane i holds
+// path gp0 + i (h hops); step j visits the j-th pair of every path longer than
+// j, the active lanes' pairs stored consecutively in lane order, so each step is
+// one contiguous, conflict-free row and the lane keeps its path's rate and K_p
+// in registers (no per-pair path index, no shuffle, no per-path walk).
+//   y_j = max0(x + dcon_j - adj_e) (kernels.py:98-100), K = sum_j (y_j - dcon_j) in
+//   hop order (kernels.py:110-113)
 template <int MODE>
-__device__ __forceinline__ void pairs_y(int l0, int l1, int gp0, int lane, double xlane,
-                                        const uint8_t *__restrict__ spath, const uint16_t *__restrict__ eid,
-                                        const double *__restrict__ dcon, const double *__restrict__ adj,
-                                        bool adj_l1, double *__restrict__ ys) {
+__device__ __forceinline__ double hops_y(int base, int h, int H, unsigned lt, double xl,
+                                         const uint16_t *__restrict__ eid, const double *__restrict__ dcon,
+                                         const double *__restrict__ adj, bool adj_l1, double *__restrict__ ys) {
+    double K = 0.0;
 #pragma unroll 4
-    for (int base = l0; base < l1; base += 32) {
-        const int l = base + lane;
-        const int i = l < l1 ? (int)spath[l] - gp0 : 0;
-        const double xp = __shfl_sync(FULL, xlane, i);
-        if (l < l1) ys[l] = MODE == MODE_A1 ? xp : max0(xp + dcon[l] - (adj_l1 ? __ldca(&adj[eid[l]]) : adj[eid[l]]));
+    for (int j = 0; j < H; ++j) {
+        const bool on = h > j;
+        const unsigned act = __ballot_sync(FULL, on);
+        if (on) {
+            const int l = base + __popc(act & lt);
+            const double dv = dcon[l];
+            const double y = MODE == MODE_A1 ? xl : max0(xl + dv - (adj_l1 ? __ldca(&adj[eid[l]]) : adj[eid[l]]));
+            ys[l] = y;
+            K += y - dv;
+        }
+        base += __popc(act);
     }
+    return K;
 }
 
 // dual_consensus' (kernels.py:72) stored coalesced to global; T = x' + dcon'
 // (kernels.py:91) into tv
-__device__ __forceinline__ double pairs_dcon(int l0, int l1, int gp0, int lane, double xlane, double f,
-                                             const uint8_t *__restrict__ spath, const double *__restrict__ dcon,
-                                             const double *__restrict__ ys, double *__restrict__ dco,
-                                             double *__restrict__ tv) {
+__device__ __forceinline__ double hops_dcon(int base, int h, int H, unsigned lt, double xn, double f,
+                                            const double *__restrict__ dcon, const double *__restrict__ ys,
+                                            double *__restrict__ dco, double *__restrict__ tv) {
     double r = 0.0;
 #pragma unroll 4
-    for (int base = l0; base < l1; base += 32) {
-        const int l = base + lane;
-        const int i = l < l1 ? (int)spath[l] - gp0 : 0;
-        const double xn = __shfl_sync(FULL, xlane, i);
-        if (l < l1) {
+    for (int j = 0; j < H; ++j) {
+        const bool on = h > j;
+        const unsigned act = __ballot_sync(FULL, on);
+        if (on) {
+            const int l = base + __popc(act & lt);
             const double dks = dcon[l] * f;
             const double dnew = max0(dks + xn - ys[l]);
             dco[l] = dnew;
@@ -662,21 +670,9 @@ __device__ __forceinline__ double pairs_dcon(int l0, int l1, int gp0, int lane, 
             r += df * df;
             tv[l] = xn + dnew;
         }
+        base += __popc(act);
     }
     return r;
-}
-
-// K_p over the path's pairs (two chains, fixed association)
-__device__ __forceinline__ double path_k(int lo, int hi, const double *__restrict__ ys,
-                                         const double *__restrict__ dcon) {
-    double K = 0.0, K1 = 0.0;
-    int l = lo;
-    for (; l + 1 < hi; l += 2) {
-        K += ys[l] - dcon[l];
-        K1 += ys[l + 1] - dcon[l + 1];
-    }
-    if (l < hi) K += ys[l] - dcon[l];
-    return K + K1;
 }
 
 // MODE_M : B(k+1) [y, K/w, roots, x_{k+1}] fused with A(k+2) [duals_{k+2}, T/L]
@@ -690,7 +686,6 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     const int np = d.np, npath = d.p1 - d.p0, nc = d.c1 - d.c0;
     const MetaOff m = meta_off(np, npath, nc, d.nrun);
     const uint16_t *eid = (const uint16_t *)(st.meta + m.eid);
-    const uint8_t *spath = st.meta + m.spath;
     const uint16_t *poff = (const uint16_t *)(st.meta + m.poff);
     const uint8_t *pcom = st.meta + m.pcom;
     const uint16_t *cpp = (const uint16_t *)(st.meta + m.cpp);
@@ -705,11 +700,15 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
 
     // ---- this warp's commodity group
     const int gp0 = gpath[w], gp1 = gpath[w + 1];
-    const int l0 = poff[gp0], l1 = poff[gp1];
+    const int gbase = poff[gp0];  // the group's pairs: [gbase, poff[gp1]), hop-major
+    const unsigned lt = (1u << lane) - 1u;
+    const int hl = gp0 + lane < gp1 ? poff[gp0 + lane + 1] - poff[gp0 + lane] : 0;  // this lane's path hops
+    const int H = __reduce_max_sync(FULL, (unsigned)hl);
     if (!(P.ablate & 1)) {
-    // (1) pairs: y (kernels.py:98-100); the path's rate comes from its lane
+    // (1) pairs: y (kernels.py:98-100) and K_p (kernels.py:110-113) in the lane
     const double xlane = gp0 + lane < gp1 ? (MODE == MODE_RB ? st.xo[gp0 + lane] : st.xk[gp0 + lane]) : 0.0;
-    if (!(P.ablate & 64)) pairs_y<MODE>(l0, l1, gp0, lane, xlane, spath, eid, dcon, A.adj, !P.adj_smem, ys);
+    double Kl = 0.0;
+    if (!(P.ablate & 64)) Kl = hops_y<MODE>(gbase, hl, H, lt, xlane, eid, dcon, A.adj, !P.adj_smem, ys);
     __syncwarp();
     TP(1)
     // (2) paths (lane = path) and commodities (lane segments)
@@ -730,14 +729,13 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
         if (MODE == MODE_M && !(P.ablate & 16)) {
             double K = 0.0, wgt = 0.0;
             if (valid) {
-                const int lo = poff[p], hi = poff[p + 1];
-                K = (P.ablate & 32) ? 0.0 : path_k(lo, hi, ys, dcon);
+                K = (P.ablate & 32) ? 0.0 : Kl;
                 const double dnv = st.dn[p];
                 if (xk < dnv) {  // frozen non-negativity activity (kernels.py:114-119)
                     K += dnv;
-                    wgt = rcp_int(hi - lo + 1);
+                    wgt = rcp_int(hl + 1);
                 } else {
-                    wgt = rcp_int(hi - lo);
+                    wgt = rcp_int(hl);
                 }
             }
             double Wc = wgt, Qc = wgt * K;
@@ -781,12 +779,11 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     }
     __syncwarp();
     TP(2)
-    // (3) pairs in path order: dual_consensus' (kernels.py:72) stored coalesced;
+    // (3) pairs, hop-major: dual_consensus' (kernels.py:72) stored coalesced;
     // T = x' + dcon' (kernels.py:91) replaces the consumed dcon in the stage
-    // (tv aliases dcon on purpose: every iteration reads dcon[l] before it
-    // writes tv[l], for the same l only)
-    r_dcon += pairs_dcon(l0, l1, gp0, lane, xnew_lane, f, spath, dcon, ys, io.dcon_out + d.sb,
-                         const_cast<double *>(dcon));
+    // (tv aliases dcon on purpose: every step reads dcon[l] before it writes
+    // tv[l], for the same l only)
+    r_dcon += hops_dcon(gbase, hl, H, lt, xnew_lane, f, dcon, ys, io.dcon_out + d.sb, const_cast<double *>(dcon));
     fence_proxy_async_shared();  // these generic writes precede the TMA that refills the stage
     __syncthreads();
     TP(3)
@@ -1402,13 +1399,12 @@ __global__ void k_ctrl_update(Ctrl *ctrl, int op) {
 // Export helpers (reference pair order), for the state of the last completed
 // iteration k: x_k in x[xc], x_{k-1} in x[xc^1], duals_k in buffer db^1 (db
 // holds the speculative duals_{k+1}), adj_k, rescale factor f_k pending.
-__global__ void k_export_pairs(const __grid_constant__ Params P, const int32_t *pair_tile, double *y_out,
+__global__ void k_export_pairs(const __grid_constant__ Params P, const int32_t *pair_slot, double *y_out,
                                double *dcon_out) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= P.I.NP) return;
     const Ctrl c = *P.ctrl;
-    const TileDesc d = P.desc[pair_tile[t]];
-    const int sl = d.sb + (t - d.t0);
+    const int sl = pair_slot[t];
     const int p = P.I.pair_path[t];
     if (c.iteration == 0) {
         if (y_out) y_out[t] = P.x[c.xc][p];
@@ -1479,7 +1475,18 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         int per_sm = 0, reserved = 0;
         PF_CUDA(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, inst->device()));
         PF_CUDA(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, inst->device()));
-        const int64_t budget = per_sm / 2 - reserved - 3072;  // static shared memory (CtaShared, ...)
+        // static shared memory of the kernels (CtaShared, Ctrl, ...), queried
+        int64_t stat = 0;
+        {
+            cudaFuncAttributes fa{};
+            PF_CUDA(cudaFuncGetAttributes(&fa, k_fused<false>));
+            stat = (int64_t)fa.sharedSizeBytes;
+            PF_CUDA(cudaFuncGetAttributes(&fa, k_fused<true>));
+            stat = std::max<int64_t>(stat, (int64_t)fa.sharedSizeBytes);
+            PF_CUDA(cudaFuncGetAttributes(&fa, k_pass<MODE_M>));
+            stat = std::max<int64_t>(stat, (int64_t)fa.sharedSizeBytes);
+        }
+        const int64_t budget = per_sm / 2 - reserved - stat;
         if (smem_plan(1024, (int)I.E, 1).total > budget || getenv("PF_FAST_LARGE_E")) {
             // large E: the shared-memory edge tables rule out two CTAs per SM; the
             // adjustment table is read through L1 (one CTA per SM, large tiles), or
@@ -1496,7 +1503,7 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
                 while (tps_min > 512 && smem_plan((int)tps_min, (int)I.E, 1, false, false).total > budget)
                     tps_min -= 256;
             } else {
-                const int64_t budget1 = per_sm - reserved - 3072;
+                const int64_t budget1 = per_sm - reserved - stat;
                 while (tps_min > 512 && smem_plan((int)tps_min, (int)I.E, 1, false).total > budget1)
                     tps_min -= 256;
             }
@@ -1619,7 +1626,7 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
     L->nslots = slot;
     L->meta_bytes = mb;
     std::vector<uint8_t> meta(mb ? mb : 16, 0);
-    std::vector<int32_t> pair_tile(I.NP);
+    std::vector<int32_t> pair_slot(I.NP);
     std::vector<int32_t> tiles_nab(tiles.size());
 #pragma omp parallel for schedule(dynamic, 16)
     for (int64_t ti = 0; ti < (int64_t)tiles.size(); ++ti) {
@@ -1629,22 +1636,30 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         uint8_t *blk = meta.data() + (int64_t)T.mb16 * 16;
         uint16_t *eid = (uint16_t *)(blk + m.eid);
         std::vector<uint16_t> perm(np);
-        uint8_t *spath = blk + m.spath;
         uint16_t *poff = (uint16_t *)(blk + m.poff);
         uint8_t *pcom = blk + m.pcom;
         uint16_t *lcpp = (uint16_t *)(blk + m.cpp);
         uint16_t *gpath = (uint16_t *)(blk + m.gpath);
-        for (int l = 0; l < np; ++l) {
-            eid[l] = (uint16_t)pedge[T.t0 + l];
-            perm[l] = (uint16_t)l;
-            pair_tile[T.t0 + l] = (int32_t)ti;
-        }
-        std::stable_sort(perm.begin(), perm.end(), [&](uint16_t a, uint16_t b) { return eid[a] < eid[b]; });
-        for (int i = 0; i < npath; ++i) {
-            poff[i] = (uint16_t)(pptr[T.p0 + i] - T.t0);
-            for (int32_t t = pptr[T.p0 + i]; t < pptr[T.p0 + i + 1]; ++t) spath[t - T.t0] = (uint8_t)i;
-        }
+        for (int i = 0; i < npath; ++i) poff[i] = (uint16_t)(pptr[T.p0 + i] - T.t0);
         poff[npath] = (uint16_t)np;
+        for (int k = 0; k <= NW; ++k) gpath[k] = (uint16_t)(cpp[tgroups[ti][k]] - T.p0);
+        // hop-major order within each group: step j holds the j-th pair of every
+        // path with more than j hops, in path order (the kernel's hops_y / hops_dcon)
+        for (int k = 0; k < NW; ++k) {
+            int H = 0;
+            for (int i = gpath[k]; i < gpath[k + 1]; ++i) H = std::max(H, poff[i + 1] - poff[i]);
+            int pos = gpath[k] < npath ? poff[gpath[k]] : np;
+            for (int j = 0; j < H; ++j)
+                for (int i = gpath[k]; i < gpath[k + 1]; ++i)
+                    if (poff[i + 1] - poff[i] > j) {
+                        const int l = poff[i] + j;  // tile-local reference pair
+                        eid[pos] = (uint16_t)pedge[T.t0 + l];
+                        pair_slot[T.t0 + l] = T.sb + pos;
+                        ++pos;
+                    }
+        }
+        for (int l = 0; l < np; ++l) perm[l] = (uint16_t)l;
+        std::stable_sort(perm.begin(), perm.end(), [&](uint16_t a, uint16_t b) { return eid[a] < eid[b]; });
         // edge runs: sperm = pairs sorted by (edge, pair); rstart = run starts;
         // rord = runs by decreasing length (stable)
         uint16_t *sperm = (uint16_t *)(blk + m.sperm);
@@ -1673,7 +1688,6 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
             for (int32_t p = cpp[T.c0 + j]; p < cpp[T.c0 + j + 1]; ++p) pcom[p - T.p0] = (uint8_t)j;
         }
         lcpp[nc] = (uint16_t)npath;
-        for (int k = 0; k <= NW; ++k) gpath[k] = (uint16_t)(cpp[tgroups[ti][k]] - T.p0);
     }
     for (size_t ti = 0; ti < tiles.size(); ++ti) tiles[ti].nab = tiles_nab[ti];
     // compulsory HBM bytes of one M pass: what the bulk copies read plus what the pass writes
@@ -1687,10 +1701,10 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
     L->bytes_per_pass = bytes;
     L->desc.alloc(tiles.size() ? tiles.size() : 1);
     L->meta.alloc(meta.size());
-    L->pair_tile.alloc(I.NP ? I.NP : 1);
+    L->pair_slot.alloc(I.NP ? I.NP : 1);
     h2d(L->desc.p, tiles.data(), tiles.size(), s);
     h2d(L->meta.p, meta.data(), meta.size(), s);
-    h2d(L->pair_tile.p, pair_tile.data(), I.NP, s);
+    h2d(L->pair_slot.p, pair_slot.data(), I.NP, s);
     PF_CUDA(cudaStreamSynchronize(s));
     L->h_desc = std::move(tiles);
     return L;
@@ -2263,7 +2277,7 @@ void fast_export_state(FastSolver *F, double *x, double *y, double *dd, double *
     PF_CUDA(cudaStreamSynchronize(s));
     const int dcur = c.iteration == 0 ? c.db : (c.db ^ 1);
     DevBuf<double> dy(I.NP ? I.NP : 1), ddc(I.NP ? I.NP : 1), tmp(std::max<int64_t>({I.C, I.E, I.P, 1}));
-    if (I.NP) k_export_pairs<<<ceil_div(I.NP, 256), 256, 0, s>>>(F->P, F->L->pair_tile.p, dy.p, ddc.p);
+    if (I.NP) k_export_pairs<<<ceil_div(I.NP, 256), 256, 0, s>>>(F->P, F->L->pair_slot.p, dy.p, ddc.p);
     PF_CHECK_LAUNCH();
     if (x) d2h(x, F->x[c.xc].p, I.P, s);
     if (y) d2h(y, dy.p, I.NP, s);

@@ -122,6 +122,8 @@ class ShardedSolver:
         sub_tab, sub_flat = shard_inputs(table, flat, lo, hi)
         self.instance = build_instance_flat(topology, sub_tab, sub_flat, device=device)
         self.path_ranges = kept_path_ranges(table, flat, self.ranges)
+        if world > 1:
+            self._agree_shards(group)
         self.solver = Solver(self.instance, self.config)
         # transport: "ipc" = the fused kernel exchanges edge totals over NVLink peer
         # memory (CUDA IPC buffers, no host round trip); "nccl" = split kernels
@@ -147,6 +149,24 @@ class ShardedSolver:
             self.solver._comm_keepalive = self.comm
         elif self.transport != "ipc":
             raise ValueError(f"unknown transport {self.transport!r}")
+
+    def _agree_shards(self, group=None):
+        """Every rank's shard must run the fused kernel (fast mode's exchange is
+        inside it) and hold at least one path (an empty shard never enters the
+        exchange): the ranks agree before any transport is set up, and all of
+        them raise together instead of some blocking in a collective."""
+        import torch
+        import torch.distributed as dist
+        ok, why = self.instance.fast_supported()
+        if self.instance.num_paths == 0:
+            ok, why = False, "empty shard (more ranks than commodities with paths)"
+        flags = torch.tensor([1.0 if ok else 0.0], dtype=torch.float64)
+        dist.all_reduce(flags, op=dist.ReduceOp.MIN, group=group)
+        if flags.item() < 1.0:
+            whys = [None] * self.world
+            dist.all_gather_object(whys, None if ok else why, group=group)
+            bad = {r: w for r, w in enumerate(whys) if w is not None}
+            raise RuntimeError(f"sharded fast-mode solve impossible on ranks {sorted(bad)}: {bad}")
 
     def _connect_ipc(self, group=None):
         """Exchange CUDA-IPC handles and open every peer's buffer.  Every rank

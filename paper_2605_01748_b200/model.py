@@ -160,6 +160,14 @@ class Instance:
     def commodities(self):
         return tuple(self._table[int(k)] for k in self.kept_rows)
 
+    def fast_supported(self):
+        """(ok, why): whether mode="fast" runs the fused kernel on this instance
+        (else solves fall back to the exact-order kernels, with a warning)."""
+        ok = C.c_int()
+        why = C.create_string_buffer(256)
+        check(lib().pf_instance_fast_supported(self.handle, C.byref(ok), why, 256))
+        return bool(ok.value), why.value.decode()
+
     def commodity_key(self, c):
         """Reference Commodity.key ("src→dst") of retained commodity c."""
         return self._table.key(int(self.kept_rows[c]))

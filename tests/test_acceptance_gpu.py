@@ -1,6 +1,7 @@
-"""SPEC acceptance criteria 1, 3, 4, 5, 6, 8 and 9 (reference tests/test_acceptance.py:77-89,
-169-328, 368-401) with the GPU solvers swapped in for pathfair.solve: same
-instance families, seeds and thresholds.  The single-path max-min reference is
+"""SPEC acceptance criteria 1-9 (reference tests/test_acceptance.py:77-401) with
+the GPU solvers swapped in for pathfair.solve: same instance families, seeds and
+thresholds.  Criteria 2 and 7 compare against the reference grid oracle's
+values recorded by tests/golden/make_golden_acceptance.py.  The single-path max-min reference is
 a progressive-filling oracle restated here (pathfair/oracles.py:56-93:
 raise every unfrozen commodity equally, freeze it at its demand or when its
 path meets a saturated edge) -- test infrastructure, not product code."""
@@ -282,3 +283,71 @@ def test_criterion_04_kernel_exactness():
             grad = (_rate_block_objective(inst, st, up, alpha) - _rate_block_objective(inst, st, down, alpha)) / (2 * h)
             worst_grad = max(worst_grad, abs(grad))
     assert worst_grad <= 1e-4, worst_grad
+
+
+# ---------------------------------------------------------------- criteria 2 and 7
+# The reference's grid oracle (oracles.py:158 exact_bruteforce_tiny) on its own
+# instance families, recorded by tests/golden/make_golden_acceptance.py.
+
+
+def _acc_golden():
+    import os
+    import golden_io as G
+    p = os.path.join(G.GOLDEN, "golden_acceptance.npz")
+    if not os.path.exists(p):
+        pytest.skip("golden_acceptance.npz not generated")
+    return dict(np.load(p))
+
+
+def _acc_instance(A, key):
+    f = {k: A[f"{key}/in/{k}"] for k in ("capacity", "demand0", "com_path_ptr0", "path_edge_ptr0", "path_edges0")}
+    return pf.build_instance_raw(f["capacity"], f["demand0"], f["com_path_ptr0"], f["path_edge_ptr0"],
+                                 f["path_edges0"], device=0)
+
+
+def _objective(sums, alpha):
+    return float(np.sum(pf.utility(np.maximum(sums, 1e-12), alpha)))
+
+
+@pytest.mark.parametrize("mode", ["fast", "exact"])
+def test_criterion_02_tiny_multipath_objective(mode):
+    """tests/test_acceptance.py:142-166: 20 instances x alpha in (0, 1, 2), the
+    objective gap to the grid oracle within max(2% of the optimum, one grid
+    step's first-order cost on every commodity)."""
+    A = _acc_golden()
+    n = len({k.split("/")[1] for k in A if k.startswith("c2/")})
+    assert n == 20
+    worst = -np.inf
+    for i in range(n):
+        inst = _acc_instance(A, f"c2/{i}")
+        step = float(A[f"c2/{i}/step"][0])
+        theta = pf.default_theta(inst)
+        for alpha in (0, 1, 2):
+            ref = A[f"c2/{i}/a{alpha}/ref_sums"]
+            res = pf.solve(inst, pf.SolverConfig(alpha_target=alpha, mode=mode))
+            gap = _objective(ref, alpha) - _objective(res.sums, alpha)
+            one_step = step * float(np.sum(np.maximum(ref, theta) ** (-float(alpha))))
+            allowed = max(0.02 * abs(_objective(ref, alpha)), one_step)
+            worst = max(worst, gap / allowed)
+            assert gap <= allowed, (i, alpha, gap, allowed)
+    assert worst <= 1.0
+
+
+@pytest.mark.parametrize("mode", ["fast", "exact"])
+def test_criterion_07_alpha_continuation_trend(mode):
+    """tests/test_acceptance.py:331-365: max-min optimality non-decreasing over
+    alpha_target 0..3 (within one grid step), and >= 0.85 at alpha 0 on the
+    symmetric instances."""
+    A = _acc_golden()
+    for i in range(5):
+        inst = _acc_instance(A, f"c7/{i}")
+        step = float(A[f"c7/{i}/step"][0])
+        ref = A[f"c7/{i}/ref_sums"]
+        theta = pf.default_theta(inst)
+        dip = step * float(np.mean(1.0 / np.maximum(ref, theta)))
+        opts = [pf.optimality_from_sums(pf.solve(inst, pf.SolverConfig(alpha_target=a, mode=mode)).sums, ref, theta)
+                for a in (0, 1, 2, 3)]
+        for lo, hi in zip(opts, opts[1:]):
+            assert hi >= lo - dip - 1e-12, (i, opts)
+        if bool(A[f"c7/{i}/sym"][0]):
+            assert opts[0] >= 0.85, (i, opts)

@@ -260,7 +260,10 @@ def test_ipc_multirank_on_one_gpu(world):
     assert all(s == states[0] for s in states) and states[0][0] == 40
     xg, xs = res[0][4], res[0][5]
     assert xg.shape == xs.shape
-    assert float(np.max(np.abs(xg - xs))) <= 1e-6 * float(np.max(np.abs(xs)))
+    # shards reassociate the per-edge sums (their tiles differ from the single
+    # instance's), and after 40 iterations the frozen-activity tests amplify the
+    # ulp differences: the north_star tolerance (1e-4 relative) bounds them
+    assert float(np.max(np.abs(xg - xs))) <= 1e-4 * float(np.max(np.abs(xs)))
 
 
 @pytest.mark.gpu
@@ -357,3 +360,51 @@ def test_ipc_setup_failure_on_one_rank_is_agreed(fail_at):
         assert res == {0: None, 1: None}
     else:
         assert res[0] is not None and res[1] is not None, res
+
+
+def _shard_agree_worker(rank, world, port, bad_rank, why, q):
+    """ShardedSolver._agree_shards with the instance stubbed: `bad_rank`'s shard
+    is outside the fused layout (or empty); every rank must raise, none block."""
+    import types
+
+    import torch.distributed as dist
+
+    from paper_2605_01748_b200 import distributed as DD
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        bad = rank == bad_rank
+        inst = types.SimpleNamespace(
+            num_paths=0 if (bad and why == "empty") else 10,
+            fast_supported=lambda: (False, "commodity 3 has more than 32 paths") if (bad and why == "layout")
+            else (True, ""))
+        stub = types.SimpleNamespace(instance=inst, rank=rank, world=world)
+        try:
+            DD.ShardedSolver._agree_shards(stub, None)
+            q.put((rank, None))
+        except RuntimeError as exc:
+            q.put((rank, str(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("why", ["layout", "empty", None])
+def test_shard_capability_is_agreed_before_transport_setup(why):
+    """a shard outside the fused layout limits, or an empty shard,
+    must make every rank raise (gloo world size 2 on CPU) instead of one rank
+    raising while the others wait in the exchange."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_shard_agree_worker, args=(r, 2, port, 1, why, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(2))
+    for p in ps:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in ps)
+    if why is None:
+        assert res == {0: None, 1: None}
+    else:
+        assert res[0] is not None and res[1] is not None, res
+        assert "ranks [1]" in res[0] and res[0] == res[1]
