@@ -231,6 +231,22 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // ------------------------------------------------------------------ TMA / mbarrier
 
 __device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// explicit shared-space accesses: tables reached through pointers that may also
+// point to global memory would otherwise compile to generic loads (LD.E), whose
+// latency the per-pair loops pay on every element
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double2 lds_f64x2(uint32_t a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_f64x2(uint32_t a, double2 v) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
 
 __device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(count) : "memory");
@@ -607,15 +623,17 @@ struct Acc {
     double2 *acc;      // per edge {T, L} in shared memory, or
     double *gT, *gL;   // this CTA's partials (large E): edge e at gT[e * gs]
     int gs;
+    uint32_t adj_s, acc_s;  // shared-space addresses of the tables (when in shared memory)
 };
 
 template <int MODE>
 __device__ __forceinline__ void acc_add(const Acc &A, int e, double T, double L) {
     if (A.acc) {
-        double2 v = A.acc[e];
+        const uint32_t a = A.acc_s + 16u * (uint32_t)e;
+        double2 v = lds_f64x2(a);
         v.x += T;
         if (MODE != MODE_RB) v.y += L;
-        A.acc[e] = v;
+        sts_f64x2(a, v);
     } else {  // L2-resident CTA-private rows (bypass L1: it holds the adjustment table)
         const size_t o = (size_t)e * A.gs;
         __stcg(&A.gT[o], __ldcg(&A.gT[o]) + T);
@@ -630,19 +648,23 @@ __device__ __forceinline__ void acc_add(const Acc &A, int e, double T, double L)
 // in registers (no per-pair path index, no shuffle, no per-path walk).
 //   y_j = max0(x + dcon_j - adj_e) (kernels.py:98-100), K = sum_j (y_j - dcon_j) in
 //   hop order (kernels.py:110-113)
-template <int MODE>
+template <int MODE, bool ADJ_L1>
 __device__ __forceinline__ double hops_y(int base, int h, int H, unsigned lt, double xl,
                                          const uint16_t *__restrict__ eid, const double *__restrict__ dcon,
-                                         const double *__restrict__ adj, bool adj_l1, double *__restrict__ ys) {
+                                         uint32_t adj_s, const double *__restrict__ adj_g, double *__restrict__ ys) {
+    // steps are branch-free (inactive lanes load a harmless in-stage slot and
+    // edge 0, and skip the store) so the unrolled steps' loads overlap
     double K = 0.0;
 #pragma unroll 4
     for (int j = 0; j < H; ++j) {
         const bool on = h > j;
         const unsigned act = __ballot_sync(FULL, on);
+        const int l = base + __popc(act & lt);
+        const double dv = dcon[l];
+        const int e = on ? (int)eid[l] : 0;
+        const double a = ADJ_L1 ? __ldca(&adj_g[e]) : lds_f64(adj_s + 8u * (uint32_t)e);
+        const double y = MODE == MODE_A1 ? xl : max0(xl + dv - a);
         if (on) {
-            const int l = base + __popc(act & lt);
-            const double dv = dcon[l];
-            const double y = MODE == MODE_A1 ? xl : max0(xl + dv - (adj_l1 ? __ldca(&adj[eid[l]]) : adj[eid[l]]));
             ys[l] = y;
             K += y - dv;
         }
@@ -661,10 +683,10 @@ __device__ __forceinline__ double hops_dcon(int base, int h, int H, unsigned lt,
     for (int j = 0; j < H; ++j) {
         const bool on = h > j;
         const unsigned act = __ballot_sync(FULL, on);
+        const int l = base + __popc(act & lt);
+        const double dks = dcon[l] * f;
+        const double dnew = max0(dks + xn - ys[l]);
         if (on) {
-            const int l = base + __popc(act & lt);
-            const double dks = dcon[l] * f;
-            const double dnew = max0(dks + xn - ys[l]);
             dco[l] = dnew;
             const double df = dnew - dks;
             r += df * df;
@@ -708,7 +730,12 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     // (1) pairs: y (kernels.py:98-100) and K_p (kernels.py:110-113) in the lane
     const double xlane = gp0 + lane < gp1 ? (MODE == MODE_RB ? st.xo[gp0 + lane] : st.xk[gp0 + lane]) : 0.0;
     double Kl = 0.0;
-    if (!(P.ablate & 64)) Kl = hops_y<MODE>(gbase, hl, H, lt, xlane, eid, dcon, A.adj, !P.adj_smem, ys);
+    if (!(P.ablate & 64)) {
+        if (P.adj_smem)
+            Kl = hops_y<MODE, false>(gbase, hl, H, lt, xlane, eid, dcon, A.adj_s, nullptr, ys);
+        else
+            Kl = hops_y<MODE, true>(gbase, hl, H, lt, xlane, eid, dcon, 0u, P.adj, ys);
+    }
     __syncwarp();
     TP(1)
     // (2) paths (lane = path) and commodities (lane segments)
@@ -928,6 +955,8 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
     A.gL = P.partL + g;
     A.gs = P.G;
     A.y = (double *)(base + sp.y);
+    A.adj_s = su32(base + sp.adj);
+    A.acc_s = su32(base + sp.acc);
     const int t0 = P.cta_ptr[g], my = P.cta_ptr[g + 1] - t0;
     const bool rev = (c.iteration & 1) != 0;
     auto tile_of = [&](int k) { return P.cta_tiles[t0 + (rev ? my - 1 - k : k)]; };
