@@ -85,14 +85,18 @@ constexpr int RUN_OCT = 8;    // runs of >= RUN_OCT pairs by 8 lanes; shorter on
 __host__ __device__ __forceinline__ int r16(int b) { return (b + 15) & ~15; }
 __host__ __device__ __forceinline__ int even(int n) { return (n + 1) & ~1; }
 
-// Byte offsets of the sections of one tile's metadata block.
+// Byte offsets of the sections of one tile's metadata block.  With run slots
+// (large-E layout) the per-pair u16 holds the pair's tile-local RUN (distinct
+// edge of the tile, in edge order) instead of its edge id, and two per-run
+// sections follow: the run's edge and its global slot (the edge-major position
+// of this (tile, run) among all tiles that touch the edge).
 struct MetaOff {
-    int eid, sperm, rstart, rord, poff, pcom, cpp, gpath, bytes;
+    int eid, sperm, rstart, rord, poff, pcom, cpp, gpath, redge, rdst, bytes;
 };
-__host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc, int nrun) {
+__host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc, int nrun, bool rs = false) {
     MetaOff m;
     int o = 0;
-    m.eid = o;  // u16 [np] edge id of each pair (hop-major within each group)
+    m.eid = o;  // u16 [np] edge id (run id with run slots) of each pair (hop-major within each group)
     o += r16(2 * np);
     m.sperm = o;  // u16 [np] tile-local pairs sorted by (edge, pair): the edge runs, back to back
     o += r16(2 * np);
@@ -108,23 +112,29 @@ __host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc, 
     o += r16(2 * (nc + 1));
     m.gpath = o;  // u16 [NW + 1] tile-local path offset of each group
     o += r16(2 * (NW + 1));
+    m.redge = o;  // run slots: u16 [nrun] edge of each run
+    if (rs) o += r16(2 * nrun);
+    m.rdst = o;  // run slots: u32 [nrun] global slot of each run's {T, L}
+    if (rs) o += r16(4 * nrun);
     m.bytes = o;
     return m;
 }
 
 // Dynamic shared memory: two stages + work arrays + the per-edge tables.
+// Run slots (rs): no per-edge tables; a per-tile adjustment table of the
+// tile's runs (at most rmax) instead.
 struct SmemPlan {
     int stage, s_dcon, s_meta, s_xk, s_xo, s_dn, s_D, s_dd;  // offsets inside a stage
-    int y, adj, acc, total;                                 // offsets from the base
+    int y, adj, acc, adjt, total;                           // offsets from the base
 };
 __host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E, int nbuf, bool adj_smem = true,
-                                                      bool acc_smem = true) {
+                                                      bool acc_smem = true, bool rs = false, int rmax = 0) {
     SmemPlan s;
     int o = 0;
     s.s_dcon = o;
     o += 8 * tps;
     s.s_meta = o;
-    o += meta_off(tps, TPATH, TCOM, tps < E ? tps : E).bytes;  // at most min(pairs, edges) runs
+    o += meta_off(tps, TPATH, TCOM, rs ? rmax : (tps < E ? tps : E), rs).bytes;  // at most min(pairs, edges) runs
     s.s_xk = o;
     o += 8 * (TPATH + 2);
     s.s_xo = o;
@@ -140,9 +150,11 @@ __host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E, int nbuf,
     s.y = o;
     o += 8 * tps;
     s.adj = o;  // per-edge adjustment table (absent for large E: read through L1)
-    if (adj_smem) o += r16(8 * E);
+    if (adj_smem && !rs) o += r16(8 * E);
     s.acc = o;  // double2 {T, L} per edge (absent for large E: the CTA's partial rows in L2)
-    if (acc_smem) o += r16(16 * E);
+    if (acc_smem && !rs) o += r16(16 * E);
+    s.adjt = o;  // run slots: adjustment of each of the tile's runs
+    if (rs) o += r16(8 * rmax);
     s.total = o;
     return s;
 }
@@ -151,6 +163,10 @@ struct TileLayout {
     int32_t ntiles = 0, tps = TPS_MIN, kspan = 1;
     bool adj_smem = true;  // false for large E: the adjustment table read through L1
     bool acc_smem = true;  // false for large E: run totals accumulate in the CTA's partial rows (L2)
+    bool run_slots = false;  // per-(tile, run) totals in edge-major global slots (any E: no per-edge tables)
+    int32_t rmax = 0;        // most runs in one tile
+    int64_t nruns = 0;       // run slots: total (tile, run) slots
+    DevBuf<int32_t> eoff;    // run slots: [E + 1] first slot of each edge
     int64_t nslots = 0, meta_bytes = 0;
     DevBuf<TileDesc> desc;      // per tile
     DevBuf<uint8_t> meta;       // per-tile metadata blocks
@@ -200,6 +216,11 @@ struct Params {
     int32_t adapt;
     int32_t probe;   // tuning only (PF_FAST_PROBE): iteration-phase times of CTA 0 into g_probe
     int32_t ablate;  // tuning only (PF_FAST_ABLATE): 1 skip y/paths/commodities/dcon, 2 skip the edge scan, 16 skip commodities, 32 skip K, 64 skip y
+    // run slots (TileLayout::run_slots): every (tile, run) stores its {T, L} into
+    // slots[2 * s], s in the edge's range eoff[e] .. eoff[e + 1] (tile order)
+    int32_t run_slots, rmax;
+    const int32_t *eoff;
+    double *slots;
 };
 
 // Iteration-phase probe (tuning only, PF_FAST_PROBE): %globaltimer deltas of
@@ -319,7 +340,7 @@ __device__ __forceinline__ void issue_tile(const Params &P, const PassIO &io, co
                                            const SmemPlan &sp, int b, uint64_t *bar) {
     char *s = base + b * sp.stage;
     const int npath = d.p1 - d.p0, nc = d.c1 - d.c0;
-    const MetaOff m = meta_off(d.np, npath, nc, d.nrun);
+    const MetaOff m = meta_off(d.np, npath, nc, d.nrun, P.run_slots);
     const int pa = d.p0 & ~1, npa = even(d.p1 - pa);
     const int ca = d.c0 & ~1, nca = even(d.c1 - ca);
     const uint32_t b_dcon = 8u * even(d.np), b_p = 8u * npa, b_c = 8u * nca;
@@ -484,6 +505,42 @@ __device__ __forceinline__ void warp_edge_sums(const double *pT, const double *p
     L = l;
 }
 
+// Run slots: the per-edge total of the (tile, run) slots eoff[e] .. eoff[e + 1]
+// by one warp: lane j sums slots j, j + 32, ... in slot (= tile) order, 8 slots
+// in flight per lane, then the same fixed shuffle tree; lane 0 holds the totals.
+__device__ __forceinline__ void warp_slot_sums(const double *slots, const int32_t *eoff, int e, int lane,
+                                               double &T, double &L) {
+    const int a = __ldg(&eoff[e]), b = __ldg(&eoff[e + 1]);
+    double t = 0.0, l = 0.0;
+    for (int s = a + lane; s < b; s += 32 * 8) {
+        double2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            v[u] = s + 32 * u < b ? __ldcg((const double2 *)slots + s + 32 * u) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (s + 32 * u < b) {
+                t += v[u].x;
+                l += v[u].y;
+            }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        t += __shfl_down_sync(FULL, t, o);
+        l += __shfl_down_sync(FULL, l, o);
+    }
+    T = t;
+    L = l;
+}
+
+// The rank-local per-edge totals {T, L} of the pass just completed, whichever
+// layout holds the partials (one warp; lane 0 holds the result)
+__device__ __forceinline__ void edge_totals(const Params &P, int e, int lane, double &T, double &L) {
+    if (P.run_slots)
+        warp_slot_sums(P.slots, P.eoff, e, lane, T, L);
+    else
+        warp_edge_sums(P.partT, P.partL, P.G, P.I.E, e, lane, T, L);
+}
+
 // Sum of the per-edge dual_capacity residuals by the whole CTA (NT threads):
 // thread i sums edges i, i + NT, ... in order, then a warp shuffle tree and the
 // warp sums in warp order.  Every thread returns the same value.
@@ -601,7 +658,7 @@ __device__ __noinline__ void edge_phase(const Params &P, double f) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int e = blockIdx.x + P.G * warp; e < I.E; e += P.G * (NT / 32)) {  // edges spread over all CTAs
         double T, L;
-        warp_edge_sums(P.partT, P.partL, P.G, I.E, e, lane, T, L);
+        edge_totals(P, e, lane, T, L);
         if (lane == 0) {
             const double cap = I.capacity[e];
             const double dold = __ldcg(&P.dc[e]) * f;
@@ -624,11 +681,20 @@ struct Acc {
     double *gT, *gL;   // this CTA's partials (large E): edge e at gT[e * gs]
     int gs;
     uint32_t adj_s, acc_s;  // shared-space addresses of the tables (when in shared memory)
+    double *adjt;           // run slots: the tile's per-run adjustment table
+    uint32_t adjt_s;
+    double *slots;          // run slots: the global {T, L} slots
 };
 
 template <int MODE>
-__device__ __forceinline__ void acc_add(const Acc &A, int e, double T, double L) {
-    if (A.acc) {
+__device__ __forceinline__ void acc_add(const Acc &A, const uint32_t *rdst, int e, double T, double L) {
+    if (rdst) {  // run slots: e is the tile-local run; one store, no read-modify-write
+        double *q = A.slots + 2 * (size_t)rdst[e];
+        if (MODE != MODE_RB)
+            __stcg((double2 *)q, make_double2(T, L));
+        else
+            __stcg(q, T);
+    } else if (A.acc) {
         const uint32_t a = A.acc_s + 16u * (uint32_t)e;
         double2 v = lds_f64x2(a);
         v.x += T;
@@ -706,8 +772,9 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
                                              double &r_dd, double &r_dcon, double &r_dn) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int np = d.np, npath = d.p1 - d.p0, nc = d.c1 - d.c0;
-    const MetaOff m = meta_off(np, npath, nc, d.nrun);
+    const MetaOff m = meta_off(np, npath, nc, d.nrun, P.run_slots);
     const uint16_t *eid = (const uint16_t *)(st.meta + m.eid);
+    const uint32_t *rdst = P.run_slots ? (const uint32_t *)(st.meta + m.rdst) : nullptr;
     const uint16_t *poff = (const uint16_t *)(st.meta + m.poff);
     const uint8_t *pcom = st.meta + m.pcom;
     const uint16_t *cpp = (const uint16_t *)(st.meta + m.cpp);
@@ -730,9 +797,15 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     // (1) pairs: y (kernels.py:98-100) and K_p (kernels.py:110-113) in the lane
     const double xlane = gp0 + lane < gp1 ? (MODE == MODE_RB ? st.xo[gp0 + lane] : st.xk[gp0 + lane]) : 0.0;
     double Kl = 0.0;
+    if (P.run_slots && MODE != MODE_A1) {  // the adjustment of each of the tile's runs (kernels.py:94-96)
+        const uint16_t *redge = (const uint16_t *)(st.meta + m.redge);
+        for (int r = threadIdx.x; r < d.nrun; r += NT) A.adjt[r] = __ldcg(&P.adj[redge[r]]);
+        __syncthreads();
+    }
     if (!(P.ablate & 64)) {
-        if (P.adj_smem)
-            Kl = hops_y<MODE, false>(gbase, hl, H, lt, xlane, eid, dcon, A.adj_s, nullptr, ys);
+        if (P.adj_smem || P.run_slots)
+            Kl = hops_y<MODE, false>(gbase, hl, H, lt, xlane, eid, dcon, P.run_slots ? A.adjt_s : A.adj_s, nullptr,
+                                     ys);
         else
             Kl = hops_y<MODE, true>(gbase, hl, H, lt, xlane, eid, dcon, 0u, P.adj, ys);
     }
@@ -851,7 +924,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
             T += __shfl_xor_sync(FULL, T, o);
             if (MODE != MODE_RB) L += __shfl_xor_sync(FULL, L, o);
         }
-        if (lane == 0) acc_add<MODE>(A, eid[sperm[a]], T, L);
+        if (lane == 0) acc_add<MODE>(A, rdst, eid[sperm[a]], T, L);
     }
     // medium runs: 8 lanes per run, four runs per warp at a time (run i on
     // warp i % NW: the longest medium runs spread over the warps)
@@ -867,7 +940,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
                 T += __shfl_xor_sync(gm, T, o);
                 if (MODE != MODE_RB) L += __shfl_xor_sync(gm, L, o);
             }
-            if (o8 == 0) acc_add<MODE>(A, eid[sperm[a]], T, L);
+            if (o8 == 0) acc_add<MODE>(A, rdst, eid[sperm[a]], T, L);
         }
     }
     TP(6)
@@ -877,7 +950,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
         const int a = rstart[r], b = rstart[r + 1];
         double T, L;
         run_sum(a, b, 1, T, L);
-        acc_add<MODE>(A, eid[sperm[a]], T, L);
+        acc_add<MODE>(A, rdst, eid[sperm[a]], T, L);
     }
     TP(4)
 }
@@ -947,7 +1020,7 @@ template <int MODE>
 __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *base, CtaShared &cs, uint32_t &seq) {
     const int g = blockIdx.x, tid = threadIdx.x;
     const int E = P.I.E;
-    const SmemPlan sp = smem_plan(P.tps, E, P.nbuf, P.adj_smem, P.acc_smem);
+    const SmemPlan sp = smem_plan(P.tps, E, P.nbuf, P.adj_smem, P.acc_smem, P.run_slots, P.rmax);
     Acc A;
     A.adj = P.adj_smem ? (double *)(base + sp.adj) : P.adj;
     A.acc = P.acc_smem ? (double2 *)(base + sp.acc) : nullptr;
@@ -957,6 +1030,9 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
     A.y = (double *)(base + sp.y);
     A.adj_s = su32(base + sp.adj);
     A.acc_s = su32(base + sp.acc);
+    A.adjt = (double *)(base + sp.adjt);
+    A.adjt_s = su32(base + sp.adjt);
+    A.slots = P.slots;
     const int t0 = P.cta_ptr[g], my = P.cta_ptr[g + 1] - t0;
     const bool rev = (c.iteration & 1) != 0;
     auto tile_of = [&](int k) { return P.cta_tiles[t0 + (rev ? my - 1 - k : k)]; };
@@ -979,7 +1055,7 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
     }
     if (!keep)
         for (int i = tid; i < my && i < DL; i += NT) cs.dl[i] = P.desc[tile_of(i)];  // visible after the barrier below
-    for (int e0 = tid; e0 < E; e0 += 4 * NT) {  // the adjustment loads of 4 edges in flight
+    for (int e0 = tid; e0 < E && !P.run_slots; e0 += 4 * NT) {  // the adjustment loads of 4 edges in flight
         double av[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -1002,7 +1078,7 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
     // without the shared table adj is read through L1 (ld.global.ca); it was
     // rewritten by the edge phase before the grid barrier: acquire at gpu scope
     // so no stale L1 line survives
-    if (!P.adj_smem) asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+    if (!P.adj_smem && !P.run_slots) asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
     __syncthreads();
     if (tid == 0 && !keep && my <= DL) cs.dl_rev = rev ? 1 : 0;  // every thread read dl_rev before the barrier
     const PassIO &io = cs.io;
@@ -1019,7 +1095,7 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
                 const TileDesc dn_ = desc_of(k + P.pf_dist);
                 prefetch_l2(io.dcon_in + dn_.sb, 8u * even(dn_.np));
                 prefetch_l2(P.meta + (size_t)dn_.mb16 * 16,
-                            (uint32_t)meta_off(dn_.np, dn_.p1 - dn_.p0, dn_.c1 - dn_.c0, dn_.nrun).bytes);
+                            (uint32_t)meta_off(dn_.np, dn_.p1 - dn_.p0, dn_.c1 - dn_.c0, dn_.nrun, P.run_slots).bytes);
             }
         }
 #ifdef PF_TPROBE
@@ -1109,7 +1185,7 @@ __device__ __noinline__ void xchg_phase(const Params &P, Ctrl &c, cg::grid_group
     bool wrote = false;  // this thread stored into peer memory
     for (int e = g + P.G * warp; e < I.E; e += P.G * (NT / 32)) {
         double T, L;
-        warp_edge_sums(P.partT, P.partL, P.G, I.E, e, lane, T, L);
+        edge_totals(P, e, lane, T, L);
         if (lane == 0) {
             wrote = true;
             for (int r = 0; r < P.nranks; ++r) {
@@ -1342,7 +1418,7 @@ __global__ void __launch_bounds__(NT) k_local_reduce(const __grid_constant__ Par
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int e = blockIdx.x + gridDim.x * warp; e < E; e += gridDim.x * (NT / 32)) {
         double T, L;
-        warp_edge_sums(P.partT, P.partL, P.G, E, e, lane, T, L);
+        edge_totals(P, e, lane, T, L);
         if (lane == 0) {
             P.tot[e] = T;
             P.tot[E + e] = L;
@@ -1516,7 +1592,20 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
             stat = std::max<int64_t>(stat, (int64_t)fa.sharedSizeBytes);
         }
         const int64_t budget = per_sm / 2 - reserved - stat;
-        if (smem_plan(1024, (int)I.E, 1).total > budget || getenv("PF_FAST_LARGE_E")) {
+        const bool large_e = smem_plan(1024, (int)I.E, 1).total > budget || getenv("PF_FAST_LARGE_E");
+        // run slots: default for large E (no per-edge shared-memory tables, so two
+        // CTAs per SM at any E); PF_FAST_RS=1 / 0 forces them on / off (tuning)
+        const char *rs_env = getenv("PF_FAST_RS");
+        L->run_slots = rs_env ? atoi(rs_env) != 0 : large_e;
+        if (L->run_slots) {
+            // the per-tile run tables are sized by the layout's most runs per tile
+            // (known after the build); half the tile's pairs bounds it for the search
+            L->adj_smem = L->acc_smem = false;
+            tps_min = TPS_CAP;
+            while (tps_min > 1024 &&
+                   smem_plan((int)tps_min, (int)I.E, 1, false, false, true, (int)tps_min / 2).total > budget)
+                tps_min -= 64;
+        } else if (large_e) {
             // large E: the shared-memory edge tables rule out two CTAs per SM; the
             // adjustment table is read through L1 (one CTA per SM, large tiles), or
             // the run totals also move to the CTA's private partial rows in L2
@@ -1602,7 +1691,7 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         for (int64_t gi = 0; gi < ng; gi = tile_end(gi, NW)) ++n0;
         int sms = 148;
         PF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, inst->device()));
-        const int64_t ctas = (int64_t)sms * (L->acc_smem ? 2 : 1);  // CTAs per SM of this layout
+        const int64_t ctas = (int64_t)sms * (L->acc_smem || L->run_slots ? 2 : 1);  // CTAs per SM of this layout
         // only with several tiles per CTA (measured: 500-node k=4, 13.2 -> 14 tiles
         // per CTA, 163.7 -> 161.4 us; config 2 unchanged; 1.6 -> 2 per CTA no gain)
         if (n0 >= 4 * ctas && !getenv("PF_FAST_NO_BALANCE")) target = (n0 + ctas - 1) / ctas * ctas;
@@ -1646,7 +1735,7 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
             tiles.push_back(d);
             tgroups.push_back(gb);
             slot += (d.np + SLOT_ALIGN - 1) / SLOT_ALIGN * SLOT_ALIGN;
-            mb += meta_off(d.np, d.p1 - d.p0, d.c1 - d.c0, d.nrun).bytes;
+            mb += meta_off(d.np, d.p1 - d.p0, d.c1 - d.c0, d.nrun, L->run_slots).bytes;
             require(slot < INT_MAX, "too many demand-path pairs for fast mode");
             gi = gj;
         }
@@ -1661,7 +1750,7 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
     for (int64_t ti = 0; ti < (int64_t)tiles.size(); ++ti) {
         const TileDesc &T = tiles[ti];
         const int np = T.np, npath = T.p1 - T.p0, nc = T.c1 - T.c0;
-        const MetaOff m = meta_off(np, npath, nc, T.nrun);
+        const MetaOff m = meta_off(np, npath, nc, T.nrun, L->run_slots);
         uint8_t *blk = meta.data() + (int64_t)T.mb16 * 16;
         uint16_t *eid = (uint16_t *)(blk + m.eid);
         std::vector<uint16_t> perm(np);
@@ -1701,6 +1790,12 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         }
         require(nr == T.nrun, "fast layout: run count mismatch");
         rstart[nr] = (uint16_t)np;
+        if (L->run_slots) {  // the run's edge; the per-pair u16 becomes the pair's run
+            uint16_t *redge = (uint16_t *)(blk + m.redge);
+            for (int r = 0; r < nr; ++r) redge[r] = eid[sperm[rstart[r]]];
+            for (int r = 0; r < nr; ++r)
+                for (int sl = rstart[r]; sl < rstart[r + 1]; ++sl) eid[sperm[sl]] = (uint16_t)r;
+        }
         for (int r = 0; r < nr; ++r) rord[r] = (uint16_t)r;
         std::stable_sort(rord, rord + nr, [&](uint16_t a, uint16_t b) {
             return rstart[a + 1] - rstart[a] > rstart[b + 1] - rstart[b];
@@ -1719,13 +1814,41 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         lcpp[nc] = (uint16_t)npath;
     }
     for (size_t ti = 0; ti < tiles.size(); ++ti) tiles[ti].nab = tiles_nab[ti];
+    if (L->run_slots) {
+        // edge-major slots: edge e's (tile, run) totals at eoff[e] .. eoff[e + 1] in
+        // tile order (the edge phase sums them in that order: deterministic)
+        std::vector<int32_t> eoff(I.E + 1, 0);
+        int64_t total = 0;
+        for (const TileDesc &T : tiles) {
+            const MetaOff m = meta_off(T.np, T.p1 - T.p0, T.c1 - T.c0, T.nrun, true);
+            const uint16_t *redge = (const uint16_t *)(meta.data() + (int64_t)T.mb16 * 16 + m.redge);
+            for (int r = 0; r < T.nrun; ++r) ++eoff[redge[r] + 1];
+            total += T.nrun;
+            L->rmax = std::max(L->rmax, T.nrun);
+        }
+        require(total < INT_MAX, "too many (tile, run) slots for fast mode");
+        for (int64_t e = 0; e < I.E; ++e) eoff[e + 1] += eoff[e];
+        std::vector<int32_t> cur(eoff.begin(), eoff.end() - 1);
+        for (const TileDesc &T : tiles) {
+            const MetaOff m = meta_off(T.np, T.p1 - T.p0, T.c1 - T.c0, T.nrun, true);
+            uint8_t *blk = meta.data() + (int64_t)T.mb16 * 16;
+            const uint16_t *redge = (const uint16_t *)(blk + m.redge);
+            uint32_t *rdst = (uint32_t *)(blk + m.rdst);
+            for (int r = 0; r < T.nrun; ++r) rdst[r] = (uint32_t)cur[redge[r]]++;
+        }
+        L->nruns = total;
+        L->eoff.alloc(I.E + 1);
+        h2d(L->eoff.p, eoff.data(), I.E + 1, s);
+    }
     // compulsory HBM bytes of one M pass: what the bulk copies read plus what the pass writes
     int64_t bytes = 0;
     for (const TileDesc &d : tiles) {
         const int npath = d.p1 - d.p0, nc = d.c1 - d.c0;
         const int npa = even(d.p1 - (d.p0 & ~1)), nca = even(d.c1 - (d.c0 & ~1));
-        bytes += 8LL * even(d.np) + meta_off(d.np, npath, nc, d.nrun).bytes + 16LL * npa + 16LL * nca;  // reads
+        bytes += 8LL * even(d.np) + meta_off(d.np, npath, nc, d.nrun, L->run_slots).bytes + 16LL * npa +
+                 16LL * nca;  // reads
         bytes += 8LL * d.np + 16LL * npath + 8LL * nc;                                            // writes
+        if (L->run_slots) bytes += 2 * 16LL * d.nrun;  // the run totals written, read back by the edge phase
     }
     L->bytes_per_pass = bytes;
     L->desc.alloc(tiles.size() ? tiles.size() : 1);
@@ -1746,7 +1869,7 @@ struct FastSolver {
     int G = 0, nbuf = 1;
     size_t smem = 0;
     DevBuf<double> dcon[2], dn[2], dd[2], x[2];
-    DevBuf<double> D, dc, adj, ne, tot, partT, partL, res, res_dc, root_sums;
+    DevBuf<double> D, dc, adj, ne, tot, partT, partL, res, res_dc, root_sums, slots;
     DevBuf<int32_t> err, cta_ptr, cta_tiles;
     DevBuf<Ctrl> ctrl;
     Params P{};
@@ -1835,7 +1958,9 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     }
     F->nbuf = 1;  // measured: a second stage costs an SM's second CTA, which hides more
     if (const char *v = getenv("PF_FAST_NBUF")) F->nbuf = std::max(1, std::min(2, atoi(v)));
-    F->smem = (size_t)smem_plan(F->L->tps, (int)I.E, F->nbuf, F->L->adj_smem, F->L->acc_smem).total;
+    F->smem = (size_t)smem_plan(F->L->tps, (int)I.E, F->nbuf, F->L->adj_smem, F->L->acc_smem, F->L->run_slots,
+                                F->L->rmax)
+                  .total;
     int dev = inst->device();
     const cudaDeviceProp &prop = device_props(dev);
     const size_t static_smem = sizeof(Ctrl) + sizeof(CtaShared) + 64;
@@ -1894,8 +2019,10 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
         h2d(F->cta_ptr.p, ptr.data(), G + 1, s);
         h2d(F->cta_tiles.p, flat.data(), flat.size(), s);
     }
-    F->partT.alloc((size_t)G * E);
-    F->partL.alloc((size_t)G * E);
+    const size_t npart = F->L->run_slots ? 1 : (size_t)G * E;  // run slots hold the partials instead
+    F->partT.alloc(npart);
+    F->partL.alloc(npart);
+    if (F->L->run_slots) F->slots.alloc(2 * (size_t)std::max<int64_t>(F->L->nruns, 1));
     F->res.alloc((size_t)G * 8);
     F->res_dc.alloc(E);
     F->err.alloc(2);
@@ -1937,6 +2064,10 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     P.tot = F->tot.p;
     P.partT = F->partT.p;
     P.partL = F->partL.p;
+    P.run_slots = F->L->run_slots ? 1 : 0;
+    P.rmax = F->L->rmax;
+    P.eoff = F->L->run_slots ? F->L->eoff.p : nullptr;
+    P.slots = F->L->run_slots ? F->slots.p : nullptr;
     P.res = F->res.p;
     P.res_dc = F->res_dc.p;
     P.root_sums = cfg.trace ? F->root_sums.p : nullptr;
