@@ -78,6 +78,7 @@ struct TileDesc {
     int32_t c0, c1, p0, p1, t0, np, sb, mb16;  // mb16: metadata offset / 16
     int32_t nrun;                              // edge runs: distinct edges of the tile's pairs
     int32_t nab;                               // runs summed by a warp (low 16 bits), by 8 lanes (high)
+    int32_t nhb;                               // entries of the hop-step table (sum over groups of hops + 1)
 };
 constexpr int RUN_WARP = 64;  // runs of >= RUN_WARP pairs are summed by a whole warp
 constexpr int RUN_OCT = 8;    // runs of >= RUN_OCT pairs by 8 lanes; shorter ones by one lane
@@ -91,9 +92,9 @@ __host__ __device__ __forceinline__ int even(int n) { return (n + 1) & ~1; }
 // sections follow: the run's edge and its global slot (the edge-major position
 // of this (tile, run) among all tiles that touch the edge).
 struct MetaOff {
-    int eid, sperm, rstart, rord, poff, pcom, cpp, gpath, redge, rdst, bytes;
+    int eid, sperm, rstart, rord, poff, pcom, cpp, gpath, hbo, hb, hperm, hinv, redge, rdst, bytes;
 };
-__host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc, int nrun, bool rs = false) {
+__host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc, int nrun, int nhb, bool rs = false) {
     MetaOff m;
     int o = 0;
     m.eid = o;  // u16 [np] edge id (run id with run slots) of each pair (hop-major within each group)
@@ -112,6 +113,17 @@ __host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc, 
     o += r16(2 * (nc + 1));
     m.gpath = o;  // u16 [NW + 1] tile-local path offset of each group
     o += r16(2 * (NW + 1));
+    // hop-major order: within a group the paths take the lanes by decreasing hop
+    // count (hop lanes), so the lanes active at step j are a prefix 0 .. n_j - 1
+    // and step j's pairs are hb[j] + lane, hb[j] .. hb[j + 1]
+    m.hbo = o;  // u16 [NW + 1] each group's first entry in hb
+    o += r16(2 * (NW + 1));
+    m.hb = o;  // u16 [nhb] per group: the tile-local start of each hop step, then the group's end
+    o += r16(2 * nhb);
+    m.hperm = o;  // u8 [npath] per group: the path (group-relative) of each hop lane
+    o += r16(npath);
+    m.hinv = o;  // u8 [npath] per group: the hop lane of each path
+    o += r16(npath);
     m.redge = o;  // run slots: u16 [nrun] edge of each run
     if (rs) o += r16(2 * nrun);
     m.rdst = o;  // run slots: u32 [nrun] global slot of each run's {T, L}
@@ -127,14 +139,14 @@ struct SmemPlan {
     int stage, s_dcon, s_meta, s_xk, s_xo, s_dn, s_D, s_dd;  // offsets inside a stage
     int y, adj, acc, adjt, total;                           // offsets from the base
 };
-__host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E, int nbuf, bool adj_smem = true,
+__host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E, int nbuf, int hbmax, bool adj_smem = true,
                                                       bool acc_smem = true, bool rs = false, int rmax = 0) {
     SmemPlan s;
     int o = 0;
     s.s_dcon = o;
     o += 8 * tps;
     s.s_meta = o;
-    o += meta_off(tps, TPATH, TCOM, rs ? rmax : (tps < E ? tps : E), rs).bytes;  // at most min(pairs, edges) runs
+    o += meta_off(tps, TPATH, TCOM, rs ? rmax : (tps < E ? tps : E), hbmax, rs).bytes;  // at most min(pairs, edges) runs
     s.s_xk = o;
     o += 8 * (TPATH + 2);
     s.s_xo = o;
@@ -165,6 +177,7 @@ struct TileLayout {
     bool acc_smem = true;  // false for large E: run totals accumulate in the CTA's partial rows (L2)
     bool run_slots = false;  // per-(tile, run) totals in edge-major global slots (any E: no per-edge tables)
     int32_t rmax = 0;        // most runs in one tile
+    int32_t hbmax = 0;       // hop-step table bound: NW * (most hops of a path + 1)
     int64_t nruns = 0;       // run slots: total (tile, run) slots
     DevBuf<int32_t> eoff;    // run slots: [E + 1] first slot of each edge
     int64_t nslots = 0, meta_bytes = 0;
@@ -219,6 +232,7 @@ struct Params {
     // run slots (TileLayout::run_slots): every (tile, run) stores its {T, L} into
     // slots[2 * s], s in the edge's range eoff[e] .. eoff[e + 1] (tile order)
     int32_t run_slots, rmax;
+    int32_t hbmax, pad1;  // most hop-step entries of one tile (the shared-memory metadata bound)
     const int32_t *eoff;
     double *slots;
 };
@@ -316,6 +330,7 @@ struct PassIO {
 
 // Stage pointers of one buffer.
 struct StageView {
+    int o_dcon, o_meta;  // byte offsets from the dynamic shared-memory base
     const double *dcon;
     const uint8_t *meta;
     const double *xk, *xo, *dn, *D, *dd;  // already shifted to the tile's first path / commodity
@@ -324,6 +339,8 @@ struct StageView {
 __device__ __forceinline__ StageView stage_view(char *base, const SmemPlan &sp, int b, const TileDesc &d) {
     char *s = base + b * sp.stage;
     StageView v;
+    v.o_dcon = b * sp.stage + sp.s_dcon;
+    v.o_meta = b * sp.stage + sp.s_meta;
     v.dcon = (double *)(s + sp.s_dcon);
     v.meta = (const uint8_t *)(s + sp.s_meta);
     v.xk = (const double *)(s + sp.s_xk) + (d.p0 & 1);
@@ -340,7 +357,7 @@ __device__ __forceinline__ void issue_tile(const Params &P, const PassIO &io, co
                                            const SmemPlan &sp, int b, uint64_t *bar) {
     char *s = base + b * sp.stage;
     const int npath = d.p1 - d.p0, nc = d.c1 - d.c0;
-    const MetaOff m = meta_off(d.np, npath, nc, d.nrun, P.run_slots);
+    const MetaOff m = meta_off(d.np, npath, nc, d.nrun, d.nhb, P.run_slots);
     const int pa = d.p0 & ~1, npa = even(d.p1 - pa);
     const int ca = d.c0 & ~1, nca = even(d.c1 - ca);
     const uint32_t b_dcon = 8u * even(d.np), b_p = 8u * npa, b_c = 8u * nca;
@@ -684,6 +701,7 @@ struct Acc {
     double *adjt;           // run slots: the tile's per-run adjustment table
     uint32_t adjt_s;
     double *slots;          // run slots: the global {T, L} slots
+    int o_y, o_adj, o_adjt; // byte offsets from the dynamic shared-memory base
 };
 
 template <int MODE>
@@ -707,58 +725,76 @@ __device__ __forceinline__ void acc_add(const Acc &A, const uint32_t *rdst, int 
     }
 }
 
-// Per-pair loops over one commodity group in its hop-major order: lane i holds
-// path gp0 + i (h hops); step j visits the j-th pair of every path longer than
-// j, the active lanes' pairs stored consecutively in lane order, so each step is
-// one contiguous, conflict-free row and the lane keeps its path's rate and K_p
-// in registers (no per-pair path index, no shuffle, no per-path walk).
+// The dynamic shared memory, addressed through the symbol so that the per-pair
+// loops compile to shared-space loads and stores (pointers handed through
+// structs or non-inlined calls degrade to generic accesses).
+extern __shared__ __align__(128) char g_smem[];
+
+// Per-pair loops over one commodity group in its hop-major order.  The group's
+// paths take the hop lanes by decreasing hop count, so the lanes active at step
+// j are a prefix 0 .. n_j - 1 and step j's pairs are hb[j] + lane: one
+// contiguous, conflict-free row per step, no per-step vote, no per-pair path
+// index, and each lane keeps its path's rate and K_p in registers.  Inactive
+// lanes read the step's first slot and store nothing (straight-line code, so
+// the unrolled steps' loads overlap).
 //   y_j = max0(x + dcon_j - adj_e) (kernels.py:98-100), K = sum_j (y_j - dcon_j) in
 //   hop order (kernels.py:110-113)
+// Offsets are bytes from the dynamic shared-memory base.
 template <int MODE, bool ADJ_L1>
-__device__ __forceinline__ double hops_y(int base, int h, int H, unsigned lt, double xl,
-                                         const uint16_t *__restrict__ eid, const double *__restrict__ dcon,
-                                         uint32_t adj_s, const double *__restrict__ adj_g, double *__restrict__ ys) {
-    // steps are branch-free (inactive lanes load a harmless in-stage slot and
-    // edge 0, and skip the store) so the unrolled steps' loads overlap
+__device__ __forceinline__ double hops_y(int hb_o, int H, int lane, double xl, int eid_o, int dcon_o, int adj_o,
+                                         const double *__restrict__ adj_g, int ys_o) {
+    const uint16_t *hb = (const uint16_t *)(g_smem + hb_o);
+    const uint16_t *eid = (const uint16_t *)(g_smem + eid_o);
+    const double *dcon = (const double *)(g_smem + dcon_o);
+    const double *adj = (const double *)(g_smem + adj_o);
+    double *ys = (double *)(g_smem + ys_o);
     double K = 0.0;
+    int b0 = hb[0];
 #pragma unroll 4
     for (int j = 0; j < H; ++j) {
-        const bool on = h > j;
-        const unsigned act = __ballot_sync(FULL, on);
-        const int l = base + __popc(act & lt);
+        const int b1 = hb[j + 1];
+        const bool on = lane < b1 - b0;
+        const int l = on ? b0 + lane : b0;
         const double dv = dcon[l];
-        const int e = on ? (int)eid[l] : 0;
-        const double a = ADJ_L1 ? __ldca(&adj_g[e]) : lds_f64(adj_s + 8u * (uint32_t)e);
-        const double y = MODE == MODE_A1 ? xl : max0(xl + dv - a);
-        if (on) {
-            ys[l] = y;
-            K += y - dv;
+        double y;
+        if (MODE == MODE_A1) {
+            y = xl;
+        } else {
+            const int e = eid[l];
+            const double a = ADJ_L1 ? __ldca(&adj_g[e]) : adj[e];
+            y = max0(xl + dv - a);
         }
-        base += __popc(act);
+        if (on) ys[l] = y;
+        K += on ? y - dv : 0.0;
+        b0 = b1;
     }
     return K;
 }
 
 // dual_consensus' (kernels.py:72) stored coalesced to global; T = x' + dcon'
-// (kernels.py:91) into tv
-__device__ __forceinline__ double hops_dcon(int base, int h, int H, unsigned lt, double xn, double f,
-                                            const double *__restrict__ dcon, const double *__restrict__ ys,
-                                            double *__restrict__ dco, double *__restrict__ tv) {
+// (kernels.py:91) into tv (tv aliases dcon on purpose: every step reads dcon[l]
+// before it writes tv[l], for its own row only)
+__device__ __forceinline__ double hops_dcon(int hb_o, int H, int lane, double xn, double f, int dcon_o, int ys_o,
+                                            double *__restrict__ dco) {
+    const uint16_t *hb = (const uint16_t *)(g_smem + hb_o);
+    double *dcon = (double *)(g_smem + dcon_o);
+    const double *ys = (const double *)(g_smem + ys_o);
     double r = 0.0;
+    int b0 = hb[0];
 #pragma unroll 4
     for (int j = 0; j < H; ++j) {
-        const bool on = h > j;
-        const unsigned act = __ballot_sync(FULL, on);
-        const int l = base + __popc(act & lt);
+        const int b1 = hb[j + 1];
+        const bool on = lane < b1 - b0;
+        const int l = on ? b0 + lane : b0;
         const double dks = dcon[l] * f;
         const double dnew = max0(dks + xn - ys[l]);
+        const double df = dnew - dks;
         if (on) {
             dco[l] = dnew;
-            const double df = dnew - dks;
-            r += df * df;
-            tv[l] = xn + dnew;
+            dcon[l] = xn + dnew;
         }
-        base += __popc(act);
+        r += on ? df * df : 0.0;
+        b0 = b1;
     }
     return r;
 }
@@ -772,7 +808,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
                                              double &r_dd, double &r_dcon, double &r_dn) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int np = d.np, npath = d.p1 - d.p0, nc = d.c1 - d.c0;
-    const MetaOff m = meta_off(np, npath, nc, d.nrun, P.run_slots);
+    const MetaOff m = meta_off(np, npath, nc, d.nrun, d.nhb, P.run_slots);
     const uint16_t *eid = (const uint16_t *)(st.meta + m.eid);
     const uint32_t *rdst = P.run_slots ? (const uint32_t *)(st.meta + m.rdst) : nullptr;
     const uint16_t *poff = (const uint16_t *)(st.meta + m.poff);
@@ -789,13 +825,17 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
 
     // ---- this warp's commodity group
     const int gp0 = gpath[w], gp1 = gpath[w + 1];
-    const int gbase = poff[gp0];  // the group's pairs: [gbase, poff[gp1]), hop-major
-    const unsigned lt = (1u << lane) - 1u;
     const int hl = gp0 + lane < gp1 ? poff[gp0 + lane + 1] - poff[gp0 + lane] : 0;  // this lane's path hops
-    const int H = __reduce_max_sync(FULL, (unsigned)hl);
+    // hop lanes: lane i runs path gp0 + hperm[gp0 + i] through the group's H hop steps
+    const uint16_t *hbo = (const uint16_t *)(st.meta + m.hbo);
+    const uint8_t *hperm = st.meta + m.hperm, *hinv = st.meta + m.hinv;
+    const int hb0 = hbo[w], H = hbo[w + 1] - hb0 - 1;
+    const int hb_o = st.o_meta + m.hb + 2 * hb0;
+    const bool hv = gp0 + lane < gp1;
+    const int ph = gp0 + (hv ? (int)hperm[gp0 + lane] : 0);
     if (!(P.ablate & 1)) {
-    // (1) pairs: y (kernels.py:98-100) and K_p (kernels.py:110-113) in the lane
-    const double xlane = gp0 + lane < gp1 ? (MODE == MODE_RB ? st.xo[gp0 + lane] : st.xk[gp0 + lane]) : 0.0;
+    // (1) pairs: y (kernels.py:98-100) and K_p (kernels.py:110-113) in the hop lane
+    const double xlane = hv ? (MODE == MODE_RB ? st.xo[ph] : st.xk[ph]) : 0.0;
     double Kl = 0.0;
     if (P.run_slots && MODE != MODE_A1) {  // the adjustment of each of the tile's runs (kernels.py:94-96)
         const uint16_t *redge = (const uint16_t *)(st.meta + m.redge);
@@ -804,12 +844,13 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     }
     if (!(P.ablate & 64)) {
         if (P.adj_smem || P.run_slots)
-            Kl = hops_y<MODE, false>(gbase, hl, H, lt, xlane, eid, dcon, P.run_slots ? A.adjt_s : A.adj_s, nullptr,
-                                     ys);
+            Kl = hops_y<MODE, false>(hb_o, H, lane, xlane, st.o_meta + m.eid, st.o_dcon,
+                                     P.run_slots ? A.o_adjt : A.o_adj, nullptr, A.o_y);
         else
-            Kl = hops_y<MODE, true>(gbase, hl, H, lt, xlane, eid, dcon, 0u, P.adj, ys);
+            Kl = hops_y<MODE, true>(hb_o, H, lane, xlane, st.o_meta + m.eid, st.o_dcon, 0, P.adj, A.o_y);
     }
-    __syncwarp();
+    // K_p from its hop lane to the path's lane (commodity order)
+    Kl = __shfl_sync(FULL, Kl, hv ? (int)hinv[gp0 + lane] : lane);
     TP(1)
     // (2) paths (lane = path) and commodities (lane segments)
     double xnew_lane = 0.0;  // x' of this lane's path
@@ -883,7 +924,8 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     // T = x' + dcon' (kernels.py:91) replaces the consumed dcon in the stage
     // (tv aliases dcon on purpose: every step reads dcon[l] before it writes
     // tv[l], for the same l only)
-    r_dcon += hops_dcon(gbase, hl, H, lt, xnew_lane, f, dcon, ys, io.dcon_out + d.sb, const_cast<double *>(dcon));
+    const double xh = __shfl_sync(FULL, xnew_lane, hv ? (int)hperm[gp0 + lane] : lane);  // back to the hop lane
+    r_dcon += hops_dcon(hb_o, H, lane, xh, f, st.o_dcon, A.o_y, io.dcon_out + d.sb);
     fence_proxy_async_shared();  // these generic writes precede the TMA that refills the stage
     __syncthreads();
     TP(3)
@@ -1020,7 +1062,7 @@ template <int MODE>
 __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *base, CtaShared &cs, uint32_t &seq) {
     const int g = blockIdx.x, tid = threadIdx.x;
     const int E = P.I.E;
-    const SmemPlan sp = smem_plan(P.tps, E, P.nbuf, P.adj_smem, P.acc_smem, P.run_slots, P.rmax);
+    const SmemPlan sp = smem_plan(P.tps, E, P.nbuf, P.hbmax, P.adj_smem, P.acc_smem, P.run_slots, P.rmax);
     Acc A;
     A.adj = P.adj_smem ? (double *)(base + sp.adj) : P.adj;
     A.acc = P.acc_smem ? (double2 *)(base + sp.acc) : nullptr;
@@ -1033,6 +1075,9 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
     A.adjt = (double *)(base + sp.adjt);
     A.adjt_s = su32(base + sp.adjt);
     A.slots = P.slots;
+    A.o_y = sp.y;
+    A.o_adj = sp.adj;
+    A.o_adjt = sp.adjt;
     const int t0 = P.cta_ptr[g], my = P.cta_ptr[g + 1] - t0;
     const bool rev = (c.iteration & 1) != 0;
     auto tile_of = [&](int k) { return P.cta_tiles[t0 + (rev ? my - 1 - k : k)]; };
@@ -1095,7 +1140,7 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
                 const TileDesc dn_ = desc_of(k + P.pf_dist);
                 prefetch_l2(io.dcon_in + dn_.sb, 8u * even(dn_.np));
                 prefetch_l2(P.meta + (size_t)dn_.mb16 * 16,
-                            (uint32_t)meta_off(dn_.np, dn_.p1 - dn_.p0, dn_.c1 - dn_.c0, dn_.nrun, P.run_slots).bytes);
+                            (uint32_t)meta_off(dn_.np, dn_.p1 - dn_.p0, dn_.c1 - dn_.c0, dn_.nrun, dn_.nhb, P.run_slots).bytes);
             }
         }
 #ifdef PF_TPROBE
@@ -1573,6 +1618,11 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
                                                   " paths per commodity (commodity " + std::to_string(c) + ")");
         max_com_pairs = std::max<int64_t>(max_com_pairs, pptr[cpp[c + 1]] - pptr[cpp[c]]);
     }
+    int64_t hmax = 0;  // most hops of one path
+    for (int64_t p = 0; p < I.P; ++p) hmax = std::max<int64_t>(hmax, pptr[p + 1] - pptr[p]);
+    require(hmax < 65535, "fast mode supports paths of at most 65534 hops");
+    const int hbmax = (int)(NW * (hmax + 1));
+    L->hbmax = hbmax;
     // largest tile (<= TPS_MIN pairs) that keeps two CTAs per SM with this
     // instance's per-edge tables; PF_FAST_TPS overrides (tuning)
     int64_t tps_min = TPS_MIN;
@@ -1592,7 +1642,7 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
             stat = std::max<int64_t>(stat, (int64_t)fa.sharedSizeBytes);
         }
         const int64_t budget = per_sm / 2 - reserved - stat;
-        const bool large_e = smem_plan(1024, (int)I.E, 1).total > budget || getenv("PF_FAST_LARGE_E");
+        const bool large_e = smem_plan(1024, (int)I.E, 1, hbmax).total > budget || getenv("PF_FAST_LARGE_E");
         // run slots: default for large E (no per-edge shared-memory tables, so two
         // CTAs per SM at any E); PF_FAST_RS=1 / 0 forces them on / off (tuning)
         const char *rs_env = getenv("PF_FAST_RS");
@@ -1603,7 +1653,7 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
             L->adj_smem = L->acc_smem = false;
             tps_min = TPS_CAP;
             while (tps_min > 1024 &&
-                   smem_plan((int)tps_min, (int)I.E, 1, false, false, true, (int)tps_min / 2).total > budget)
+                   smem_plan((int)tps_min, (int)I.E, 1, hbmax, false, false, true, (int)tps_min / 2).total > budget)
                 tps_min -= 64;
         } else if (large_e) {
             // large E: the shared-memory edge tables rule out two CTAs per SM; the
@@ -1618,11 +1668,11 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
             L->adj_smem = false;
             if (getenv("PF_FAST_ACC_L2")) {
                 L->acc_smem = false;
-                while (tps_min > 512 && smem_plan((int)tps_min, (int)I.E, 1, false, false).total > budget)
+                while (tps_min > 512 && smem_plan((int)tps_min, (int)I.E, 1, hbmax, false, false).total > budget)
                     tps_min -= 256;
             } else {
                 const int64_t budget1 = per_sm - reserved - stat;
-                while (tps_min > 512 && smem_plan((int)tps_min, (int)I.E, 1, false).total > budget1)
+                while (tps_min > 512 && smem_plan((int)tps_min, (int)I.E, 1, hbmax, false).total > budget1)
                     tps_min -= 256;
             }
         } else {
@@ -1630,7 +1680,7 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
             // the per-tile fixed costs (config 2: 2,560 pairs 307 us/iteration,
             // 2,816 pairs 302 us; one more pair-row and only one CTA fits)
             tps_min = TPS_CAP;
-            while (tps_min > 1024 && smem_plan((int)tps_min, (int)I.E, 1).total > budget) tps_min -= 64;
+            while (tps_min > 1024 && smem_plan((int)tps_min, (int)I.E, 1, hbmax).total > budget) tps_min -= 64;
         }
     }
     {  // small instances: smaller tiles so that the tiles fill the grid (per-tile latency
@@ -1727,6 +1777,12 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
             d.mb16 = (int32_t)(mb / 16);
             d.nrun = 0;
             d.nab = 0;
+            d.nhb = 0;
+            for (int k = 0; k < NW; ++k) {  // hop steps of each group + its end
+                int64_t H = 0;
+                for (int32_t p = cpp[gb[k]]; p < cpp[gb[k + 1]]; ++p) H = std::max<int64_t>(H, pptr[p + 1] - pptr[p]);
+                d.nhb += (int32_t)H + 1;
+            }
             for (int32_t t = d.t0; t < d.t0 + d.np; ++t)
                 if (emark[pedge[t]] != (int32_t)tiles.size()) {
                     emark[pedge[t]] = (int32_t)tiles.size();
@@ -1735,7 +1791,7 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
             tiles.push_back(d);
             tgroups.push_back(gb);
             slot += (d.np + SLOT_ALIGN - 1) / SLOT_ALIGN * SLOT_ALIGN;
-            mb += meta_off(d.np, d.p1 - d.p0, d.c1 - d.c0, d.nrun, L->run_slots).bytes;
+            mb += meta_off(d.np, d.p1 - d.p0, d.c1 - d.c0, d.nrun, d.nhb, L->run_slots).bytes;
             require(slot < INT_MAX, "too many demand-path pairs for fast mode");
             gi = gj;
         }
@@ -1750,7 +1806,7 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
     for (int64_t ti = 0; ti < (int64_t)tiles.size(); ++ti) {
         const TileDesc &T = tiles[ti];
         const int np = T.np, npath = T.p1 - T.p0, nc = T.c1 - T.c0;
-        const MetaOff m = meta_off(np, npath, nc, T.nrun, L->run_slots);
+        const MetaOff m = meta_off(np, npath, nc, T.nrun, T.nhb, L->run_slots);
         uint8_t *blk = meta.data() + (int64_t)T.mb16 * 16;
         uint16_t *eid = (uint16_t *)(blk + m.eid);
         std::vector<uint16_t> perm(np);
@@ -1761,21 +1817,45 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         for (int i = 0; i < npath; ++i) poff[i] = (uint16_t)(pptr[T.p0 + i] - T.t0);
         poff[npath] = (uint16_t)np;
         for (int k = 0; k <= NW; ++k) gpath[k] = (uint16_t)(cpp[tgroups[ti][k]] - T.p0);
-        // hop-major order within each group: step j holds the j-th pair of every
-        // path with more than j hops, in path order (the kernel's hops_y / hops_dcon)
+        // hop-major order within each group: the group's paths take the hop lanes
+        // by decreasing hop count (stable), and step j holds the j-th pair of
+        // every path with more than j hops, in hop-lane order (the kernel's
+        // hops_y / hops_dcon): the lanes active at step j are a prefix
+        uint16_t *hbo = (uint16_t *)(blk + m.hbo);
+        uint16_t *hb = (uint16_t *)(blk + m.hb);
+        uint8_t *hperm = blk + m.hperm;
+        uint8_t *hinv = blk + m.hinv;
+        int hbn = 0;
+        std::vector<int> ord;
         for (int k = 0; k < NW; ++k) {
-            int H = 0;
-            for (int i = gpath[k]; i < gpath[k + 1]; ++i) H = std::max(H, poff[i + 1] - poff[i]);
-            int pos = gpath[k] < npath ? poff[gpath[k]] : np;
-            for (int j = 0; j < H; ++j)
-                for (int i = gpath[k]; i < gpath[k + 1]; ++i)
-                    if (poff[i + 1] - poff[i] > j) {
-                        const int l = poff[i] + j;  // tile-local reference pair
-                        eid[pos] = (uint16_t)pedge[T.t0 + l];
-                        pair_slot[T.t0 + l] = T.sb + pos;
-                        ++pos;
-                    }
+            const int g0 = gpath[k], g1 = gpath[k + 1];
+            ord.clear();
+            for (int i = g0; i < g1; ++i) ord.push_back(i);
+            std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
+                return poff[a + 1] - poff[a] > poff[b + 1] - poff[b];
+            });
+            for (int i = 0; i < (int)ord.size(); ++i) {
+                hperm[g0 + i] = (uint8_t)(ord[i] - g0);
+                hinv[ord[i]] = (uint8_t)i;
+            }
+            const int H = ord.empty() ? 0 : poff[ord[0] + 1] - poff[ord[0]];
+            int pos = g0 < npath ? poff[g0] : np;
+            hbo[k] = (uint16_t)hbn;
+            hb[hbn++] = (uint16_t)pos;
+            for (int j = 0; j < H; ++j) {
+                for (int i = 0; i < (int)ord.size(); ++i) {
+                    const int pth = ord[i];
+                    if (poff[pth + 1] - poff[pth] <= j) break;  // a prefix of the hop lanes
+                    const int l = poff[pth] + j;              // tile-local reference pair
+                    eid[pos] = (uint16_t)pedge[T.t0 + l];
+                    pair_slot[T.t0 + l] = T.sb + pos;
+                    ++pos;
+                }
+                hb[hbn++] = (uint16_t)pos;
+            }
         }
+        hbo[NW] = (uint16_t)hbn;
+        require(hbn == T.nhb, "fast layout: hop-step count mismatch");
         for (int l = 0; l < np; ++l) perm[l] = (uint16_t)l;
         std::stable_sort(perm.begin(), perm.end(), [&](uint16_t a, uint16_t b) { return eid[a] < eid[b]; });
         // edge runs: sperm = pairs sorted by (edge, pair); rstart = run starts;
@@ -1820,7 +1900,7 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         std::vector<int32_t> eoff(I.E + 1, 0);
         int64_t total = 0;
         for (const TileDesc &T : tiles) {
-            const MetaOff m = meta_off(T.np, T.p1 - T.p0, T.c1 - T.c0, T.nrun, true);
+            const MetaOff m = meta_off(T.np, T.p1 - T.p0, T.c1 - T.c0, T.nrun, T.nhb, true);
             const uint16_t *redge = (const uint16_t *)(meta.data() + (int64_t)T.mb16 * 16 + m.redge);
             for (int r = 0; r < T.nrun; ++r) ++eoff[redge[r] + 1];
             total += T.nrun;
@@ -1830,7 +1910,7 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         for (int64_t e = 0; e < I.E; ++e) eoff[e + 1] += eoff[e];
         std::vector<int32_t> cur(eoff.begin(), eoff.end() - 1);
         for (const TileDesc &T : tiles) {
-            const MetaOff m = meta_off(T.np, T.p1 - T.p0, T.c1 - T.c0, T.nrun, true);
+            const MetaOff m = meta_off(T.np, T.p1 - T.p0, T.c1 - T.c0, T.nrun, T.nhb, true);
             uint8_t *blk = meta.data() + (int64_t)T.mb16 * 16;
             const uint16_t *redge = (const uint16_t *)(blk + m.redge);
             uint32_t *rdst = (uint32_t *)(blk + m.rdst);
@@ -1845,7 +1925,7 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
     for (const TileDesc &d : tiles) {
         const int npath = d.p1 - d.p0, nc = d.c1 - d.c0;
         const int npa = even(d.p1 - (d.p0 & ~1)), nca = even(d.c1 - (d.c0 & ~1));
-        bytes += 8LL * even(d.np) + meta_off(d.np, npath, nc, d.nrun, L->run_slots).bytes + 16LL * npa +
+        bytes += 8LL * even(d.np) + meta_off(d.np, npath, nc, d.nrun, d.nhb, L->run_slots).bytes + 16LL * npa +
                  16LL * nca;  // reads
         bytes += 8LL * d.np + 16LL * npath + 8LL * nc;                                            // writes
         if (L->run_slots) bytes += 2 * 16LL * d.nrun;  // the run totals written, read back by the edge phase
@@ -1958,7 +2038,7 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     }
     F->nbuf = 1;  // measured: a second stage costs an SM's second CTA, which hides more
     if (const char *v = getenv("PF_FAST_NBUF")) F->nbuf = std::max(1, std::min(2, atoi(v)));
-    F->smem = (size_t)smem_plan(F->L->tps, (int)I.E, F->nbuf, F->L->adj_smem, F->L->acc_smem, F->L->run_slots,
+    F->smem = (size_t)smem_plan(F->L->tps, (int)I.E, F->nbuf, F->L->hbmax, F->L->adj_smem, F->L->acc_smem, F->L->run_slots,
                                 F->L->rmax)
                   .total;
     int dev = inst->device();
@@ -2066,6 +2146,7 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     P.partL = F->partL.p;
     P.run_slots = F->L->run_slots ? 1 : 0;
     P.rmax = F->L->rmax;
+    P.hbmax = F->L->hbmax;
     P.eoff = F->L->run_slots ? F->L->eoff.p : nullptr;
     P.slots = F->L->run_slots ? F->slots.p : nullptr;
     P.res = F->res.p;
