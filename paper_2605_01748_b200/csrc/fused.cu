@@ -62,12 +62,16 @@ namespace pf {
 #ifndef PF_NW
 #define PF_NW 8
 #endif
+#ifndef PF_MINB
+#define PF_MINB 2  // resident CTAs per SM the fused kernels are register-bounded for
+#endif
 constexpr int NW = PF_NW;         // warps per CTA = commodity groups per tile
 constexpr int NT = 32 * NW;       // threads per CTA
 constexpr int GPATH = 32;         // max paths per group (one lane per path)
 constexpr int TPATH = NW * GPATH; // max paths per tile
 constexpr int TCOM = TPATH;       // max commodities per tile
 static_assert(TPATH <= 256, "tile-local path / commodity indices are u8");
+static_assert(3 * 8 * (TPATH + 2) >= NT * 17, "the edge-run head pieces reuse the stage's per-path arrays");
 constexpr int TPS_MIN = 2560;     // default max pairs per tile (large-E layouts)
 constexpr int TPS_CAP = 4096;     // upper bound of the shared-memory fit (two CTAs per SM)
 constexpr int SLOT_ALIGN = 16;    // tile start alignment in the per-pair arrays (128 B)
@@ -330,7 +334,7 @@ struct PassIO {
 
 // Stage pointers of one buffer.
 struct StageView {
-    int o_dcon, o_meta;  // byte offsets from the dynamic shared-memory base
+    int o_dcon, o_meta, o_xk;  // byte offsets from the dynamic shared-memory base
     const double *dcon;
     const uint8_t *meta;
     const double *xk, *xo, *dn, *D, *dd;  // already shifted to the tile's first path / commodity
@@ -341,6 +345,7 @@ __device__ __forceinline__ StageView stage_view(char *base, const SmemPlan &sp, 
     StageView v;
     v.o_dcon = b * sp.stage + sp.s_dcon;
     v.o_meta = b * sp.stage + sp.s_meta;
+    v.o_xk = b * sp.stage + sp.s_xk;
     v.dcon = (double *)(s + sp.s_dcon);
     v.meta = (const uint8_t *)(s + sp.s_meta);
     v.xk = (const double *)(s + sp.s_xk) + (d.p0 & 1);
@@ -809,14 +814,11 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int np = d.np, npath = d.p1 - d.p0, nc = d.c1 - d.c0;
     const MetaOff m = meta_off(np, npath, nc, d.nrun, d.nhb, P.run_slots);
-    const uint16_t *eid = (const uint16_t *)(st.meta + m.eid);
     const uint32_t *rdst = P.run_slots ? (const uint32_t *)(st.meta + m.rdst) : nullptr;
     const uint16_t *poff = (const uint16_t *)(st.meta + m.poff);
     const uint8_t *pcom = st.meta + m.pcom;
     const uint16_t *cpp = (const uint16_t *)(st.meta + m.cpp);
     const uint16_t *gpath = (const uint16_t *)(st.meta + m.gpath);
-    const double *dcon = st.dcon;
-    double *ys = A.y;
     TP_DECL
     TP(-1)
     const double f = io.f;
@@ -934,65 +936,82 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     if (P.ablate & 2) return;
     // (4) per-edge sums over the tile's edge runs: T = sum (x' + dcon')
     // (kernels.py:91) and L = sum y (kernels.py:210).  A run is the tile's pairs
-    // on one edge (sperm[rstart[r] .. rstart[r + 1]), in pair order).  Runs are
-    // taken in decreasing length (rord) in three classes -- a warp, 8 lanes or
-    // one lane per run -- so the longest run (a source's out-edge, ~160 pairs
-    // at config 2) is not one serial chain; each run is summed in a fixed order
-    // and added to the CTA accumulator of its edge by one lane.  Runs of one tile have
-    // distinct edges, so no two lanes touch the same accumulator, and tiles are
-    // separated by block barriers: deterministic without atomics.
-    const uint16_t *sperm = (const uint16_t *)(st.meta + m.sperm);
-    const uint16_t *rstart = (const uint16_t *)(st.meta + m.rstart);
-    const uint16_t *rord = (const uint16_t *)(st.meta + m.rord);
-    const double *tv = dcon;  // x' + dcon' per pair (written over dcon by step 3)
-    const int nA = d.nab & 0xffff, nAB = nA + (d.nab >> 16);
-    // one run's items a, a + stp, a + 2 stp, ... < b into T, L (in order)
-    auto run_sum = [&](int a, int b, int stp, double &T, double &L) {
-        T = 0.0;
-        L = 0.0;
-        for (int s = a; s < b; s += stp) {
-            const int u = sperm[s];
-            T += tv[u];
-            if (MODE != MODE_RB) L += ys[u];
-        }
-    };
-    // long runs: a whole warp per run, then a fixed shuffle tree
-    for (int i = w; i < nA; i += NW) {
-        const int r = rord[i];
-        const int a = rstart[r], b = rstart[r + 1];
-        double T, L;
-        run_sum(a + lane, b, 32, T, L);
-        for (int o = 16; o > 0; o >>= 1) {
-            T += __shfl_xor_sync(FULL, T, o);
-            if (MODE != MODE_RB) L += __shfl_xor_sync(FULL, L, o);
-        }
-        if (lane == 0) acc_add<MODE>(A, rdst, eid[sperm[a]], T, L);
-    }
-    // medium runs: 8 lanes per run, four runs per warp at a time (run i on
-    // warp i % NW: the longest medium runs spread over the warps)
+    // on one edge; sperm lists the tile's pairs sorted by (edge, pair), so the
+    // runs lie back to back.  Thread t sums the contiguous chunk
+    // [t * cs, (t + 1) * cs) of that order in sequence: a run that starts and
+    // ends inside the chunk goes straight to its edge accumulator; a chunk's
+    // head piece (the continuation of a run begun in an earlier chunk) is
+    // published, and after a barrier the thread where a crossing run begins adds
+    // the following chunks' head pieces in chunk order.  Every run is summed
+    // in a fixed order and added once by one thread; runs of one tile have
+    // distinct edges and tiles are separated by block barriers: deterministic
+    // without atomics, balanced by items rather than runs.
     {
-        const int o8 = lane & 7;
-        const unsigned gm = 0xffu << (lane & 24);
-        for (int i = nA + (lane >> 3) * NW + w; i < nAB; i += NW * 4) {
-            const int r = rord[i];
-            const int a = rstart[r], b = rstart[r + 1];
-            double T, L;
-            run_sum(a + o8, b, 8, T, L);
-            for (int o = 4; o > 0; o >>= 1) {
-                T += __shfl_xor_sync(gm, T, o);
-                if (MODE != MODE_RB) L += __shfl_xor_sync(gm, L, o);
+        const int tid = threadIdx.x;
+        const int so = st.o_meta + m.sperm;  // shared offsets
+        const uint16_t *sperm = (const uint16_t *)(g_smem + so);
+        const uint16_t *ed = (const uint16_t *)(g_smem + st.o_meta + m.eid);  // edge (run) of each pair
+        const double *tv = (const double *)(g_smem + st.o_dcon);             // x' + dcon' (step 3)
+        const double *yv = (const double *)(g_smem + A.o_y);
+        // head pieces: the stage's per-path arrays are dead once step 3 is done
+        double2 *hp = (double2 *)(g_smem + st.o_xk);
+        uint8_t *hf = (uint8_t *)(hp + NT);  // 0 none, 1 a head piece, 2 the whole chunk continues
+        const int cs = max((np + NT - 1) / NT, 4);  // small tiles: fewer, longer chunks (fewer crossings)
+        const int a0 = tid * cs, b0 = min(a0 + cs, np);
+        double T = 0.0, L = 0.0;
+        int cur = -1, flag = 0;
+        bool inside = false;  // the current piece started inside this chunk
+        if (a0 < b0) {
+            const int prev = a0 > 0 ? (int)ed[sperm[a0 - 1]] : -1;
+            cur = ed[sperm[a0]];
+            inside = cur != prev;
+#pragma unroll 4
+            for (int q = a0; q < b0; ++q) {
+                const int u = sperm[q];
+                const int e = ed[u];
+                const double t = tv[u];
+                const double yy = MODE != MODE_RB ? yv[u] : 0.0;
+                if (e != cur) {  // the piece of run `cur` ends here
+                    if (inside) {
+                        acc_add<MODE>(A, rdst, cur, T, L);
+                    } else {
+                        hp[tid] = make_double2(T, L);
+                        flag = 1;
+                    }
+                    cur = e;
+                    inside = true;
+                    T = 0.0;
+                    L = 0.0;
+                }
+                T += t;
+                if (MODE != MODE_RB) L += yy;
             }
-            if (o8 == 0) acc_add<MODE>(A, rdst, eid[sperm[a]], T, L);
+            const bool cont = b0 < np && (int)ed[sperm[b0]] == cur;
+            if (!cont) {
+                if (inside) {
+                    acc_add<MODE>(A, rdst, cur, T, L);
+                } else {
+                    hp[tid] = make_double2(T, L);
+                    flag = 1;
+                }
+                inside = false;  // nothing left to finish
+            } else if (!inside) {
+                hp[tid] = make_double2(T, L);  // the whole chunk lies inside one crossing run
+                flag = 2;
+            }
         }
-    }
-    TP(6)
-    // short runs: one lane per run
-    for (int i = nAB + lane * NW + w; i < d.nrun; i += NT) {
-        const int r = rord[i];
-        const int a = rstart[r], b = rstart[r + 1];
-        double T, L;
-        run_sum(a, b, 1, T, L);
-        acc_add<MODE>(A, rdst, eid[sperm[a]], T, L);
+        hf[tid] = (uint8_t)flag;
+        TP(6)
+        __syncthreads();
+        if (inside) {  // this chunk's tail begins a run that crosses into the next chunks
+            for (int k = tid + 1; k < NT; ++k) {
+                const double2 v = hp[k];
+                T += v.x;
+                L += v.y;
+                if (hf[k] != 2) break;
+            }
+            acc_add<MODE>(A, rdst, cur, T, L);
+        }
     }
     TP(4)
 }
@@ -1341,7 +1360,7 @@ __device__ void xchg_controller_eval(const Params &P, Ctrl &c) {
 // DIST: the multi-GPU variant with the in-kernel peer-memory exchange (a
 // separate instantiation keeps the single-GPU kernel's registers untouched)
 template <bool DIST>
-__global__ void __launch_bounds__(NT, 2) k_fused(const __grid_constant__ Params P) {
+__global__ void __launch_bounds__(NT, PF_MINB) k_fused(const __grid_constant__ Params P) {
     extern __shared__ __align__(128) char smem_raw[];
     __shared__ Ctrl c;
     __shared__ CtaShared cs;
@@ -1443,7 +1462,7 @@ __global__ void __launch_bounds__(NT, 2) k_fused(const __grid_constant__ Params 
 // the same branch and issue matching collectives.
 
 template <int MODE>
-__global__ void __launch_bounds__(NT, 2) k_pass(const __grid_constant__ Params P) {
+__global__ void __launch_bounds__(NT, PF_MINB) k_pass(const __grid_constant__ Params P) {
     extern __shared__ __align__(128) char smem_raw[];
     __shared__ Ctrl c;
     __shared__ CtaShared cs;
@@ -1641,19 +1660,22 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
             PF_CUDA(cudaFuncGetAttributes(&fa, k_pass<MODE_M>));
             stat = std::max<int64_t>(stat, (int64_t)fa.sharedSizeBytes);
         }
-        const int64_t budget = per_sm / 2 - reserved - stat;
-        const bool large_e = smem_plan(1024, (int)I.E, 1, hbmax).total > budget || getenv("PF_FAST_LARGE_E");
+        const int64_t budget = per_sm / PF_MINB - reserved - stat;
+        // large E: the per-edge tables leave room for no tile of 2,048 pairs
+        const bool large_e = smem_plan(2048, (int)I.E, 1, hbmax).total > budget || getenv("PF_FAST_LARGE_E");
         // run slots: default for large E (no per-edge shared-memory tables, so two
         // CTAs per SM at any E); PF_FAST_RS=1 / 0 forces them on / off (tuning)
         const char *rs_env = getenv("PF_FAST_RS");
         L->run_slots = rs_env ? atoi(rs_env) != 0 : large_e;
         if (L->run_slots) {
             // the per-tile run tables are sized by the layout's most runs per tile
-            // (known after the build); half the tile's pairs bounds it for the search
+            // (known after the build); a quarter of the tile's pairs for the search
+            // (config 2: 270 runs per 2,345-pair tile, config 3: 394 per 2,846)
             L->adj_smem = L->acc_smem = false;
             tps_min = TPS_CAP;
             while (tps_min > 1024 &&
-                   smem_plan((int)tps_min, (int)I.E, 1, hbmax, false, false, true, (int)tps_min / 2).total > budget)
+                   smem_plan((int)tps_min, (int)I.E, 1, hbmax, false, false, true,
+                             (int)std::min<int64_t>(I.E, tps_min / 4)).total > budget)
                 tps_min -= 64;
         } else if (large_e) {
             // large E: the shared-memory edge tables rule out two CTAs per SM; the
@@ -1741,7 +1763,7 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         for (int64_t gi = 0; gi < ng; gi = tile_end(gi, NW)) ++n0;
         int sms = 148;
         PF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, inst->device()));
-        const int64_t ctas = (int64_t)sms * (L->acc_smem || L->run_slots ? 2 : 1);  // CTAs per SM of this layout
+        const int64_t ctas = (int64_t)sms * (L->acc_smem || L->run_slots ? PF_MINB : 1);  // CTAs per SM of this layout
         // only with several tiles per CTA (measured: 500-node k=4, 13.2 -> 14 tiles
         // per CTA, 163.7 -> 161.4 us; config 2 unchanged; 1.6 -> 2 per CTA no gain)
         if (n0 >= 4 * ctas && !getenv("PF_FAST_NO_BALANCE")) target = (n0 + ctas - 1) / ctas * ctas;
@@ -1938,6 +1960,10 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
     h2d(L->meta.p, meta.data(), meta.size(), s);
     h2d(L->pair_slot.p, pair_slot.data(), I.NP, s);
     PF_CUDA(cudaStreamSynchronize(s));
+    if (getenv("PF_FAST_DEBUG"))
+        fprintf(stderr, "[fast layout] tps %d gmax %lld tiles %d run_slots %d rmax %d hbmax %d nruns %lld meta %lld B\n",
+                L->tps, (long long)gmax, L->ntiles, (int)L->run_slots, L->rmax, L->hbmax, (long long)L->nruns,
+                (long long)L->meta_bytes);
     L->h_desc = std::move(tiles);
     return L;
 }
@@ -2059,6 +2085,8 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
         per_sm = std::min(per_sm, per_sm_d);
     }
     require(per_sm >= 1, "fast kernel does not fit on an SM");
+    if (getenv("PF_FAST_DEBUG"))
+        fprintf(stderr, "[fast layout] dynamic smem %zu B per CTA, %d CTAs per SM\n", F->smem, per_sm);
     int G = prop.multiProcessorCount * per_sm;
     G = std::max(1, std::min(G, F->L->ntiles));
     F->G = G;

@@ -17,4 +17,4 @@ b0 = s.result().beta
 ms, per = s.time_loop(N)
 r = s.result()
 print(f"{name}: after {W}, {N} iterations {ms:.3f} ms, {per * 1e3:.1f} us/iter (beta {b0:g} -> {r.beta:g}, "
-      f"alpha {r.alpha})", flush=True)
+      f"alpha {r.alpha}; grid {s.kernel_stats()['grid']}, tiles {s.kernel_stats()['tiles']})", flush=True)
