@@ -81,11 +81,8 @@ constexpr unsigned FULL = 0xffffffffu;
 struct TileDesc {
     int32_t c0, c1, p0, p1, t0, np, sb, mb16;  // mb16: metadata offset / 16
     int32_t nrun;                              // edge runs: distinct edges of the tile's pairs
-    int32_t nab;                               // runs summed by a warp (low 16 bits), by 8 lanes (high)
     int32_t nhb;                               // entries of the hop-step table (sum over groups of hops + 1)
 };
-constexpr int RUN_WARP = 64;  // runs of >= RUN_WARP pairs are summed by a whole warp
-constexpr int RUN_OCT = 8;    // runs of >= RUN_OCT pairs by 8 lanes; shorter ones by one lane
 
 __host__ __device__ __forceinline__ int r16(int b) { return (b + 15) & ~15; }
 __host__ __device__ __forceinline__ int even(int n) { return (n + 1) & ~1; }
@@ -96,7 +93,7 @@ __host__ __device__ __forceinline__ int even(int n) { return (n + 1) & ~1; }
 // sections follow: the run's edge and its global slot (the edge-major position
 // of this (tile, run) among all tiles that touch the edge).
 struct MetaOff {
-    int eid, sperm, rstart, rord, poff, pcom, cpp, gpath, hbo, hb, hperm, hinv, redge, rdst, bytes;
+    int eid, sperm, poff, pcom, cpp, gpath, hbo, hb, hperm, hinv, redge, rdst, bytes;
 };
 __host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc, int nrun, int nhb, bool rs = false) {
     MetaOff m;
@@ -105,10 +102,6 @@ __host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc, 
     o += r16(2 * np);
     m.sperm = o;  // u16 [np] tile-local pairs sorted by (edge, pair): the edge runs, back to back
     o += r16(2 * np);
-    m.rstart = o;  // u16 [nrun + 1] start of each run in sperm (runs in edge order)
-    o += r16(2 * (nrun + 1));
-    m.rord = o;  // u16 [nrun] runs by decreasing length (work order: balanced over the warps)
-    o += r16(2 * nrun);
     m.poff = o;  // u16 [npath + 1] tile-local pair offset of each path
     o += r16(2 * (npath + 1));
     m.pcom = o;  // u8 [npath] tile-local commodity of each path
@@ -1798,7 +1791,6 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
             require(mb / 16 < INT_MAX, "fast-mode metadata exceeds 32 GB");
             d.mb16 = (int32_t)(mb / 16);
             d.nrun = 0;
-            d.nab = 0;
             d.nhb = 0;
             for (int k = 0; k < NW; ++k) {  // hop steps of each group + its end
                 int64_t H = 0;
@@ -1823,7 +1815,6 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
     L->meta_bytes = mb;
     std::vector<uint8_t> meta(mb ? mb : 16, 0);
     std::vector<int32_t> pair_slot(I.NP);
-    std::vector<int32_t> tiles_nab(tiles.size());
 #pragma omp parallel for schedule(dynamic, 16)
     for (int64_t ti = 0; ti < (int64_t)tiles.size(); ++ti) {
         const TileDesc &T = tiles[ti];
@@ -1880,42 +1871,28 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         require(hbn == T.nhb, "fast layout: hop-step count mismatch");
         for (int l = 0; l < np; ++l) perm[l] = (uint16_t)l;
         std::stable_sort(perm.begin(), perm.end(), [&](uint16_t a, uint16_t b) { return eid[a] < eid[b]; });
-        // edge runs: sperm = pairs sorted by (edge, pair); rstart = run starts;
-        // rord = runs by decreasing length (stable)
+        // edge runs: sperm = pairs sorted by (edge, pair), the runs back to back
         uint16_t *sperm = (uint16_t *)(blk + m.sperm);
-        uint16_t *rstart = (uint16_t *)(blk + m.rstart);
-        uint16_t *rord = (uint16_t *)(blk + m.rord);
-        int nr = 0;
+        std::vector<int> rstart;
         for (int sl = 0; sl < np; ++sl) {
             sperm[sl] = perm[sl];
-            if (sl == 0 || eid[perm[sl]] != eid[perm[sl - 1]]) rstart[nr++] = (uint16_t)sl;
+            if (sl == 0 || eid[perm[sl]] != eid[perm[sl - 1]]) rstart.push_back(sl);
         }
+        const int nr = (int)rstart.size();
         require(nr == T.nrun, "fast layout: run count mismatch");
-        rstart[nr] = (uint16_t)np;
+        rstart.push_back(np);
         if (L->run_slots) {  // the run's edge; the per-pair u16 becomes the pair's run
             uint16_t *redge = (uint16_t *)(blk + m.redge);
             for (int r = 0; r < nr; ++r) redge[r] = eid[sperm[rstart[r]]];
             for (int r = 0; r < nr; ++r)
                 for (int sl = rstart[r]; sl < rstart[r + 1]; ++sl) eid[sperm[sl]] = (uint16_t)r;
         }
-        for (int r = 0; r < nr; ++r) rord[r] = (uint16_t)r;
-        std::stable_sort(rord, rord + nr, [&](uint16_t a, uint16_t b) {
-            return rstart[a + 1] - rstart[a] > rstart[b + 1] - rstart[b];
-        });
-        int na = 0, nb = 0;
-        for (int r = 0; r < nr; ++r) {
-            const int len = rstart[rord[r] + 1] - rstart[rord[r]];
-            na += len >= RUN_WARP;
-            nb += len >= RUN_OCT && len < RUN_WARP;
-        }
-        tiles_nab[ti] = na | (nb << 16);
         for (int j = 0; j < nc; ++j) {
             lcpp[j] = (uint16_t)(cpp[T.c0 + j] - T.p0);
             for (int32_t p = cpp[T.c0 + j]; p < cpp[T.c0 + j + 1]; ++p) pcom[p - T.p0] = (uint8_t)j;
         }
         lcpp[nc] = (uint16_t)npath;
     }
-    for (size_t ti = 0; ti < tiles.size(); ++ti) tiles[ti].nab = tiles_nab[ti];
     if (L->run_slots) {
         // edge-major slots: edge e's (tile, run) totals at eoff[e] .. eoff[e + 1] in
         // tile order (the edge phase sums them in that order: deterministic)
