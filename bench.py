@@ -284,55 +284,37 @@ def time_to_quality(name, device=0, cpu=True, chunk=None):
     topo, tab, flat = build_inputs(name)
     inst = pf.build_instance_flat(topo, tab, flat, device=device)
     fp = oracle_fixed_point(name)
-    s = pf.Solver(inst, pf.SolverConfig(mode="fast", max_iterations=5000)).init()
-    s.run(5000)
-    r = s.result()
-    _, own = s.finish()
     theta = pf.default_theta(inst)
     if fp is not None:
         meta, opt = fp
         opt_kind = "reference algorithm's fixed point (exact-order oracle, tests/golden/golden_fixed_points.npz)"
+        own = None
     else:
+        s = pf.Solver(inst, pf.SolverConfig(mode="fast", max_iterations=5000)).init()
+        s.run(5000)
+        _, own = s.finish()
         meta, opt = None, own
         opt_kind = "fast solver's own end point (no oracle fixture for this instance)"
-
-    def quality(k):
-        q = pf.Solver(inst, pf.SolverConfig(mode="fast", max_iterations=5000)).init()
-        q.run(k)
-        _, sums = q.finish()
-        return pf.optimality_from_sums(sums, opt, theta)
-
-    n = int(r.iterations)
-    step = chunk or max(1, n // 40)
-    lo, hi = 0, None
-    probe = pf.Solver(inst, pf.SolverConfig(mode="fast", max_iterations=5000)).init()
-    k = 0
-    while k < n:
-        k2 = min(n, k + step)
-        probe.run(k2 - k)
-        k = k2
-        _, sums = probe.finish()
-        if pf.optimality_from_sums(sums, opt, theta) >= 0.99:
-            hi = k
-            break
-        lo = k
-    reached = hi is not None
-    if hi is None:
-        hi = n
-    while reached and hi - lo > 1:  # quality is monotone in practice; bisect inside the chunk
-        mid = (lo + hi) // 2
-        if quality(mid) >= 0.99:
-            hi = mid
-        else:
-            lo = mid
-    kstar = hi if reached else None
+    # k*: one pass on the device (sampled post-projection optimality, the crossing
+    # chunk replayed from a device snapshot; pf_solver_time_to_quality)
+    srch = pf.Solver(inst, pf.SolverConfig(mode="fast", max_iterations=5000)).init()
+    found = srch.time_to_quality(opt, 0.99, sample_every=chunk or 125)
+    kstar = found["k_star"]
+    srch.run(5000)  # on to the algorithm's own stop: its end point vs OPT_ref
+    r = srch.result()
+    _, end = srch.finish()
+    hi = kstar if kstar is not None else int(r.iterations)
     t = pf.Solver(inst, pf.SolverConfig(mode="fast", max_iterations=5000)).init()
     ms_loop, _ = t.time_loop(hi)
     t.finish()
     ms_proj = t.result().projection_ms
     out = {"config": name, "k_star": kstar, "opt_ref": opt_kind,
-           "end_optimality_vs_opt_ref": pf.optimality_from_sums(own, opt, theta),
-           "fast_stop": {"iterations": n, "alpha": int(r.alpha), "converged": bool(r.converged)},
+           "end_optimality_vs_opt_ref": pf.optimality_from_sums(end, opt, theta),
+           "fast_stop": {"iterations": int(r.iterations), "alpha": int(r.alpha), "converged": bool(r.converged)},
+           "k_star_search": {"how": "one device pass: optimality sampled every "
+                                    f"{chunk or 125} iterations, crossing chunk replayed from a device snapshot",
+                             "samples": len(found["samples"]), "loop_ms": found["loop_ms"],
+                             "quality_ms": found["quality_ms"]},
            "gpu_ms": ms_loop + ms_proj, "gpu_loop_ms": ms_loop, "gpu_projection_ms": ms_proj,
            "pairs": inst.num_pairs, "mode": "fast"}
     if meta is not None:

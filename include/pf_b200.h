@@ -203,6 +203,27 @@ int pf_solver_kernel_stats(pf_solver *s, int64_t *launches, int64_t *tiles, int6
 /* The IterationTrace rows recorded so far (controller.py:173-194): copies min(cap, total) rows,
  * *total = the number recorded (lets a caller size its buffer by the actual run, not max_iterations). */
 int pf_solver_trace(pf_solver *s, pf_trace_row *rows /*nullable when cap == 0*/, int64_t cap, int64_t *total);
+/* Time to quality, on the device in one pass (the optimality column of controller.py:173-194
+ * used as a stopping instrument): from the solver's current state, run until the
+ * first iteration k whose post-projection optimality_from_sums(S_k, reference_sums,
+ * default_theta) (oracles.py:51-53, 244-254) is >= target, or the controller stops / reaches
+ * max_iterations.  S_k = commodity sums of project(x_k, alpha_k) (the trace row's alpha).  The
+ * quality is sampled every `sample_every` iterations (a device projection, a device metric, one
+ * scalar read); the chunk where it first reaches the target is replayed from a device snapshot
+ * one iteration at a time, so k* is exact without re-solving from the start.  On return the
+ * solver stands at k* (or at the stop).  Fast mode, single GPU.  Each sample is a
+ * (iteration, optimality) pair, bitwise the trace row's optimality at that iteration. */
+typedef struct {
+    int64_t k_star;      /* -1: target not reached */
+    int64_t iterations;  /* the solver's iteration on return */
+    double quality;      /* optimality at k* (or at the last sample) */
+    double loop_ms;      /* device time of the iterations run (replays included) */
+    double quality_ms;   /* device time of the projections + metrics */
+    int64_t samples;     /* samples taken (may exceed sample_cap; min(cap, samples) are stored) */
+} pf_ttq_result;
+int pf_solver_time_to_quality(pf_solver *s, const double *reference_sums /*host C*/, double target,
+                              int64_t sample_every, pf_ttq_result *out, int64_t *sample_iteration /*nullable*/,
+                              double *sample_quality /*nullable*/, int64_t sample_cap);
 int pf_solver_destroy(pf_solver *s);
 
 /* ---- multi-GPU: one process per GPU, NCCL over NVLink (dlopen'ed libnccl) ---- */

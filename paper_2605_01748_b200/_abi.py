@@ -42,6 +42,11 @@ class Result(C.Structure):
                 ("projection_ms", f64), ("exact_fallback", i32), ("reserved", i32)]
 
 
+class TtqResult(C.Structure):
+    _fields_ = [("k_star", i64), ("iterations", i64), ("quality", f64), ("loop_ms", f64), ("quality_ms", f64),
+                ("samples", i64)]
+
+
 class Violation(C.Structure):
     _fields_ = [("n_violated", i64), ("negative_count", i64), ("worst_negative", f64),
                 ("pct_violated", f64), ("mean_relative_violation", f64)]
@@ -84,6 +89,7 @@ SIGNATURES = {
     "pf_solver_time_loop": (C.c_int, [vp, i64, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "pf_solver_kernel_stats": (C.c_int, [vp, i64p, i64p, i64p, i64p]),
     "pf_solver_trace": (C.c_int, [vp, vp, i64, i64p]),
+    "pf_solver_time_to_quality": (C.c_int, [vp, f64p, f64, i64, C.POINTER(TtqResult), i64p, f64p, i64]),
     "pf_solver_destroy": (C.c_int, [vp]),
     "pf_comm_unique_id": (C.c_int, [vp]),
     "pf_comm_create": (C.c_int, [C.c_int, C.c_int, vp, C.c_int, C.POINTER(vp)]),

@@ -284,6 +284,31 @@ class Solver:
         check(lib().pf_solver_trace(self._h, buf, total.value, C.byref(total)))
         return _trace_rows(buf, total.value)
 
+    def time_to_quality(self, reference_sums, target: float = 0.99, sample_every: int = 125,
+                        sample_cap: int = 100000) -> dict:
+        """From the current state, run to the first iteration k* whose
+        post-projection optimality_from_sums(S_k, reference_sums,
+        default_theta) >= target (the trace optimality column of
+        controller.py:173-194, oracles.py:244-254), in one pass on the device:
+        the quality is sampled every `sample_every` iterations and the crossing
+        chunk replayed from a device snapshot (pf_solver_time_to_quality).  The
+        solver stands at k* (or where the controller stopped) afterwards."""
+        ref = np.ascontiguousarray(reference_sums, dtype=np.float64)
+        if ref.shape != (self.instance.num_commodities,):
+            raise InputError("commodity sets differ between allocation and reference")
+        out = A.TtqResult()
+        it = np.zeros(sample_cap, np.int64)
+        q = np.zeros(sample_cap, np.float64)
+        rc = lib().pf_solver_time_to_quality(self._h, _p(ref), float(target), int(sample_every), C.byref(out),
+                                             it.ctypes.data_as(A.i64p), _p(q), int(sample_cap))
+        if rc != A.PF_OK:
+            r = self.result()
+            _raise(self.instance, rc, r.bad_commodity, r.iterations)
+        n = min(int(out.samples), sample_cap)
+        return {"k_star": int(out.k_star) if out.k_star >= 0 else None, "quality": float(out.quality),
+                "iterations": int(out.iterations), "loop_ms": float(out.loop_ms),
+                "quality_ms": float(out.quality_ms), "samples": list(zip(it[:n].tolist(), q[:n].tolist()))}
+
     def kernel_stats(self):
         vals = [C.c_int64() for _ in range(4)]
         check(lib().pf_solver_kernel_stats(self._h, *(C.byref(v) for v in vals)))

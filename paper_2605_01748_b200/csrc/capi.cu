@@ -1016,6 +1016,96 @@ int pf_solver_trace(pf_solver *S, pf_trace_row *rows, int64_t cap, int64_t *tota
     });
 }
 
+// pf_solver_time_to_quality: see include/pf_b200.h
+static void solver_time_to_quality(pf_solver *S, const double *ref, double target, int64_t every,
+                                   pf_ttq_result *out, int64_t *si, double *sq, int64_t cap) {
+    require(S->initialized, "solver not initialized");
+    require(S->fast != nullptr && S->comm == nullptr, "time_to_quality needs a single-GPU fast-mode solver");
+    require(every >= 1, "sample_every must be >= 1");
+    DeviceGuard g(S->inst->device());
+    const InstView I = S->inst->view();
+    cudaStream_t st = S->stream;
+    FastSolver *F = S->fast;
+    std::memset(out, 0, sizeof(*out));
+    out->k_star = -1;
+    out->quality = NAN;
+    if (S->P() == 0) return;
+    std::vector<double> dem(S->C());
+    d2h(dem.data(), S->inst->demand.p, S->C(), st);
+    PF_CUDA(cudaStreamSynchronize(st));
+    const double theta = default_theta(dem);
+    DevBuf<double> ref_d(S->C() + 1), q_d(1);
+    h2d(ref_d.p, ref, S->C(), st);
+    if (S->trace_proj.n < (size_t)S->P() + 1) S->trace_proj.alloc(S->P() + 1);
+    if (S->trace_sums.n < (size_t)S->C() + 1) S->trace_sums.alloc(S->C() + 1);
+    double *xcur = fast_scratch(F, 1);  // free until finish()
+    auto quality = [&](int64_t alpha) {
+        PF_CUDA(cudaEventRecord(S->ev0, st));
+        fast_copy_x(F, xcur, st);
+        project_device(S->inst, xcur, alpha, S->trace_proj.p, st, true);  // as the trace row (solver_trace_row)
+        exact_commodity_sums(I, S->trace_proj.p, S->trace_sums.p, st);
+        optimality_sum_dev(I, S->trace_sums.p, ref_d.p, theta, S->ts, q_d.p, st);
+        PF_CUDA(cudaEventRecord(S->ev1, st));
+        double h = 0.0;
+        d2h(&h, q_d.p, 1, st);
+        PF_CUDA(cudaStreamSynchronize(st));
+        float ms = 0.f;
+        PF_CUDA(cudaEventElapsedTime(&ms, S->ev0, S->ev1));
+        out->quality_ms += ms;
+        return S->C() ? h / (double)S->C() : 1.0;
+    };
+    auto record = [&](int64_t it, double q) {
+        if (out->samples < cap) {
+            if (si) si[out->samples] = it;
+            if (sq) sq[out->samples] = q;
+        }
+        ++out->samples;
+    };
+    auto run = [&](int64_t n) {
+        float ms = 0.f;
+        const int64_t k = fast_run(F, n, st, &ms);
+        out->loop_ms += ms;
+        S->loop_ms += ms;
+        return k;
+    };
+    for (;;) {
+        FastStatus fs = fast_status(F, st);
+        if (fs.stopped || fs.status || fs.iteration >= S->cfg.max_iterations) break;
+        const int64_t it0 = fs.iteration;
+        fast_snapshot(F, st);
+        const int64_t n = run(every);
+        if (n == 0) break;
+        fs = fast_status(F, st);
+        const double q = quality(fs.alpha_used);
+        record(fs.iteration, q);
+        out->quality = q;
+        if (q >= target) {  // the first crossing lies in (it0, it0 + n]: replay it one iteration at a time
+            fast_restore(F, st);
+            for (int64_t j = 1; j <= n; ++j) {
+                if (run(1) == 0) break;
+                const FastStatus fj = fast_status(F, st);
+                const double qj = j == n ? q : quality(fj.alpha_used);
+                if (j < n) record(fj.iteration, qj);
+                if (qj >= target) {
+                    out->k_star = fj.iteration;
+                    out->quality = qj;
+                    break;
+                }
+            }
+            break;
+        }
+    }
+    out->iterations = fast_status(F, st).iteration;
+}
+
+int pf_solver_time_to_quality(pf_solver *S, const double *ref, double target, int64_t every, pf_ttq_result *out,
+                              int64_t *si, double *sq, int64_t cap) {
+    return guard([&] {
+        require(S != nullptr && ref != nullptr && out != nullptr, "null argument");
+        solver_time_to_quality(S, ref, target, every, out, si, sq, cap);
+    });
+}
+
 int pf_solver_destroy(pf_solver *S) {
     return guard([&] { solver_destroy(S); });
 }

@@ -549,6 +549,16 @@ __global__ void __launch_bounds__(1024) k_np_sum(const double *a, int64_t n, dou
     if (threadIdx.x == 0) *out = r;
 }
 
+// oracles.py:244-254 per-commodity term min(S_c / max(OPT_c, theta), 1) (the
+// host metric's expressions: NaN becomes 1 as in min(v, 1) written v < 1 ? v : 1)
+__global__ void k_opt_ratio(int32_t C, const double *sums, const double *ref, double theta, double *r) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    const double den = ref[c] > theta ? ref[c] : theta;
+    const double v = sums[c] / den;
+    r[c] = v < 1.0 ? v : 1.0;
+}
+
 // kernels.py:47-66 utility of max(S, 1e-12) (controller.py:175)
 __global__ void k_utility(int32_t C, const double *sums, int64_t alpha, double *u) {
     int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -818,6 +828,20 @@ void trace_stats(const InstView &I, const double *x, const double *root_sums, in
     host_out4[1] = rep.pct_violated;
     host_out4[2] = rep.mean_relative_violation;
     host_out4[3] = (double)rep.n_violated;
+}
+
+// optimality_from_sums' numerator on the device: the numpy pairwise sum of the
+// per-commodity terms into *d_sum (the mean divides by C on the host)
+void optimality_sum_dev(const InstView &I, const double *sums, const double *ref, double theta, TraceScratch &ts,
+                        double *d_sum, cudaStream_t s) {
+    ensure_trace_scratch(I, ts);
+    if (!I.C) {
+        PF_CUDA(cudaMemsetAsync(d_sum, 0, sizeof(double), s));
+        return;
+    }
+    k_opt_ratio<<<ceil_div(I.C, TB), TB, 0, s>>>(I.C, sums, ref, theta, ts.tmp.p);
+    k_np_sum<<<1, 1024, 0, s>>>(ts.tmp.p, I.C, d_sum, ts.leaf_lo.p, ts.leaf_sum.p);
+    PF_CHECK_LAUNCH();
 }
 
 // trace_stats without a host round trip (traced fast runs): row[0] objective,

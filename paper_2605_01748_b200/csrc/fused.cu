@@ -1971,6 +1971,7 @@ struct FastSolver {
     DevBuf<unsigned long long> xepoch;       // exchanges done
     // per-solve scratch kept with the (pooled) solver: warm-start staging, outputs
     DevBuf<double> x0stage, rates_out, sums_out, flag;
+    DevBuf<char> snap;  // fast_snapshot's copy of the dynamic state
 };
 
 static void fast_set_config(FastSolver *F, const pf_config &cfg) {
@@ -2343,6 +2344,44 @@ static int64_t fast_run_dist(FastSolver *F, int64_t max_steps, cudaStream_t s, f
     if (ms) *ms = t;
     c = read();
     return c.iteration - start;
+}
+
+// The buffers a launch reads and writes (both halves of the double buffers).
+static std::vector<std::pair<void *, size_t>> fast_state_bufs(FastSolver *F) {
+    std::vector<std::pair<void *, size_t>> v;
+    for (int b = 0; b < 2; ++b) {
+        v.push_back({F->dcon[b].p, F->dcon[b].bytes()});
+        v.push_back({F->dn[b].p, F->dn[b].bytes()});
+        v.push_back({F->dd[b].p, F->dd[b].bytes()});
+        v.push_back({F->x[b].p, F->x[b].bytes()});
+    }
+    for (DevBuf<double> *d : {&F->dc, &F->adj, &F->partT, &F->partL, &F->slots, &F->res, &F->res_dc})
+        if (d->p) v.push_back({d->p, d->bytes()});
+    v.push_back({F->err.p, F->err.bytes()});
+    v.push_back({F->ctrl.p, F->ctrl.bytes()});
+    return v;
+}
+
+void fast_snapshot(FastSolver *F, cudaStream_t s) {
+    require(F->nranks == 0 && F->comm == nullptr, "snapshots are single-GPU");
+    const auto bufs = fast_state_bufs(F);
+    size_t total = 0;
+    for (const auto &b : bufs) total += (b.second + 255) & ~(size_t)255;
+    if (F->snap.n < total) F->snap.alloc(total);
+    size_t o = 0;
+    for (const auto &b : bufs) {
+        PF_CUDA(cudaMemcpyAsync(F->snap.p + o, b.first, b.second, cudaMemcpyDeviceToDevice, s));
+        o += (b.second + 255) & ~(size_t)255;
+    }
+}
+
+void fast_restore(FastSolver *F, cudaStream_t s) {
+    require(F->snap.p != nullptr, "no snapshot to restore");
+    size_t o = 0;
+    for (const auto &b : fast_state_bufs(F)) {
+        PF_CUDA(cudaMemcpyAsync(b.first, F->snap.p + o, b.second, cudaMemcpyDeviceToDevice, s));
+        o += (b.second + 255) & ~(size_t)255;
+    }
 }
 
 void fast_init(FastSolver *F, const double *d_x0, int64_t alpha0, double beta0, cudaStream_t s) {

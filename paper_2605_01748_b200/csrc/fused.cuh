@@ -48,6 +48,11 @@ const double *fast_root_sums(FastSolver *f);
 void fast_export_state(FastSolver *f, double *x, double *y, double *dd, double *dc, double *dcon, double *dn,
                        cudaStream_t s);
 void fast_stats(FastSolver *f, int64_t *launches, int64_t *tiles, int64_t *grid, int64_t *bytes_per_iter);
+// A device copy of every buffer the next launch reads (iterates, duals, edge
+// partials, controller): restoring it makes the following iterations bitwise
+// those that followed the snapshot (every reduction has a fixed order).
+void fast_snapshot(FastSolver *f, cudaStream_t s);
+void fast_restore(FastSolver *f, cudaStream_t s);
 
 // Multi-GPU hooks (dist.cu): reduce edge partial vectors / residual scalars across ranks.
 struct CommOps {

@@ -271,6 +271,8 @@ void trace_stats(const InstView &I, const double *x, const double *root_sums, in
                  double tol, double *host_out4, cudaStream_t s);
 void trace_stats_dev(const InstView &I, const double *x, const double *root_sums, const int64_t *d_alpha,
                      TraceScratch &ts, double tol, double *row4, cudaStream_t s);
+void optimality_sum_dev(const InstView &I, const double *sums, const double *ref, double theta, TraceScratch &ts,
+                        double *d_sum, cudaStream_t s);
 void violation_stats(const InstView &I, const double *x, double tol, double *d_overload, double *d_excess,
                      TraceScratch &ts, pf_violation *rep, cudaStream_t s);
 

@@ -163,3 +163,35 @@ def test_cfg3_sample_incidence_and_fused_iterations():
             assert np.array_equal(want, getattr(o, fb)), (it, fa_)  # exact == oracle, bitwise
             scale = max(float(np.max(np.abs(want))), xs)
             assert float(np.max(np.abs(got - want))) <= 1e-9 * scale, (it, fa_)
+
+
+@pytest.mark.parametrize("name", ["cfg1_v0.3", "target_k4_v0.3"])
+def test_time_to_quality_one_device_pass(name):
+    """f3: k* found in one device pass (sampled post-projection optimality,
+    crossing chunk replayed from a snapshot) equals the first traced row whose
+    optimality column (controller.py:176-183, one projection per row) reaches
+    0.99; every sample is bitwise that row's optimality; the solver stands
+    bitwise where a fresh solver run to k* stands."""
+    meta, arrs = _fixed_points()
+    if name not in meta:
+        pytest.skip(f"{name} not in golden_fixed_points")
+    m = meta[name]
+    inst, _ = _build(*INSTANCES[name])
+    opt = arrs[f"{name}/opt_sums"]
+    dev = pf.Solver(inst, pf.SolverConfig(mode="fast", max_iterations=5000)).init()
+    found = dev.time_to_quality(opt, 0.99, sample_every=64)
+    k = found["k_star"]
+    assert k is not None and abs(k - m["k_star"]) <= 0.02 * m["k_star"], (k, m["k_star"])
+    assert dev.result().iterations == k
+    # the per-row instrument (a projection and the metric per traced row)
+    tr2 = pf.Solver(inst, pf.SolverConfig(mode="fast", max_iterations=5000, trace=True, reference_sums=opt)).init()
+    tr2.run(k)
+    rows = {r.iteration: r.optimality for r in tr2.trace()}
+    first = min(i for i, q in rows.items() if q >= 0.99)
+    assert first == k
+    for it, q in found["samples"]:
+        if it in rows:
+            assert q == rows[it], (it, q, rows[it])
+    ref = pf.Solver(inst, pf.SolverConfig(mode="fast", max_iterations=5000)).init()
+    ref.run(k)
+    assert np.array_equal(ref.x(), dev.x())
