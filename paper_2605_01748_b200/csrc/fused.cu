@@ -350,12 +350,12 @@ __device__ __forceinline__ StageView stage_view(char *base, const SmemPlan &sp, 
 }
 
 // One elected thread: bulk copies of a tile's inputs into stage b.
-template <int MODE>
+template <int MODE, bool RS>
 __device__ __forceinline__ void issue_tile(const Params &P, const PassIO &io, const TileDesc &d, char *base,
                                            const SmemPlan &sp, int b, uint64_t *bar) {
     char *s = base + b * sp.stage;
     const int npath = d.p1 - d.p0, nc = d.c1 - d.c0;
-    const MetaOff m = meta_off(d.np, npath, nc, d.nrun, d.nhb, P.run_slots);
+    const MetaOff m = meta_off(d.np, npath, nc, d.nrun, d.nhb, RS);
     const int pa = d.p0 & ~1, npa = even(d.p1 - pa);
     const int ca = d.c0 & ~1, nca = even(d.c1 - ca);
     const uint32_t b_dcon = 8u * even(d.np), b_p = 8u * npa, b_c = 8u * nca;
@@ -702,9 +702,9 @@ struct Acc {
     int o_y, o_adj, o_adjt; // byte offsets from the dynamic shared-memory base
 };
 
-template <int MODE>
+template <int MODE, bool RS>
 __device__ __forceinline__ void acc_add(const Acc &A, const uint32_t *rdst, int e, double T, double L) {
-    if (rdst) {  // run slots: e is the tile-local run; one store, no read-modify-write
+    if (RS) {  // run slots: e is the tile-local run; one store, no read-modify-write
         double *q = A.slots + 2 * (size_t)rdst[e];
         if (MODE != MODE_RB)
             __stcg((double2 *)q, make_double2(T, L));
@@ -800,14 +800,14 @@ __device__ __forceinline__ double hops_dcon(int hb_o, int H, int lane, double xn
 // MODE_M : B(k+1) [y, K/w, roots, x_{k+1}] fused with A(k+2) [duals_{k+2}, T/L]
 // MODE_RB: A(k+2) only, recomputing y_{k+1} from x_k, dcon_{k+1}, adj_{k+1}
 // MODE_A1: A(1) with y_0 = x_0[pair_path] (controller.py:118)
-template <int MODE>
+template <int MODE, bool RS>
 __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, const PassIO &io, const TileDesc &d,
                                              const StageView &st, const Acc &A, double &r_x,
                                              double &r_dd, double &r_dcon, double &r_dn) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int np = d.np, npath = d.p1 - d.p0, nc = d.c1 - d.c0;
-    const MetaOff m = meta_off(np, npath, nc, d.nrun, d.nhb, P.run_slots);
-    const uint32_t *rdst = P.run_slots ? (const uint32_t *)(st.meta + m.rdst) : nullptr;
+    const MetaOff m = meta_off(np, npath, nc, d.nrun, d.nhb, RS);
+    const uint32_t *rdst = RS ? (const uint32_t *)(st.meta + m.rdst) : nullptr;
     const uint16_t *poff = (const uint16_t *)(st.meta + m.poff);
     const uint8_t *pcom = st.meta + m.pcom;
     const uint16_t *cpp = (const uint16_t *)(st.meta + m.cpp);
@@ -832,15 +832,15 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     // (1) pairs: y (kernels.py:98-100) and K_p (kernels.py:110-113) in the hop lane
     const double xlane = hv ? (MODE == MODE_RB ? st.xo[ph] : st.xk[ph]) : 0.0;
     double Kl = 0.0;
-    if (P.run_slots && MODE != MODE_A1) {  // the adjustment of each of the tile's runs (kernels.py:94-96)
+    if (RS && MODE != MODE_A1) {  // the adjustment of each of the tile's runs (kernels.py:94-96)
         const uint16_t *redge = (const uint16_t *)(st.meta + m.redge);
         for (int r = threadIdx.x; r < d.nrun; r += NT) A.adjt[r] = __ldcg(&P.adj[redge[r]]);
         __syncthreads();
     }
     if (!(P.ablate & 64)) {
-        if (P.adj_smem || P.run_slots)
-            Kl = hops_y<MODE, false>(hb_o, H, lane, xlane, st.o_meta + m.eid, st.o_dcon,
-                                     P.run_slots ? A.o_adjt : A.o_adj, nullptr, A.o_y);
+        if (RS || P.adj_smem)
+            Kl = hops_y<MODE, false>(hb_o, H, lane, xlane, st.o_meta + m.eid, st.o_dcon, RS ? A.o_adjt : A.o_adj,
+                                     nullptr, A.o_y);
         else
             Kl = hops_y<MODE, true>(hb_o, H, lane, xlane, st.o_meta + m.eid, st.o_dcon, 0, P.adj, A.o_y);
     }
@@ -966,7 +966,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
                 const double yy = MODE != MODE_RB ? yv[u] : 0.0;
                 if (e != cur) {  // the piece of run `cur` ends here
                     if (inside) {
-                        acc_add<MODE>(A, rdst, cur, T, L);
+                        acc_add<MODE, RS>(A, rdst, cur, T, L);
                     } else {
                         hp[tid] = make_double2(T, L);
                         flag = 1;
@@ -982,7 +982,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
             const bool cont = b0 < np && (int)ed[sperm[b0]] == cur;
             if (!cont) {
                 if (inside) {
-                    acc_add<MODE>(A, rdst, cur, T, L);
+                    acc_add<MODE, RS>(A, rdst, cur, T, L);
                 } else {
                     hp[tid] = make_double2(T, L);
                     flag = 1;
@@ -1003,7 +1003,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
                 L += v.y;
                 if (hf[k] != 2) break;
             }
-            acc_add<MODE>(A, rdst, cur, T, L);
+            acc_add<MODE, RS>(A, rdst, cur, T, L);
         }
     }
     TP(4)
@@ -1070,11 +1070,11 @@ struct CtaShared {
 // in reverse so a pass first re-reads what the previous pass wrote last (L2
 // reuse).  `seq` counts the tiles this CTA has staged (stage = seq & 1, mbarrier
 // parity = (seq >> 1) & 1), persistent across passes.
-template <int MODE>
+template <int MODE, bool RS>
 __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *base, CtaShared &cs, uint32_t &seq) {
     const int g = blockIdx.x, tid = threadIdx.x;
     const int E = P.I.E;
-    const SmemPlan sp = smem_plan(P.tps, E, P.nbuf, P.hbmax, P.adj_smem, P.acc_smem, P.run_slots, P.rmax);
+    const SmemPlan sp = smem_plan(P.tps, E, P.nbuf, P.hbmax, P.adj_smem, P.acc_smem, RS, P.rmax);
     Acc A;
     A.adj = P.adj_smem ? (double *)(base + sp.adj) : P.adj;
     A.acc = P.acc_smem ? (double2 *)(base + sp.acc) : nullptr;
@@ -1107,12 +1107,12 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
         if (my > 0) {
             const int b = dbl ? (seq & 1) : 0;
             cs.sd[b] = keep ? desc_of(0) : P.desc[tile_of(0)];
-            issue_tile<MODE>(P, cs.io, cs.sd[b], base, sp, b, &cs.bar[b]);
+            issue_tile<MODE, RS>(P, cs.io, cs.sd[b], base, sp, b, &cs.bar[b]);
         }
     }
     if (!keep)
         for (int i = tid; i < my && i < DL; i += NT) cs.dl[i] = P.desc[tile_of(i)];  // visible after the barrier below
-    for (int e0 = tid; e0 < E && !P.run_slots; e0 += 4 * NT) {  // the adjustment loads of 4 edges in flight
+    for (int e0 = tid; e0 < E && !RS; e0 += 4 * NT) {  // the adjustment loads of 4 edges in flight
         double av[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -1135,7 +1135,7 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
     // without the shared table adj is read through L1 (ld.global.ca); it was
     // rewritten by the edge phase before the grid barrier: acquire at gpu scope
     // so no stale L1 line survives
-    if (!P.adj_smem && !P.run_slots) asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+    if (!P.adj_smem && !RS) asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
     __syncthreads();
     if (tid == 0 && !keep && my <= DL) cs.dl_rev = rev ? 1 : 0;  // every thread read dl_rev before the barrier
     const PassIO &io = cs.io;
@@ -1147,12 +1147,12 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
             if (dbl) {  // prefetch the next tile into the other stage
                 const int nb = b ^ 1;
                 cs.sd[nb] = desc_of(k + 1);
-                issue_tile<MODE>(P, io, cs.sd[nb], base, sp, nb, &cs.bar[nb]);
+                issue_tile<MODE, RS>(P, io, cs.sd[nb], base, sp, nb, &cs.bar[nb]);
             } else if (k + P.pf_dist < my) {  // single stage: warm L2 with a later tile's pair data
                 const TileDesc dn_ = desc_of(k + P.pf_dist);
                 prefetch_l2(io.dcon_in + dn_.sb, 8u * even(dn_.np));
                 prefetch_l2(P.meta + (size_t)dn_.mb16 * 16,
-                            (uint32_t)meta_off(dn_.np, dn_.p1 - dn_.p0, dn_.c1 - dn_.c0, dn_.nrun, dn_.nhb, P.run_slots).bytes);
+                            (uint32_t)meta_off(dn_.np, dn_.p1 - dn_.p0, dn_.c1 - dn_.c0, dn_.nrun, dn_.nhb, RS).bytes);
             }
         }
 #ifdef PF_TPROBE
@@ -1167,7 +1167,7 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
 #endif
         const TileDesc d = cs.sd[b];
         const StageView st = stage_view(base, sp, b, d);
-        tile_compute<MODE>(P, c, io, d, st, A, r_x, r_dd, r_dcon, r_dn);
+        tile_compute<MODE, RS>(P, c, io, d, st, A, r_x, r_dd, r_dcon, r_dn);
 #ifdef PF_TPROBE
         const unsigned long long tb0 = clock64();
 #endif
@@ -1177,7 +1177,7 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
 #endif
         if (!dbl && tid == 0 && k + 1 < my) {  // before the fix-ups (they do not touch the stage)
             cs.sd[0] = desc_of(k + 1);
-            issue_tile<MODE>(P, io, cs.sd[0], base, sp, 0, &cs.bar[0]);
+            issue_tile<MODE, RS>(P, io, cs.sd[0], base, sp, 0, &cs.bar[0]);
         }
     }
     for (int e = tid; e < E; e += NT) {
@@ -1364,7 +1364,7 @@ __global__ void __launch_bounds__(NT, PF_MINB) k_fused(const __grid_constant__ P
     __syncthreads();
     constexpr bool dist = DIST;
     if (c.need_a1) {
-        pass_tiles<MODE_A1>(P, c, smem_raw, cs, seq);
+        (P.run_slots ? pass_tiles<MODE_A1, true>(P, c, smem_raw, cs, seq) : pass_tiles<MODE_A1, false>(P, c, smem_raw, cs, seq));
         grid.sync();
         if (dist) xchg_phase(P, c, grid);
         if (threadIdx.x == 0) {
@@ -1408,7 +1408,7 @@ __global__ void __launch_bounds__(NT, PF_MINB) k_fused(const __grid_constant__ P
             }
             __syncthreads();
         }
-        pass_tiles<MODE_M>(P, c, smem_raw, cs, seq);
+        (P.run_slots ? pass_tiles<MODE_M, true>(P, c, smem_raw, cs, seq) : pass_tiles<MODE_M, false>(P, c, smem_raw, cs, seq));
         mark(2);
         grid.sync();
         mark(3);
@@ -1429,7 +1429,7 @@ __global__ void __launch_bounds__(NT, PF_MINB) k_fused(const __grid_constant__ P
         }
         mark(4);
         if (!c.stopped && !c.status && c.f != 1.0) {
-            pass_tiles<MODE_RB>(P, c, smem_raw, cs, seq);
+            (P.run_slots ? pass_tiles<MODE_RB, true>(P, c, smem_raw, cs, seq) : pass_tiles<MODE_RB, false>(P, c, smem_raw, cs, seq));
             grid.sync();
             if (dist) xchg_phase(P, c, grid);
         }
@@ -1463,7 +1463,7 @@ __global__ void __launch_bounds__(NT, PF_MINB) k_pass(const __grid_constant__ Pa
     uint32_t seq = 0;
     if (threadIdx.x == 0) c = *P.ctrl;
     __syncthreads();
-    pass_tiles<MODE>(P, c, smem_raw, cs, seq);
+    (P.run_slots ? pass_tiles<MODE, true>(P, c, smem_raw, cs, seq) : pass_tiles<MODE, false>(P, c, smem_raw, cs, seq));
 }
 
 // CTA partials -> rank totals in the single-GPU association (one warp per
