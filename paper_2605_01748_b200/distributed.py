@@ -258,6 +258,62 @@ def consistency_check(sh, topo, tab, flat, world, rank):
     return out
 
 
+def _sharded_time_to_quality(args, bench, rank, world, local, name="target_k4_v0.3"):
+    """Time to within 1% at N GPUs on the north-star instance (BASELINE
+    north_star): the sharded solver runs k* iterations from cold
+    (k* = the reference trajectory's own, from the committed oracle fixture),
+    timed on the device as the max over ranks, plus the gather and one GPU
+    projection on rank 0; the projected sums are then scored against the
+    reference fixed point, so the line shows the quality actually reached."""
+    import time as _time
+
+    import torch
+    import torch.distributed as dist
+
+    fp = bench.oracle_fixed_point(name)
+    if fp is None or getattr(args, "no_ttq", False):
+        return None
+    meta, opt = fp
+    kstar = int(meta["k_star"])
+    if rank == 0:
+        bench.build_inputs(name)
+    dist.barrier()
+    topo, tab, flat = bench.build_inputs(name)
+    sh = ShardedSolver(topo, tab, flat, SolverConfig(mode="fast", max_iterations=5000), rank, world, local)
+    sh.init()
+    dist.barrier()
+    ms, _ = sh.time_loop(kstar)
+    t = torch.tensor([ms], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_loop = float(t.item())
+    r = sh.result()
+    alpha = int(r.alpha)
+    if int(r.iterations) != kstar or int(r.status) != 0:
+        raise RuntimeError(f"sharded time-to-quality run stopped at iteration {int(r.iterations)} of {kstar} "
+                           f"(status {int(r.status)}, converged {int(r.converged)})")
+    t0 = _time.perf_counter()
+    xg = sh.gather_x()
+    out = None
+    if rank == 0:
+        from .metrics import default_theta, optimality_from_sums
+        from .model import build_instance_flat, commodity_sums
+        from .projection import project
+        full = build_instance_flat(topo, tab, flat, device=local)
+        t1 = _time.perf_counter()
+        rates = project(full, xg, alpha)
+        torch.cuda.synchronize()
+        proj_ms = 1e3 * (_time.perf_counter() - t1)
+        gather_ms = 1e3 * (t1 - t0)
+        q = optimality_from_sums(commodity_sums(full, rates), opt, default_theta(full))
+        out = {"config": name, "k_star_reference": kstar, "gpu_loop_ms_max_over_ranks": ms_loop,
+               "gather_ms": gather_ms, "projection_ms": proj_ms, "gpu_ms": ms_loop + gather_ms + proj_ms,
+               "optimality_at_k_star_vs_reference_fixed_point": q, "n_gpus": world,
+               "how": "k* sharded iterations from cold (one launch per rank, max over ranks) + gather_x + "
+                      "project on rank 0 (host wall); quality scored against the oracle's fixed point"}
+    dist.barrier()
+    return out
+
+
 def bench_main(args, bench):
     """bench.py --gpus N under torchrun: one instance (config 3 by default)
     sharded over N GPUs (fixed total work: strong scaling)."""
@@ -316,6 +372,7 @@ def bench_main(args, bench):
     te = torch.tensor([e2e_s], dtype=torch.float64)
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_s = float(te.item())
+    ttq = _sharded_time_to_quality(args, bench, rank, world, local)
     if rank == 0:
         C_, P_, E_ = len(tab), int(flat.com_path_ptr[-1]), topo.num_edges
         NPt = int(tn.item())
@@ -341,7 +398,8 @@ def bench_main(args, bench):
                 "e2e": {"value": args.steps / e2e_s, "unit": "iterations/s",
                         "h2d_bytes_per_step": 8 * P_ / args.steps, "d2h_bytes_per_step": 16 * P_ / args.steps,
                         "call": "ShardedSolver: host warm start -> K iterations -> gather_x -> project (rank 0)"},
-                "check": check_}
+                "check": check_,
+                "time_to_1pct": ttq}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
     return 0
