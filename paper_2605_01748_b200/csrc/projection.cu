@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(CL_NT, 1) k_edge_trim_cluster(InstView I, cons
             for (int32_t j = tid * 32; j < l2; j += CL_NT * 32)
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(path_order + lo2 + a2 + j));
         }
-        for (int32_t j0 = tid; j0 < len; j0 += 8 * CL_NT) {  // gather: 8 independent loads in flight
+        for (int32_t j0 = tid; j0 < len && !(stats & 2 && vi); j0 += 8 * CL_NT) {  // gather: 8 independent loads in flight
             int32_t pi[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
@@ -608,9 +608,181 @@ __global__ void __launch_bounds__(CL_NT, 1) k_edge_trim_cluster(InstView I, cons
         st_trimmed += maxchg >= 0;
         cl.sync();  // the written rates are visible to the whole cluster before the next gather
     }
-    if (stats && tid == 0)
+    if ((stats & 1) && tid == 0)
         printf("[k_edge_trim_cluster] rank %d/%d violated %d slices trimmed %lld passes %lld\n", rank, ncl, nviol,
                st_trimmed, st_passes);
+}
+
+// The cluster trim with the gathers pipelined across edges: the score-ordered
+// path slice (static during phase 3) is loaded two edges ahead, and the rates of
+// the next edge are gathered speculatively while the current edge is trimmed.
+// The speculative rates are used only when the current edge changed nothing
+// (a cluster-uniform fact: its load did not exceed its capacity on the first
+// pass); otherwise they are gathered again after the current edge's
+// write-back.  Every decision and every sum is the one k_edge_trim_cluster
+// makes: the result is bitwise the same.  Shared memory per CTA: three path
+// slices and two rate slices of `cap` entries (cap <= PIPE_PF * CL_NT).
+constexpr int PIPE_PF = 8;  // slice entries per thread held in registers while prefetching
+constexpr int PIPE_ENTRY = 3 * sizeof(int32_t) + 2 * sizeof(double);
+constexpr size_t PIPE_SMEM_MAX = 224 * 1024;
+
+__device__ __forceinline__ void slice_of(const InstView &I, const int32_t *edge_order, int32_t v, int rank, int ncl,
+                                         int32_t &lo, int32_t &len) {
+    const int32_t e = edge_order[v];
+    const int32_t l0 = I.edge_pair_ptr[e], n = I.edge_pair_ptr[e + 1] - l0;
+    const int32_t chunk = (n + ncl - 1) / ncl;
+    const int32_t a = min(n, rank * chunk);
+    lo = l0 + a;
+    len = min(n, a + chunk) - a;
+}
+
+__global__ void __launch_bounds__(CL_NT, 1) k_edge_trim_cluster_pipe(InstView I, const int32_t *edge_order,
+                                                                    const int32_t *nviol_p, const int32_t *path_order,
+                                                                    double *x, int32_t cap, int stats) {
+    extern __shared__ __align__(16) char dsm[];
+    double *sxb = (double *)dsm;                          // [2][cap]
+    int32_t *spb = (int32_t *)(dsm + 2 * (size_t)cap * sizeof(double));  // [3][cap]
+    __shared__ double s_part[2][8];
+    __shared__ int32_t s_found[2][8];
+    __shared__ double wsum[32];
+    __shared__ int32_t s_js;
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank(), ncl = (int)cl.num_blocks();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = CL_NT >> 5;
+    const int32_t nviol = *nviol_p;
+    long long st_trimmed = 0, st_passes = 0, st_regather = 0;
+    int ph = 0;
+    cl.sync();
+    // prologue: the path slices of edges 0 and 1, the rates of edge 0
+    for (int v = 0; v < 2 && v < nviol; ++v) {
+        int32_t lo, len;
+        slice_of(I, edge_order, v, rank, ncl, lo, len);
+        for (int32_t j = tid; j < len; j += CL_NT) spb[v * cap + j] = __ldcg(path_order + lo + j);
+    }
+    __syncthreads();
+    bool fresh = false;  // the rate slice of the current edge holds current rates
+    for (int32_t vi = 0; vi < nviol; ++vi) {
+        const int32_t e = edge_order[vi];
+        int32_t lo, len;
+        slice_of(I, edge_order, vi, rank, ncl, lo, len);
+        const double cap_e = I.capacity[e];
+        double *sx = sxb + (vi & 1) * cap;
+        int32_t *sp = spb + (vi % 3) * cap;
+        if (!fresh) {  // (edge 0, or the previous edge trimmed): gather the rates now
+            for (int32_t j0 = tid; j0 < len; j0 += 8 * CL_NT) {
+                double xv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int32_t j = j0 + u * CL_NT;
+                    xv[u] = j < len ? __ldcg(x + sp[j]) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int32_t j = j0 + u * CL_NT;
+                    if (j < len) sx[j] = xv[u];
+                }
+            }
+            st_regather += vi > 0;
+            __syncthreads();
+        }
+        // prefetch into registers: the next edge's rates (speculative) and the
+        // path slice two edges ahead
+        int32_t len1 = 0, len2 = 0, lo2 = 0;
+        if (vi + 1 < nviol) {
+            int32_t lo1;
+            slice_of(I, edge_order, vi + 1, rank, ncl, lo1, len1);
+        }
+        if (vi + 2 < nviol) slice_of(I, edge_order, vi + 2, rank, ncl, lo2, len2);
+        const int32_t *sp1 = spb + ((vi + 1) % 3) * cap;
+        double nx[PIPE_PF];
+        int32_t np2[PIPE_PF];
+#pragma unroll
+        for (int u = 0; u < PIPE_PF; ++u) {
+            const int32_t j = tid + u * CL_NT;
+            nx[u] = j < len1 ? __ldcg(x + sp1[j]) : 0.0;
+            np2[u] = j < len2 ? __ldcg(path_order + lo2 + j) : 0;
+        }
+        const int32_t m = (len + CL_NT - 1) / CL_NT;  // each thread owns a contiguous run
+        const int32_t r0 = min(len, tid * m), r1 = min(len, r0 + m);
+        int32_t maxchg = -1;
+        int npass = 0;
+        for (int pass = 0;; ++pass) {
+            double ts = 0.0;
+            for (int32_t j = r0; j < r1; ++j) ts += sx[j];
+            double ws = ts;
+            for (int o = 1; o < 32; o <<= 1) {
+                const double t = __shfl_up_sync(0xffffffffu, ws, o);
+                if (lane >= o) ws += t;
+            }
+            if (lane == 31) wsum[warp] = ws;
+            if (tid == 0) s_js = INT_MAX;
+            __syncthreads();
+            if (warp == 0) {
+                double v = lane < nw ? wsum[lane] : 0.0;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double t = __shfl_up_sync(0xffffffffu, v, o);
+                    if (lane >= o) v += t;
+                }
+                if (lane < nw) wsum[lane] = v;
+            }
+            __syncthreads();
+            if (tid < ncl) *cl.map_shared_rank(&s_part[ph][rank], tid) = wsum[nw - 1];
+            cl.sync();
+            double load = 0.0, carry = 0.0;
+            for (int q = 0; q < ncl; ++q) {
+                if (q == rank) carry = load;
+                load += s_part[ph][q];
+            }
+            const double excess = load - cap_e;
+            if (!(excess > 0.0) || pass == 16) break;  // uniform across the cluster
+            ++npass;
+            st_passes += 1;
+            double pre = carry + (warp ? wsum[warp - 1] : 0.0) + (ws - ts);
+            for (int32_t j = r0; j < r1; ++j) {
+                pre += sx[j];
+                if (pre >= excess) {
+                    atomicMin(&s_js, j);
+                    break;
+                }
+            }
+            __syncthreads();
+            const int32_t js = s_js;
+            if (tid < ncl) *cl.map_shared_rank(&s_found[ph][rank], tid) = js;
+            cl.sync();
+            bool earlier = false;
+            for (int q = 0; q < rank; ++q) earlier |= s_found[ph][q] != INT_MAX;
+            if (!earlier) {
+                const int32_t cut = js == INT_MAX ? len : js;
+                if (cut < len && cut >= r0 && cut < r1) {
+                    double p2 = carry + (warp ? wsum[warp - 1] : 0.0) + (ws - ts);
+                    for (int32_t j = r0; j <= cut; ++j) p2 += sx[j];
+                    sx[cut] = max0(p2 - excess);
+                }
+                __syncthreads();
+                for (int32_t j = tid; j < cut; j += CL_NT) sx[j] = 0.0;
+                maxchg = max(maxchg, cut < len ? cut : len - 1);
+            }
+            ph ^= 1;
+            __syncthreads();
+        }
+        ph ^= 1;
+        for (int32_t j = tid; j <= maxchg; j += CL_NT) x[sp[j]] = sx[j];
+        st_trimmed += maxchg >= 0;
+        // the prefetched slices into shared memory (buffers of finished edges)
+        double *sx1 = sxb + ((vi + 1) & 1) * cap;
+        int32_t *sp2 = spb + ((vi + 2) % 3) * cap;
+#pragma unroll
+        for (int u = 0; u < PIPE_PF; ++u) {
+            const int32_t j = tid + u * CL_NT;
+            if (j < len1) sx1[j] = nx[u];
+            if (j < len2) sp2[j] = np2[u];
+        }
+        fresh = npass == 0;  // this edge changed nothing: the speculative rates are current
+        cl.sync();  // write-back and prefetched slices visible before the next edge
+    }
+    if ((stats & 1) && tid == 0)
+        printf("[k_edge_trim_cluster_pipe] rank %d/%d violated %d slices trimmed %lld passes %lld regathers %lld\n",
+               rank, ncl, nviol, st_trimmed, st_passes, st_regather);
 }
 
 constexpr int TRIM_SMEM = 2 * TCH * (sizeof(double) + sizeof(int32_t));
@@ -680,6 +852,8 @@ static ProjWS &workspace(const pf_instance *inst, cudaStream_t s) {
     PF_CUDA(cudaFuncSetAttribute(k_edge_trim, cudaFuncAttributeMaxDynamicSharedMemorySize, TRIM_SMEM));
     PF_CUDA(cudaFuncSetAttribute(k_edge_trim_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, TRIM_FAST_SMEM));
     PF_CUDA(cudaFuncSetAttribute(k_edge_trim_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SMEM));
+    PF_CUDA(cudaFuncSetAttribute(k_edge_trim_cluster_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 PIPE_SMEM_MAX));
     lap("attributes");
     inst->proj_ws = ws;
     return *ws;
@@ -755,7 +929,7 @@ void project_device(const pf_instance *inst, const double *rates, int64_t alpha,
         PF_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(ws.cub.p, bytes, ws.pkeys.p, ws.pkeys_out.p, ws.pvals.p,
                                                          ws.porder.p, I.NP, I.E, ws.sb.p, ws.se.p, 0, 64, s));
     }
-    static const int stats = getenv("PF_PROJ_STATS") ? 1 : 0;
+    static const int stats = (getenv("PF_PROJ_STATS") ? 1 : 0) | (getenv("PF_PROJ_ABLATE") ? 2 : 0);  // 2: timing ablation
     PF_CUDA(cudaMemsetAsync(ws.dirty.p, 0, I.E + 1, s));
     // PF_PROJ_CLUSTER: CTAs per cluster for the fast trim (0 = single-CTA kernel)
     static const int cl_env = getenv("PF_PROJ_CLUSTER") ? atoi(getenv("PF_PROJ_CLUSTER")) : -1;
@@ -771,7 +945,26 @@ void project_device(const pf_instance *inst, const double *rates, int64_t alpha,
             while (ncl < 8 && (ncl < cl_env || ncl < need)) ncl *= 2;
         }
     }
-    if (fast && ncl > 0) {
+    // the pipelined cluster trim when the slices of the largest edge fit its
+    // shared memory (config 2: 8 CTAs x 6,656 entries); PF_PROJ_PIPE=0 disables it
+    static const bool pipe_env = !getenv("PF_PROJ_PIPE") || atoi(getenv("PF_PROJ_PIPE")) != 0;
+    const int32_t pcap = ncl > 0 ? ((ws.max_ne + ncl - 1) / ncl + 31) / 32 * 32 : 0;
+    if (fast && ncl > 0 && pipe_env && pcap <= PIPE_PF * CL_NT && (size_t)pcap * PIPE_ENTRY <= PIPE_SMEM_MAX) {
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(ncl);
+        lc.blockDim = dim3(CL_NT);
+        lc.dynamicSmemBytes = (size_t)pcap * PIPE_ENTRY;
+        lc.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = ncl;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        PF_CUDA(cudaLaunchKernelEx(&lc, k_edge_trim_cluster_pipe, I, (const int32_t *)ws.eorder.p,
+                                   (const int32_t *)ws.nviol.p, (const int32_t *)ws.porder.p, x, pcap, stats));
+    } else if (fast && ncl > 0) {
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3(ncl);
         lc.blockDim = dim3(CL_NT);

@@ -1,6 +1,7 @@
 """Subprocess helper for test_fast_projection_cluster_variants: the fast-mode
 projection of a raw iterate under the PF_PROJ_CLUSTER set in the environment
-(read once per process).  Prints a JSON line."""
+(read once per process), and PF_PROJ_PIPE (pipelined cluster trim).  Prints a JSON line."""
+import hashlib
 import json
 import os
 import sys
@@ -22,7 +23,7 @@ for rep in range(2):
     x = s.x()
     alpha = int(s.state().alpha)
     rates, sums = s.finish()
-    out.setdefault("digests", []).append(str(hash(rates.tobytes())))
+    out.setdefault("digests", []).append(hashlib.sha256(rates.tobytes()).hexdigest())
 exact = pf.project(inst, x, alpha)
 ex_sums = pf.commodity_sums(inst, exact)
 rep0 = pf.validate_allocation(inst, np.maximum(x, 0.0))

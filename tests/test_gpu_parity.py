@@ -510,6 +510,26 @@ def test_fast_projection_cluster_variants(ncl):
     assert out["sums_rel"] <= 1e-6, out
 
 
+def test_fast_projection_pipelined_trim_bitwise():
+    """The pipelined cluster trim (path slices loaded two edges ahead, the next
+    edge's rates gathered speculatively and used only when the current edge
+    changed nothing) gives bitwise the rates of the plain cluster trim."""
+    import json
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    outs = []
+    for pipe in ("0", "1"):
+        env = dict(os.environ, PF_PROJ_CLUSTER="8", PF_PROJ_PIPE=pipe)
+        r = subprocess.run([sys.executable, os.path.join(here, "_proj_variant.py"), "150", "4", "12"], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0]["feasible"] and outs[1]["feasible"] and outs[1]["deterministic"]
+    assert outs[0]["digests"][0] == outs[1]["digests"][0]
+
+
 def test_fast_trace_batched_rows_equal_per_row_path():
     """Traced fast runs without an optimality column compute their rows on the
     device in batches (no host round trip per iteration); with reference sums
