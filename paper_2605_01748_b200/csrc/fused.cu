@@ -772,10 +772,13 @@ __device__ __forceinline__ double hops_y(int hb_o, int H, int lane, double xl, i
 // dual_consensus' (kernels.py:72) stored coalesced to global; T = x' + dcon'
 // (kernels.py:91) into tv (tv aliases dcon on purpose: every step reads dcon[l]
 // before it writes tv[l], for its own row only)
+// Inactive lanes read `dummy_o`, a double nobody writes in this phase (the
+// step's own slots are rewritten by the active lanes).
 __device__ __forceinline__ double hops_dcon(int hb_o, int H, int lane, double xn, double f, int dcon_o, int ys_o,
-                                            double *__restrict__ dco) {
+                                            double *__restrict__ dco, int dummy_o) {
     const uint16_t *hb = (const uint16_t *)(g_smem + hb_o);
     double *dcon = (double *)(g_smem + dcon_o);
+    const double *dummy = (const double *)(g_smem + dummy_o);
     const double *ys = (const double *)(g_smem + ys_o);
     double r = 0.0;
     int b0 = hb[0];
@@ -784,7 +787,7 @@ __device__ __forceinline__ double hops_dcon(int hb_o, int H, int lane, double xn
         const int b1 = hb[j + 1];
         const bool on = lane < b1 - b0;
         const int l = on ? b0 + lane : b0;
-        const double dks = dcon[l] * f;
+        const double dks = (on ? dcon + l : dummy)[0] * f;
         const double dnew = max0(dks + xn - ys[l]);
         const double df = dnew - dks;
         if (on) {
@@ -920,7 +923,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
     // (tv aliases dcon on purpose: every step reads dcon[l] before it writes
     // tv[l], for the same l only)
     const double xh = __shfl_sync(FULL, xnew_lane, hv ? (int)hperm[gp0 + lane] : lane);  // back to the hop lane
-    r_dcon += hops_dcon(hb_o, H, lane, xh, f, st.o_dcon, A.o_y, io.dcon_out + d.sb);
+    r_dcon += hops_dcon(hb_o, H, lane, xh, f, st.o_dcon, A.o_y, io.dcon_out + d.sb, st.o_xk);
     fence_proxy_async_shared();  // these generic writes precede the TMA that refills the stage
     __syncthreads();
     TP(3)
