@@ -100,7 +100,7 @@ __host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc, 
     int o = 0;
     m.eid = o;  // u16 [np] edge id (run id with run slots) of each pair (hop-major within each group)
     o += r16(2 * np);
-    m.sperm = o;  // u16 [np] tile-local pairs sorted by (edge, pair): the edge runs, back to back
+    m.sperm = o;  // u16 [np] tile-local pairs sorted by (edge, pair): the edge runs, back to back; bit 15 = run start
     o += r16(2 * np);
     m.poff = o;  // u16 [npath + 1] tile-local pair offset of each path
     o += r16(2 * (npath + 1));
@@ -958,16 +958,19 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
         int cur = -1, flag = 0;
         bool inside = false;  // the current piece started inside this chunk
         if (a0 < b0) {
-            const int prev = a0 > 0 ? (int)ed[sperm[a0 - 1]] : -1;
-            cur = ed[sperm[a0]];
-            inside = cur != prev;
+            // sperm: bit 15 marks the first pair of a run, bits 0-14 the pair;
+            // the run's edge (or run id) is read once per run
+            const int w0 = sperm[a0];
+            cur = ed[w0 & 0x7fff];
+            inside = (w0 >> 15) != 0;
 #pragma unroll 4
             for (int q = a0; q < b0; ++q) {
-                const int u = sperm[q];
-                const int e = ed[u];
+                const int wq = sperm[q];
+                const int u = wq & 0x7fff;
                 const double t = tv[u];
                 const double yy = MODE != MODE_RB ? yv[u] : 0.0;
-                if (e != cur) {  // the piece of run `cur` ends here
+                if (q > a0 && (wq >> 15)) {  // the piece of run `cur` ends here
+                    const int e = ed[u];
                     if (inside) {
                         acc_add<MODE, RS>(A, rdst, cur, T, L);
                     } else {
@@ -982,7 +985,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
                 T += t;
                 if (MODE != MODE_RB) L += yy;
             }
-            const bool cont = b0 < np && (int)ed[sperm[b0]] == cur;
+            const bool cont = b0 < np && !(sperm[b0] >> 15);
             if (!cont) {
                 if (inside) {
                     acc_add<MODE, RS>(A, rdst, cur, T, L);
@@ -1877,18 +1880,20 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         // edge runs: sperm = pairs sorted by (edge, pair), the runs back to back
         uint16_t *sperm = (uint16_t *)(blk + m.sperm);
         std::vector<int> rstart;
+        require(np <= 0x7fff, "fast layout: more than 32,767 pairs in a tile");
         for (int sl = 0; sl < np; ++sl) {
-            sperm[sl] = perm[sl];
-            if (sl == 0 || eid[perm[sl]] != eid[perm[sl - 1]]) rstart.push_back(sl);
+            const bool start = sl == 0 || eid[perm[sl]] != eid[perm[sl - 1]];
+            sperm[sl] = (uint16_t)(perm[sl] | (start ? 0x8000 : 0));  // bit 15: a run starts here
+            if (start) rstart.push_back(sl);
         }
         const int nr = (int)rstart.size();
         require(nr == T.nrun, "fast layout: run count mismatch");
         rstart.push_back(np);
         if (L->run_slots) {  // the run's edge; the per-pair u16 becomes the pair's run
             uint16_t *redge = (uint16_t *)(blk + m.redge);
-            for (int r = 0; r < nr; ++r) redge[r] = eid[sperm[rstart[r]]];
+            for (int r = 0; r < nr; ++r) redge[r] = eid[sperm[rstart[r]] & 0x7fff];
             for (int r = 0; r < nr; ++r)
-                for (int sl = rstart[r]; sl < rstart[r + 1]; ++sl) eid[sperm[sl]] = (uint16_t)r;
+                for (int sl = rstart[r]; sl < rstart[r + 1]; ++sl) eid[sperm[sl] & 0x7fff] = (uint16_t)r;
         }
         for (int j = 0; j < nc; ++j) {
             lcpp[j] = (uint16_t)(cpp[T.c0 + j] - T.p0);
