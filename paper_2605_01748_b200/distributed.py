@@ -344,6 +344,11 @@ def bench_main(args, bench):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     st = sh.solver.kernel_stats()
+    # compulsory HBM bytes per iteration summed over the ranks' layouts
+    # (kernel_stats; ncu cannot profile a multi-rank run -- at N = 1 ncu measures
+    # ~0.99x of the layout's compulsory bytes, profiles/r02*_fused_*.json)
+    tb = torch.tensor([float(st["bytes_per_iter"])], dtype=torch.float64)
+    dist.all_reduce(tb)
     NP = np.array([sh.instance.num_pairs], np.int64)
     tn = torch.tensor(NP)
     dist.all_reduce(tn)
@@ -393,7 +398,9 @@ def bench_main(args, bench):
                               **({"shared_gpus": torch.cuda.device_count()}
                                  if os.environ.get("PF_BENCH_SHARE_GPU") == "1" else {})},
                 "roofline": {"bound": "hbm", "achieved": ach, "peak": peak * world, "unit": "GB/s",
-                             "frac": ach / (peak * world), "traffic": None, "peak_kind": kind},
+                             "frac": ach / (peak * world), "traffic": float(tb.item()),
+                             "traffic_kind": "compulsory layout bytes per iteration, summed over ranks (not ncu)",
+                             "peak_kind": kind},
                 "clocks": clk, "gpu_launches": int(st["launches"]), "max_over_ranks_ms": ms_max,
                 "e2e": {"value": args.steps / e2e_s, "unit": "iterations/s",
                         "h2d_bytes_per_step": 8 * P_ / args.steps, "d2h_bytes_per_step": 16 * P_ / args.steps,
