@@ -445,12 +445,17 @@ def test_fast_iterations_match_exact_generated(n, k):
             np.testing.assert_allclose(getattr(b, f), getattr(a, f), rtol=1e-10, atol=1e-10, err_msg=f"{it} {f}")
 
 
-def test_fast_large_edge_mode_matches_exact(monkeypatch):
-    """The large-E layout (one CTA per SM, adjustment table read through L1,
-    PF_FAST_LARGE_E forces it on a small instance): iterations 1-3 agree with the
-    exact-order path to 1e-10, and the converged solve matches the default layout."""
+@pytest.mark.parametrize("run_slots", ["1", "0"])
+def test_fast_large_edge_mode_matches_exact(monkeypatch, run_slots):
+    """The large-E layouts (PF_FAST_LARGE_E forces them on a small instance):
+    run slots (per-(tile, run) edge totals in edge-major global slots, a per-tile
+    run adjustment table; the default for large E) and the older per-CTA
+    accumulators with the adjustment table read through L1 (PF_FAST_RS=0):
+    iterations 1-3 agree with the exact-order path to 1e-10, and the converged
+    solve matches the default layout."""
     from b200_helpers import generated
     monkeypatch.setenv("PF_FAST_LARGE_E", "1")
+    monkeypatch.setenv("PF_FAST_RS", run_slots)
     topo, tab, ps = generated(60, 8, 1.5)
     inst = pf.build_instance(topo, tab, ps, device=0)  # fresh index set: the layout is built with the override
     ex = pf.Solver(inst, pf.SolverConfig(mode="exact")).init()
@@ -463,6 +468,7 @@ def test_fast_large_edge_mode_matches_exact(monkeypatch):
             np.testing.assert_allclose(getattr(b, f), getattr(a, f), rtol=1e-10, atol=1e-10, err_msg=f"{it} {f}")
     big = pf.solve(inst, pf.SolverConfig(mode="fast", max_iterations=400))
     monkeypatch.delenv("PF_FAST_LARGE_E")
+    monkeypatch.delenv("PF_FAST_RS")
     inst2 = pf.build_instance(topo, tab, ps, device=0)
     small = pf.solve(inst2, pf.SolverConfig(mode="fast", max_iterations=400))
     assert pf.validate_allocation(inst, big.rates).feasible
