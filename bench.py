@@ -397,6 +397,77 @@ def config45(name, device=0):
     return out4, out5
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")  # the unmodified reference, pip-installed (git-ignored)
+
+
+def reference_numba(name, cpp, pep, pe, iterations=2):
+    """The reference's OWN implementation (pathfair, Python + numba, installed
+    unmodified into baseline/_ref) timed on this host for `iterations` loop
+    bodies (controller.py:226-236: update_duals, update_slacks,
+    update_rate_suggestions, solve_commodity_sums, update_rates,
+    compute_residuals, called through the reference's public kernel API) at
+    set_threads(cpu_count) and set_threads(1).  The
+    instance is the reference's build_instance of its own random_topology /
+    gravity_demands with the k-shortest paths of this workload (the native
+    KSP, pinned equal to the reference's networkx one).  Runs in a child
+    process (numba's thread pool is sized at import).  Reported next to the
+    C port; the arm's value stays the port's."""
+    if not os.path.isdir(os.path.join(REF_DIR, "pathfair")):
+        return {"unavailable": "baseline/_ref not installed (pip install --target baseline/_ref the reference)"}
+    import tempfile
+    n, k, vol, _ = CONFIGS[name]
+    with tempfile.TemporaryDirectory() as td:
+        np.savez(os.path.join(td, "paths.npz"), cpp=cpp, pep=pep, pe=pe)
+        env = dict(os.environ, NUMBA_CACHE_DIR=os.path.join(td, "nb"), NUMBA_NUM_THREADS=str(os.cpu_count()),
+                   PYTHONPATH=REF_DIR)
+        code = f"""
+import copy, json, os, time
+import numpy as np
+import pathfair as R
+from pathfair import kernels as K, controller as Ctl, _reduce as RD
+z = np.load({os.path.join(td, "paths.npz")!r})
+cpp, pep, pe = z["cpp"], z["pep"], z["pe"]
+topo = R.harness.random_topology({n}, seed={n})
+coms = R.harness.gravity_demands(topo, {vol} * float(topo.capacity.sum()))
+lists = [[tuple(int(e) for e in pe[pep[p]:pep[p + 1]]) for p in range(cpp[c], cpp[c + 1])] for c in range(len(coms))]
+t0 = time.perf_counter()
+inst = R.build_instance(topo, coms, R.PathSet.from_lists(lists))
+t_build = time.perf_counter() - t0
+cfg = Ctl.SolverConfig(gamma=1e-12)
+out = {{"build_instance_s": t_build, "pairs": int(inst.num_pairs)}}
+def body(state):
+    prev = copy.copy(state)
+    dd, dc, dcon, dn = K.update_duals(state, inst)
+    sd, sc = K.update_slacks(state, inst)
+    state.dual_demand, state.dual_capacity, state.dual_consensus, state.dual_nonneg = dd, dc, dcon, dn
+    state.slack_demand, state.slack_capacity = sd, sc
+    state.y = K.update_rate_suggestions(state, inst)
+    sums = K.solve_commodity_sums(state, inst, state.alpha)
+    state.x = K.update_rates(state, inst, sums, state.alpha)
+    Ctl.compute_residuals(prev, state)
+for threads in (os.cpu_count(), 1):
+    eff = RD.set_threads(threads)
+    state = Ctl.initialize_state(inst, cfg)
+    body(state)  # JIT + warm-up
+    t = time.perf_counter()
+    for _ in range({iterations}):
+        body(state)
+    dt = (time.perf_counter() - t) / {iterations}
+    out[f"threads_{{eff}}"] = {{"iterations_per_s": 1.0 / dt, "ms_per_iteration": 1e3 * dt}}
+print(json.dumps(out))
+"""
+        try:
+            r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+        except subprocess.TimeoutExpired:
+            return {"unavailable": "timed out"}
+        if r.returncode != 0:
+            return {"unavailable": (r.stderr.strip().splitlines() or ["failed"])[-1][:300]}
+        out = json.loads(r.stdout.strip().splitlines()[-1])
+    out.update(kind="reference (pathfair, numba, unmodified, baseline/_ref)", workload=name,
+               sample=f"{iterations} loop bodies per thread count after one warm-up body")
+    return out
+
+
 def run_reference(args):
     """--impl reference: the reference algorithm's CPU implementation (the
     exact-order C oracle, all host threads) on the same workload; rank 0 only.
@@ -432,6 +503,8 @@ def run_reference(args):
                              "sample": f"{steps} iterations of the full instance (C oracle, exact reference "
                                        f"op order, OpenMP)"},
             "e2e": {"value": v, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if not getattr(args, "no_reference_numba", False):
+        line["reference_numba"] = reference_numba(name, cpp, pep, pe)
     print(json.dumps(line), flush=True)
     return 0
 
@@ -585,6 +658,8 @@ def main(argv=None):
     ap.add_argument("--ttq", default="cfg1_v0.3,cfg2_v0.3,target_k4_v0.3", help="configs for time-to-within-1%%")
     ap.add_argument("--no-extras", action="store_true", help="skip the config 4 / config 5 measurements")
     ap.add_argument("--extras-config", default="cfg2_v0.3", help="instance for the config 4 / 5 measurements")
+    ap.add_argument("--no-reference-numba", action="store_true",
+                    help="reference arm: skip timing the reference's own numba implementation (baseline/_ref)")
     ap.add_argument("--sharded-config", default="cfg3",
                     help="at N=1 also time this workload on one GPU (the N=1 point of the sharded curve; '' skips)")
     args = ap.parse_args(argv)
