@@ -517,7 +517,10 @@ def resolve_config(args, world):
 
 def single_gpu_rate(name, device, steps=20, warmup=3):
     """Fused-loop iterations/s of one workload on one GPU (the N=1 point of a
-    sharded config's scaling curve)."""
+    sharded config's scaling curve): `steps` iterations in one launch after
+    `warmup`, so the window holds the beta ramp's rollback passes in the same
+    proportion as the main line's 1,000 iterations do (rollbacks: a second pass
+    on the iterations where beta changes, every 10 iterations while it ramps)."""
     import torch
 
     import paper_2605_01748_b200 as pf
@@ -605,7 +608,7 @@ def run_b200(args):
     del solver
     sharded_n1 = None
     if rank == 0 and args.sharded_config and args.sharded_config != args.config:
-        sharded_n1 = single_gpu_rate(args.sharded_config, local)
+        sharded_n1 = single_gpu_rate(args.sharded_config, local, steps=200, warmup=10)
     line = {
         "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,

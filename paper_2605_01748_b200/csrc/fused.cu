@@ -231,6 +231,7 @@ struct Params {
     int32_t run_slots, rmax;
     int32_t hbmax, pad1;  // most hop-step entries of one tile (the shared-memory metadata bound)
     const int32_t *eoff;
+    const int32_t *ebound;  // run slots, single GPU: CTA g sums edges ebound[g] .. ebound[g + 1] (slot-balanced)
     double *slots;
 };
 
@@ -668,6 +669,56 @@ __device__ void controller_eval(const Params &P, Ctrl &c) {
 // One warp per edge: the CTA partials summed by warp_edge_sums, then
 // kernels.py:212 (dual_capacity) and :94-96 (adjustment); the squared
 // dual_capacity change per edge for the residual (summed by dcs_block).
+// Run slots, single GPU: one CTA per edge at a time over a slot-balanced range
+// of edges (a heavily shared edge of config 3 holds tens of thousands of
+// slots; a warp per edge left the phase waiting on the heaviest edges).  Thread
+// t sums slots t, t + NT, ... in order (8 in flight), then a fixed block tree;
+// then kernels.py:212 and :94-96 as edge_phase.
+__device__ __noinline__ void edge_phase_rs(const Params &P, double f) {
+    const InstView &I = P.I;
+    __shared__ double2 wsum[NT / 32];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const double2 *slots = (const double2 *)P.slots;
+    for (int e = P.ebound[blockIdx.x]; e < P.ebound[blockIdx.x + 1]; ++e) {
+        const int a = __ldg(&P.eoff[e]), b = __ldg(&P.eoff[e + 1]);
+        double t = 0.0, l = 0.0;
+        for (int s0 = a + tid; s0 < b; s0 += 8 * NT) {
+            double2 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = s0 + u * NT < b ? __ldcg(slots + s0 + u * NT) : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (s0 + u * NT < b) {
+                    t += v[u].x;
+                    l += v[u].y;
+                }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            t += __shfl_down_sync(FULL, t, o);
+            l += __shfl_down_sync(FULL, l, o);
+        }
+        if (lane == 0) wsum[warp] = make_double2(t, l);
+        __syncthreads();
+        if (tid == 0) {
+            double T = wsum[0].x, L = wsum[0].y;
+            for (int w = 1; w < NT / 32; ++w) {
+                T += wsum[w].x;
+                L += wsum[w].y;
+            }
+            const double cap = I.capacity[e];
+            const double dold = __ldcg(&P.dc[e]) * f;
+            const double dnew = npmax0(dold + (L - cap));
+            double adj = (T + dnew - cap) / (P.ne[e] + 1.0);
+            if (adj < 0.0) adj = 0.0;
+            P.dc[e] = dnew;
+            P.adj[e] = adj;
+            const double d = dnew - dold;
+            P.res_dc[e] = d * d;
+        }
+        __syncthreads();
+    }
+}
+
 __device__ __noinline__ void edge_phase(const Params &P, double f) {
     const InstView &I = P.I;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1403,7 +1454,7 @@ __global__ void __launch_bounds__(NT, PF_MINB) k_fused(const __grid_constant__ P
             if (dist)
                 xchg_edge_apply(P, c, c.f);
             else
-                edge_phase(P, c.f);
+                (P.ebound ? edge_phase_rs(P, c.f) : edge_phase(P, c.f));
             mark(0);
             grid.sync();
             mark(1);
@@ -1961,7 +2012,7 @@ struct FastSolver {
     size_t smem = 0;
     DevBuf<double> dcon[2], dn[2], dd[2], x[2];
     DevBuf<double> D, dc, adj, ne, tot, partT, partL, res, res_dc, root_sums, slots;
-    DevBuf<int32_t> err, cta_ptr, cta_tiles;
+    DevBuf<int32_t> err, cta_ptr, cta_tiles, ebound;
     DevBuf<Ctrl> ctrl;
     Params P{};
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -2162,6 +2213,24 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     P.rmax = F->L->rmax;
     P.hbmax = F->L->hbmax;
     P.eoff = F->L->run_slots ? F->L->eoff.p : nullptr;
+    P.ebound = nullptr;
+    if (F->L->run_slots && !getenv("PF_FAST_RS_WARP_EDGES")) {
+        // slot-balanced contiguous edge ranges, one per CTA (edge_phase_rs)
+        std::vector<int32_t> eoff(I.E + 1), eb(G + 1, (int32_t)I.E);
+        d2h(eoff.data(), F->L->eoff.p, I.E + 1, s);
+        PF_CUDA(cudaStreamSynchronize(s));
+        const int64_t tot = eoff[I.E];
+        int64_t e = 0;
+        for (int g = 0; g <= G; ++g) {
+            const int64_t want = tot * g / G;
+            while (e < I.E && eoff[e] < want) ++e;
+            eb[g] = (int32_t)(g == G ? I.E : e);
+        }
+        eb[0] = 0;
+        F->ebound.alloc(G + 1);
+        h2d(F->ebound.p, eb.data(), G + 1, s);
+        P.ebound = F->ebound.p;
+    }
     P.slots = F->L->run_slots ? F->slots.p : nullptr;
     P.res = F->res.p;
     P.res_dc = F->res_dc.p;
