@@ -608,7 +608,7 @@ def run_b200(args):
     del solver
     sharded_n1 = None
     if rank == 0 and args.sharded_config and args.sharded_config != args.config:
-        sharded_n1 = single_gpu_rate(args.sharded_config, local, steps=200, warmup=10)
+        sharded_n1 = single_gpu_rate(args.sharded_config, local, steps=1000, warmup=10)
     line = {
         "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
