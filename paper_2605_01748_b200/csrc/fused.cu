@@ -191,6 +191,9 @@ struct Ctrl {
     int32_t just_incremented, stopped, status, xc, db, need_a1, need_edge, pad;
     int64_t bad;
     uint64_t xepoch;  // multi-GPU exchanges done (mirrors *Params::xepoch)
+    double fspec;     // the rescale factor the M pass speculated (predict_f); a rollback iff f != fspec
+    double fnext;     // predict_f for the next M pass (set at the end of controller_step)
+    int64_t rollbacks;  // rollback passes run (statistics)
 };
 
 struct Params {
@@ -229,7 +232,9 @@ struct Params {
     // run slots (TileLayout::run_slots): every (tile, run) stores its {T, L} into
     // slots[2 * s], s in the edge's range eoff[e] .. eoff[e + 1] (tile order)
     int32_t run_slots, rmax;
-    int32_t hbmax, pad1;  // most hop-step entries of one tile (the shared-memory metadata bound)
+    int32_t hbmax;        // most hop-step entries of one tile (the shared-memory metadata bound)
+    int32_t spec_f;       // speculate the rescale factor (predict_f); 0: always f = 1 (PF_FAST_SPEC=0)
+    double spec_margin;   // predict_f's margin past the residual-ratio threshold (PF_FAST_SPEC_MARGIN)
     const int32_t *eoff;
     const int32_t *ebound;  // run slots, single GPU: CTA g sums edges ebound[g] .. ebound[g + 1] (slot-balanced)
     double *slots;
@@ -582,8 +587,30 @@ __device__ double dcs_block(const double *res_dc, int E) {
 
 // ------------------------------------------------------------------ controller
 
+// The dual rescale factor f_{k+1} the M pass applies speculatively to A(k+2):
+// the beta decision of controller.py:251-266 taken on the residual EMAs as
+// they stand before this iteration's residuals move them by 10%.  Certain when
+// adaptation is off or a cooldown is running (f = 1); during beta's ramp the
+// ratio of the EMAs sits far from the thresholds, so the prediction holds and
+// no rollback pass is needed.  A wrong prediction costs the rollback pass the
+// kernel always had (a recomputation of A(k+2) with the true f from the
+// intact duals_{k+1}): the iterates are bitwise those of the rollback path.
+__device__ __forceinline__ double predict_f(const Params &P, const Ctrl &c) {
+    if (!P.adapt || c.cooldown > 0 || c.ema_s < 0.0) return 1.0;
+    double b = c.beta;
+    const double m = P.spec_margin;  // predict a change only this far past the threshold
+    if (c.ema_r > m * P.residual_ratio * c.ema_s)
+        b = b * P.beta_scale;
+    else if (c.ema_s > m * P.residual_ratio * c.ema_r)
+        b = b / P.beta_scale;
+    const double lo = b > P.beta_min ? b : P.beta_min;
+    const double nb = lo < P.beta_max ? lo : P.beta_max;
+    return nb != c.beta ? c.beta / nb : 1.0;
+}
+
 // controller.py:237-273 on the residuals of the iteration just completed.
 __device__ __noinline__ void controller_step(const Params &P, Ctrl &c, double s, double r, int32_t ec, int32_t er) {
+    c.fspec = c.fnext;  // what the M pass applied
     c.s = s;
     c.r = r;
     c.f = 1.0;
@@ -644,6 +671,7 @@ __device__ __noinline__ void controller_step(const Params &P, Ctrl &c, double s,
         c.alpha += 1;
         c.just_incremented = 1;
     }
+    c.fnext = P.spec_f ? predict_f(P, c) : 1.0;  // off the next pass's start: its state is this one
 }
 
 // Every CTA reduces the residual partials in the same fixed order and runs the
@@ -1079,7 +1107,7 @@ __device__ PassIO pass_io(const Params &P, const Ctrl &c) {
         io.dn_out = P.dn[c.db ^ 1];
         io.dd_out = P.dd[c.db ^ 1];
         io.x_out = P.x[c.xc ^ 1];
-        io.f = 1.0;  // speculative f_{k+1}
+        io.f = c.fnext;  // speculative f_{k+1} (predict_f, taken by the previous controller step)
         io.par = (int)((c.iteration + 2) & 1);
     } else if (MODE == MODE_RB) {  // after the M pass flipped xc/db: duals_{k+1} in db^1, x_{k+1} in xc
         io.dcon_in = P.dcon[c.db ^ 1];
@@ -1148,7 +1176,10 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
     A.o_adj = sp.adj;
     A.o_adjt = sp.adjt;
     const int t0 = P.cta_ptr[g], my = P.cta_ptr[g + 1] - t0;
-    const bool rev = (c.iteration & 1) != 0;
+    // the rollback pass (after the iteration count moved on) walks in its M
+    // pass's direction: the CTA partials keep the M pass's association, so a
+    // speculated rescale factor gives bitwise the rollback path's iterates
+    const bool rev = ((MODE == MODE_RB ? c.iteration - 1 : c.iteration) & 1) != 0;
     auto tile_of = [&](int k) { return P.cta_tiles[t0 + (rev ? my - 1 - k : k)]; };
     // the next tile's descriptor from shared memory: no dependent global loads
     // on thread 0's path between two tiles (its TMA issue and L2 prefetch).  A
@@ -1485,7 +1516,8 @@ __global__ void __launch_bounds__(NT, PF_MINB) k_fused(const __grid_constant__ P
             controller_eval(P, c);
         }
         mark(4);
-        if (!c.stopped && !c.status && c.f != 1.0) {
+        if (!c.stopped && !c.status && c.f != c.fspec) {
+            if (threadIdx.x == 0) c.rollbacks += 1;
             (P.run_slots ? pass_tiles<MODE_RB, true>(P, c, smem_raw, cs, seq) : pass_tiles<MODE_RB, false>(P, c, smem_raw, cs, seq));
             grid.sync();
             if (dist) xchg_phase(P, c, grid);
@@ -1577,7 +1609,7 @@ __global__ void __launch_bounds__(NT) k_ctrl_dist(const __grid_constant__ Params
     *P.ctrl = c;
     if (in_graph) {
         const bool live = !c.stopped && !c.status;
-        cudaGraphSetConditional(h_rb, live && c.f != 1.0 ? 1u : 0u);
+        cudaGraphSetConditional(h_rb, live && c.f != c.fspec ? 1u : 0u);
         cudaGraphSetConditional(h_loop, live && c.iteration < c.target && c.iteration < P.max_iterations ? 1u : 0u);
     }
 }
@@ -2212,6 +2244,8 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     P.run_slots = F->L->run_slots ? 1 : 0;
     P.rmax = F->L->rmax;
     P.hbmax = F->L->hbmax;
+    P.spec_f = !getenv("PF_FAST_SPEC") || atoi(getenv("PF_FAST_SPEC")) != 0;
+    P.spec_margin = getenv("PF_FAST_SPEC_MARGIN") ? atof(getenv("PF_FAST_SPEC_MARGIN")) : 1.5;
     P.eoff = F->L->run_slots ? F->L->eoff.p : nullptr;
     P.ebound = nullptr;
     if (F->L->run_slots && !getenv("PF_FAST_RS_WARP_EDGES")) {
@@ -2407,7 +2441,7 @@ static int64_t fast_run_dist(FastSolver *F, int64_t max_steps, cudaStream_t s, f
         PF_CHECK_LAUNCH();
         F->launches += 5;
         c = read();
-        if (!c.stopped && !c.status && c.f != 1.0) {
+        if (!c.stopped && !c.status && c.f != c.fspec) {
             k_pass<MODE_RB><<<F->G, NT, F->smem, s>>>(F->P);
             PF_CHECK_LAUNCH();
             reduce_allreduce();
@@ -2483,6 +2517,7 @@ void fast_init(FastSolver *F, const double *d_x0, int64_t alpha0, double beta0, 
     c.beta = c.beta_used = beta0;
     c.ema_s = c.ema_r = -1.0;
     c.f = 1.0;
+    c.fspec = c.fnext = 1.0;
     c.alpha = c.alpha_used = alpha0;
     c.s = c.r = NAN;
     c.bad = -1;
@@ -2602,6 +2637,9 @@ int64_t fast_run(FastSolver *F, int64_t max_steps, cudaStream_t s, float *ms) {
         PF_CUDA(cudaMemcpyToSymbol(g_tprobe, z, sizeof(z)));
     }
 #endif
+    if (getenv("PF_FAST_DEBUG"))
+        fprintf(stderr, "[fast run] iterations %lld, rollback passes so far %lld\n", (long long)c.iteration,
+                (long long)c.rollbacks);
     return c.iteration - start;
 }
 

@@ -536,6 +536,27 @@ def test_fast_projection_pipelined_trim_bitwise():
     assert outs[0]["digests"][0] == outs[1]["digests"][0]
 
 
+def test_speculated_rescale_bitwise():
+    """The M pass applies the predicted dual rescale factor (predict_f) instead
+    of 1, and a rollback pass runs only on a wrong prediction: the iterates
+    (several tiles per CTA, beta's ramp and its plateau) are bitwise those of
+    the always-1 speculation with its rollback on every beta change."""
+    import json
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    outs = []
+    for spec in ("0", "1"):
+        env = dict(os.environ, PF_FAST_SPEC=spec)
+        r = subprocess.run([sys.executable, os.path.join(here, "_spec_variant.py"), "150", "4", "400"], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0] == outs[1]
+    assert outs[0]["beta"] > 1.0  # beta moved: the rollback / speculation paths ran
+
+
 def test_fast_trace_batched_rows_equal_per_row_path():
     """Traced fast runs without an optimality column compute their rows on the
     device in batches (no host round trip per iteration); with reference sums
