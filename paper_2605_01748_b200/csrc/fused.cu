@@ -71,7 +71,7 @@ constexpr int GPATH = 32;         // max paths per group (one lane per path)
 constexpr int TPATH = NW * GPATH; // max paths per tile
 constexpr int TCOM = TPATH;       // max commodities per tile
 static_assert(TPATH <= 256, "tile-local path / commodity indices are u8");
-static_assert(3 * 8 * (TPATH + 2) >= NT * 17, "the edge-run head pieces reuse the stage's per-path arrays");
+static_assert(3 * 8 * (TPATH + 2) >= NT * 16, "the edge-run head pieces reuse the stage's per-path arrays");
 constexpr int TPS_MIN = 2560;     // default max pairs per tile (large-E layouts)
 constexpr int TPS_CAP = 4096;     // upper bound of the shared-memory fit (two CTAs per SM)
 constexpr int SLOT_ALIGN = 16;    // tile start alignment in the per-pair arrays (128 B)
@@ -93,7 +93,7 @@ __host__ __device__ __forceinline__ int even(int n) { return (n + 1) & ~1; }
 // sections follow: the run's edge and its global slot (the edge-major position
 // of this (tile, run) among all tiles that touch the edge).
 struct MetaOff {
-    int eid, sperm, poff, pcom, cpp, gpath, hbo, hb, hperm, hinv, redge, rdst, bytes;
+    int eid, sperm, poff, pcom, cpp, gpath, hbo, hb, hperm, hinv, xlen, redge, rdst, bytes;
 };
 __host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc, int nrun, int nhb, bool rs = false) {
     MetaOff m;
@@ -121,6 +121,8 @@ __host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc, 
     o += r16(npath);
     m.hinv = o;  // u8 [npath] per group: the hop lane of each path
     o += r16(npath);
+    m.xlen = o;  // u16 [NT] per walk chunk: how many following chunks its tail's crossing run reaches (0: none)
+    o += r16(2 * NT);
     m.redge = o;  // run slots: u16 [nrun] edge of each run
     if (rs) o += r16(2 * nrun);
     m.rdst = o;  // run slots: u32 [nrun] global slot of each run's {T, L}
@@ -1030,7 +1032,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
         const double *yv = (const double *)(g_smem + A.o_y);
         // head pieces: the stage's per-path arrays are dead once step 3 is done
         double2 *hp = (double2 *)(g_smem + st.o_xk);
-        uint8_t *hf = (uint8_t *)(hp + NT);  // 0 none, 1 a head piece, 2 the whole chunk continues
+        const uint16_t *xlen = (const uint16_t *)(g_smem + st.o_meta + m.xlen);
         const int cs = max((np + NT - 1) / NT, 4);  // small tiles: fewer, longer chunks (fewer crossings)
         const int a0 = tid * cs, b0 = min(a0 + cs, np);
         double T = 0.0, L = 0.0;
@@ -1078,15 +1080,16 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
                 flag = 2;
             }
         }
-        hf[tid] = (uint8_t)flag;
+        (void)flag;
         TP(6)
         __syncthreads();
-        if (inside) {  // this chunk's tail begins a run that crosses into the next chunks
-            for (int k = tid + 1; k < NT; ++k) {
-                const double2 v = hp[k];
+        const int nx = inside ? (int)xlen[tid] : 0;  // static: the layout knows which chunks a run crosses
+        if (nx > 0) {  // this chunk's tail begins a run that crosses into the next nx chunks
+#pragma unroll 4
+            for (int k = 1; k <= nx; ++k) {
+                const double2 v = hp[tid + k];
                 T += v.x;
                 L += v.y;
-                if (hf[k] != 2) break;
             }
             acc_add<MODE, RS>(A, rdst, cur, T, L);
         }
@@ -1972,6 +1975,22 @@ static std::shared_ptr<TileLayout> build_tiles(const pf_instance *inst, cudaStre
         const int nr = (int)rstart.size();
         require(nr == T.nrun, "fast layout: run count mismatch");
         rstart.push_back(np);
+        {  // the walk's chunks (tile_compute step 5: cs items per thread): for each
+           // chunk whose last item's run began inside it and continues, the number
+           // of following chunks that run reaches (their head pieces are added
+           // to it in chunk order)
+            uint16_t *xlen = (uint16_t *)(blk + m.xlen);
+            const int cs = std::max((np + NT - 1) / NT, 4);
+            int r = 0;
+            for (int t = 0; t < NT; ++t) {
+                xlen[t] = 0;
+                const int a = t * cs, b = std::min(a + cs, np);
+                if (a >= b) continue;
+                while (rstart[r + 1] <= b - 1) ++r;  // the run holding item b - 1
+                const int s0 = rstart[r], s1 = rstart[r + 1];
+                if (s0 >= a && s1 > b) xlen[t] = (uint16_t)((s1 - b + cs - 1) / cs);
+            }
+        }
         if (L->run_slots) {  // the run's edge; the per-pair u16 becomes the pair's run
             uint16_t *redge = (uint16_t *)(blk + m.redge);
             for (int r = 0; r < nr; ++r) redge[r] = eid[sperm[rstart[r]] & 0x7fff];
