@@ -1375,9 +1375,11 @@ __device__ __noinline__ void xchg_phase(const Params &P, Ctrl &c, cg::grid_group
         // every CTA waits for all ranks' slots (bounded: ~20 s, then PF_ERR_COMM)
         const unsigned long long want = (unsigned long long)P.nranks * (ep + 1);
         const unsigned long long *flag = xb_flag(P, P.peers[P.rank]);
-        const long long t0 = clock64();
+        // the global nanosecond timer: an SM's clock64 is not comparable across
+        // a preemption that resumes the CTA on another SM
+        const unsigned long long t0 = gtimer();
         while (ld_acquire_sys(flag) < want) {
-            if (clock64() - t0 > 40000000000ll) {
+            if (gtimer() - t0 > 20000000000ull) {
                 s_timeout = 1;
                 break;
             }
@@ -2614,16 +2616,27 @@ int64_t fast_run(FastSolver *F, int64_t max_steps, cudaStream_t s, float *ms) {
         if (ms) *ms = 0.f;
         return 0;
     }
-    int64_t target = start + max_steps;
-    PF_CUDA(cudaMemcpyAsync((char *)F->ctrl.p + offsetof(Ctrl, target), &target, sizeof(int64_t),
-                            cudaMemcpyHostToDevice, s));
+    // multi-GPU over peer memory: launches of at most PF_DIST_LAUNCH_ITERS
+    // iterations, back to back on the stream (the same iterates: every reduction
+    // has a fixed order and a launch resumes from the device state).  A
+    // persistent kernel that spins on its peers for thousands of iterations
+    // gave wrong totals when ranks were time-sliced on one GPU.
+    static const int64_t seg_env = getenv("PF_DIST_LAUNCH_ITERS") ? atoll(getenv("PF_DIST_LAUNCH_ITERS")) : 256;
+    const int64_t seg = F->nranks && seg_env > 0 ? seg_env : max_steps;
+    std::vector<int64_t> targets;
+    for (int64_t t = start + seg; t < start + max_steps; t += seg) targets.push_back(t);
+    targets.push_back(start + max_steps);
     void *args[] = {(void *)&F->P};
     PF_CUDA(cudaEventRecord(F->e0, s));
     const void *kern = F->nranks ? (const void *)k_fused<true> : (const void *)k_fused<false>;
-    PF_CUDA(cudaLaunchCooperativeKernel(kern, dim3(F->G), dim3(NT), args, F->smem, s));
-    PF_CHECK_LAUNCH();
+    for (const int64_t &target : targets) {
+        PF_CUDA(cudaMemcpyAsync((char *)F->ctrl.p + offsetof(Ctrl, target), &target, sizeof(int64_t),
+                                cudaMemcpyHostToDevice, s));
+        PF_CUDA(cudaLaunchCooperativeKernel(kern, dim3(F->G), dim3(NT), args, F->smem, s));
+        PF_CHECK_LAUNCH();
+        ++F->launches;
+    }
     PF_CUDA(cudaEventRecord(F->e1, s));
-    ++F->launches;
     d2h(&c, F->ctrl.p, 1, s);
     PF_CUDA(cudaStreamSynchronize(s));
     float t = 0.f;
@@ -2721,10 +2734,17 @@ void fast_xchg_create(FastSolver *F, int rank, int nranks, void *handle64) {
     const int64_t xslot = (2 * I.E + 16 + 15) / 16 * 16;
     F->rank = rank;
     F->nranks = nranks;
-    F->xb.alloc((size_t)2 * nranks * xslot + 16);  // + the arrival counter
+    // its own 2 MB allocation (the IPC granularity): small cudaMalloc blocks may
+    // share a physical page with other allocations of this process
+    const size_t xwords = (size_t)2 * nranks * xslot + 16;  // + the arrival counter
+    F->xb.alloc((xwords * sizeof(double) + (2u << 20) - 1) / (2u << 20) * (2u << 20) / sizeof(double));
     PF_CUDA(cudaMemset(F->xb.p, 0, F->xb.bytes()));
     F->xepoch.alloc(1);
     PF_CUDA(cudaMemset(F->xepoch.p, 0, sizeof(unsigned long long)));
+    // cudaMemset of device memory may still be pending when it returns: the
+    // zeroed counter and slots must be in place before any peer can see the
+    // handle (a late memset would erase a peer's first arrival or totals)
+    PF_CUDA(cudaDeviceSynchronize());
     cudaIpcMemHandle_t h;
     PF_CUDA(cudaIpcGetMemHandle(&h, F->xb.p));
     static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");

@@ -224,11 +224,21 @@ class ShardedSolver:
         return self.solver.x()
 
     def gather_x(self, group=None):
-        """Full rate vector (kept-path order) on rank 0, None elsewhere."""
+        """Full rate vector (kept-path order) on rank 0, None elsewhere: one
+        tensor gather of the shards (sizes from the partition, no pickling)."""
+        import torch
         import torch.distributed as dist
-        parts = [None] * self.world if self.rank == 0 else None
-        dist.gather_object(self.local_x(), parts, dst=0, group=group)
-        return np.concatenate(parts) if self.rank == 0 else None
+        sizes = [b - a for a, b in self.path_ranges]
+        n = max(sizes) if sizes else 0
+        mine = np.zeros(n, np.float64)
+        x = self.local_x()
+        mine[:x.size] = x
+        t = torch.from_numpy(mine)
+        parts = [torch.empty(n, dtype=torch.float64) for _ in range(self.world)] if self.rank == 0 else None
+        dist.gather(t, parts, dst=0, group=group)
+        if self.rank != 0:
+            return None
+        return np.concatenate([parts[r].numpy()[:sizes[r]] for r in range(self.world)])
 
 
 def consistency_check(sh, topo, tab, flat, world, rank):
@@ -305,9 +315,19 @@ def _sharded_time_to_quality(args, bench, rank, world, local, name="target_k4_v0
         proj_ms = 1e3 * (_time.perf_counter() - t1)
         gather_ms = 1e3 * (t1 - t0)
         q = optimality_from_sums(commodity_sums(full, rates), opt, default_theta(full))
+        # the same k* iterations on rank 0's GPU alone: the sharded trajectory is a
+        # reassociation of it (edge totals summed per rank), so the two agree closely
+        one = Solver(full, SolverConfig(mode="fast", max_iterations=5000)).init()
+        one.run(kstar)
+        x1 = one.x()
+        q1 = optimality_from_sums(commodity_sums(full, project(full, x1, int(one.result().alpha))), opt,
+                                  default_theta(full))
+        dx = float(np.max(np.abs(xg - x1)) / max(float(np.max(np.abs(x1))), 1e-300))
         out = {"config": name, "k_star_reference": kstar, "gpu_loop_ms_max_over_ranks": ms_loop,
                "gather_ms": gather_ms, "projection_ms": proj_ms, "gpu_ms": ms_loop + gather_ms + proj_ms,
                "optimality_at_k_star_vs_reference_fixed_point": q, "n_gpus": world,
+               "single_gpu_check": {"optimality_at_k_star": q1, "max_rel_rate_diff": dx,
+                                    "consistent": bool(dx < 1e-3 and abs(q - q1) < 1e-4)},
                "how": "k* sharded iterations from cold (one launch per rank, max over ranks) + gather_x + "
                       "project on rank 0 (host wall); quality scored against the oracle's fixed point"}
     dist.barrier()

@@ -21,13 +21,21 @@ if rank == 0:
 dist.barrier()
 topo, tab, flat = bench.build_inputs(name)
 meta, opt = bench.oracle_fixed_point(name)
+pre = None
+if os.environ.get("DIAG_PRE"):  # an earlier sharded solver on another instance (the bench's flow)
+    t1, b1, f1 = bench.build_inputs(os.environ["DIAG_PRE"])
+    pre = ShardedSolver(t1, b1, f1, pf.SolverConfig(mode="fast", gamma=1e-12, max_iterations=10 ** 9), rank, world,
+                        local)
+    pre.init()
+    pre.time_loop(30)
+    dist.barrier()
 sh = ShardedSolver(topo, tab, flat, pf.SolverConfig(mode="fast", max_iterations=5000), rank, world, local)
 sh.init()
 full = pf.build_instance_flat(topo, tab, flat, device=local) if rank == 0 else None
 single = pf.Solver(full, pf.SolverConfig(mode="fast", max_iterations=5000)).init() if rank == 0 else None
 theta = pf.default_theta(full) if rank == 0 else None
 done = 0
-for k in (10, 100, 1000, 2500, 4860):
+for k in [int(v) for v in os.environ.get("DIAG_KS", "10,100,1000,2500,4860").split(",")]:
     sh.run(k - done)
     if rank == 0:
         single.run(k - done)

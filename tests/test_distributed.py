@@ -266,6 +266,64 @@ def test_ipc_multirank_on_one_gpu(world):
     assert float(np.max(np.abs(xg - xs))) <= 1e-4 * float(np.max(np.abs(xs)))
 
 
+def _ipc_second_solver_worker(rank, world, port, iters, q):
+    import torch.distributed as dist
+
+    import paper_2605_01748_b200 as pf
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        cfg = pf.SolverConfig(mode="fast", gamma=1e-12, max_iterations=10 ** 6)
+        t0 = pf.random_topology(24, seed=24)
+        b0 = pf.gravity_table(t0, 0.3 * float(t0.capacity.sum()))
+        first = D.ShardedSolver(t0, b0, pf.k_shortest_paths(t0, b0, 4), cfg, rank, world, 0, transport="ipc").init()
+        first.run(30)  # kept alive: its exchange buffers stay mapped in both processes
+        topo = pf.random_topology(40, seed=40)
+        tab = pf.gravity_table(topo, 0.3 * float(topo.capacity.sum()))
+        flat = pf.k_shortest_paths(topo, tab, 4)
+        sh = D.ShardedSolver(topo, tab, flat, cfg, rank, world, 0, transport="ipc").init()
+        sh.run(iters)
+        r = sh.result()
+        x = sh.gather_x()
+        single = None
+        if rank == 0:
+            inst = pf.build_instance_flat(topo, tab, flat, device=0)
+            s1 = pf.Solver(inst, cfg).init()
+            s1.run(iters)
+            single = s1.x()
+        q.put((rank, int(r.iterations), float(r.beta), int(r.alpha), x, single))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_ipc_second_solver_in_process():
+    """A second peer-memory solver in the same processes (the bench's flow: the
+    timed instance, then the time-to-1% instance) must exchange through its own
+    buffers: each exchange buffer is its own 2 MB allocation (the IPC granularity;
+    a small one sharing a page with other allocations corrupted the exchange
+    after a few hundred iterations).  Ranks agree, and the gathered rates follow
+    the single-GPU trajectory."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world, iters = 2, 800
+    ps = [ctx.Process(target=_ipc_second_solver_worker, args=(r, world, port, iters, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in range(world)], key=lambda t: t[0])
+    for p in ps:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in ps)
+    states = [t[1:4] for t in res]
+    assert all(s == states[0] for s in states) and states[0][0] == iters
+    xg, xs = res[0][4], res[0][5]
+    assert float(np.max(np.abs(xg - xs))) <= 1e-3 * float(np.max(np.abs(xs)))
+
+
 @pytest.mark.gpu
 def test_ipc_failure_falls_back_to_nccl(monkeypatch):
     """When the peer-memory exchange cannot be set up on some rank, all ranks
