@@ -342,6 +342,20 @@ __global__ void k_edge_path_keys_violated(InstView I, const double *scores, cons
     vals[t] = p;
 }
 
+// alpha = 0: a path's score is its count of violated edges (S^0 = 1), an
+// integer <= hmax, so the descending stable order is the ascending stable order
+// of hmax - count: a few-bit radix key (one sort pass instead of eight)
+__global__ void k_edge_path_keys_violated_count(InstView I, const double *scores, const double *over, int32_t hmax,
+                                                uint64_t *keys, int32_t *vals) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= I.NP) return;
+    int32_t pr = I.edge_pairs[t];
+    if (!(over[I.pair_edge[pr]] > 0.0)) return;
+    int32_t p = I.pair_path[pr];
+    keys[t] = (uint64_t)(hmax - (int32_t)scores[p]);
+    vals[t] = p;
+}
+
 __global__ void k_edge_paths(InstView I, int32_t *epath) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t < I.NP) epath[t] = I.pair_path[I.edge_pairs[t]];
@@ -798,6 +812,7 @@ struct ProjWS {
     DevBuf<char> cub;
     size_t cub_bytes = 0;
     int32_t max_ne = 0;
+    int32_t max_hops = 0;  // most edges of one path (the alpha = 0 score bound)
 };
 
 static ProjWS &workspace(const pf_instance *inst, cudaStream_t s) {
@@ -840,6 +855,12 @@ static ProjWS &workspace(const pf_instance *inst, cudaStream_t s) {
     PF_CUDA(cudaStreamSynchronize(s));
     lap("edge paths + sync");
     for (int32_t e = 0; e < I.E; ++e) ws->max_ne = std::max(ws->max_ne, eptr[e + 1] - eptr[e]);
+    {
+        std::vector<int32_t> pptr(I.P + 1);
+        d2h(pptr.data(), I.pair_ptr, I.P + 1, s);
+        PF_CUDA(cudaStreamSynchronize(s));
+        for (int64_t p = 0; p < I.P; ++p) ws->max_hops = std::max(ws->max_hops, pptr[p + 1] - pptr[p]);
+    }
     ws->parts.alloc((ws->max_ne + BLK - 1) / BLK + 1);
     size_t a = 0, b = 0;
     PF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, a, ws->ekeys.p, ws->ekeys_out.p, ws->eids.p, ws->eorder.p,
@@ -921,13 +942,22 @@ void project_device(const pf_instance *inst, const double *rates, int64_t alpha,
     // projection.py:81 (post-phase-2 rates): the loads of these rates were just computed
     score_paths_ws(inst, ws, x, alpha, ws.scores.p, s, fast, true);
     if (I.E) k_violated_segments<<<ceil_div(I.E, TB), TB, 0, s>>>(I.E, ws.over.p, I.edge_pair_ptr, ws.sb.p, ws.se.p);
-    if (I.NP) k_edge_path_keys_violated<<<ceil_div(I.NP, TB), TB, 0, s>>>(I, ws.scores.p, ws.over.p, ws.pkeys.p,
-                                                                         ws.pvals.p);
+    int end_bit = 64;
+    if (alpha == 0) {
+        end_bit = 1;
+        while ((1ll << end_bit) <= ws.max_hops) ++end_bit;
+        if (I.NP)
+            k_edge_path_keys_violated_count<<<ceil_div(I.NP, TB), TB, 0, s>>>(I, ws.scores.p, ws.over.p, ws.max_hops,
+                                                                            ws.pkeys.p, ws.pvals.p);
+    } else if (I.NP) {
+        k_edge_path_keys_violated<<<ceil_div(I.NP, TB), TB, 0, s>>>(I, ws.scores.p, ws.over.p, ws.pkeys.p,
+                                                                  ws.pvals.p);
+    }
     PF_CHECK_LAUNCH();
     if (I.NP) {
         size_t bytes = ws.cub_bytes;
         PF_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(ws.cub.p, bytes, ws.pkeys.p, ws.pkeys_out.p, ws.pvals.p,
-                                                         ws.porder.p, I.NP, I.E, ws.sb.p, ws.se.p, 0, 64, s));
+                                                         ws.porder.p, I.NP, I.E, ws.sb.p, ws.se.p, 0, end_bit, s));
     }
     static const int stats = (getenv("PF_PROJ_STATS") ? 1 : 0) | (getenv("PF_PROJ_ABLATE") ? 2 : 0);  // 2: timing ablation
     PF_CUDA(cudaMemsetAsync(ws.dirty.p, 0, I.E + 1, s));
