@@ -136,7 +136,7 @@ __host__ __device__ __forceinline__ MetaOff meta_off(int np, int npath, int nc, 
 // tile's runs (at most rmax) instead.
 struct SmemPlan {
     int stage, s_dcon, s_meta, s_xk, s_xo, s_dn, s_D, s_dd;  // offsets inside a stage
-    int y, adj, acc, adjt, total;                           // offsets from the base
+    int y, adj, acc, adjt, hp, total;                       // offsets from the base
 };
 __host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E, int nbuf, int hbmax, bool adj_smem = true,
                                                       bool acc_smem = true, bool rs = false, int rmax = 0) {
@@ -166,6 +166,8 @@ __host__ __device__ __forceinline__ SmemPlan smem_plan(int tps, int E, int nbuf,
     if (acc_smem && !rs) o += r16(16 * E);
     s.adjt = o;  // run slots: adjustment of each of the tile's runs
     if (rs) o += r16(8 * rmax);
+    s.hp = o;  // the edge-run walk's head pieces (outside the stage: the next tile's copy may start early)
+    o += 16 * NT;
     s.total = o;
     return s;
 }
@@ -780,7 +782,7 @@ struct Acc {
     double *adjt;           // run slots: the tile's per-run adjustment table
     uint32_t adjt_s;
     double *slots;          // run slots: the global {T, L} slots
-    int o_y, o_adj, o_adjt; // byte offsets from the dynamic shared-memory base
+    int o_y, o_adj, o_adjt, o_hp;  // byte offsets from the dynamic shared-memory base
 };
 
 template <int MODE, bool RS>
@@ -887,7 +889,8 @@ __device__ __forceinline__ double hops_dcon(int hb_o, int H, int lane, double xn
 template <int MODE, bool RS>
 __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, const PassIO &io, const TileDesc &d,
                                              const StageView &st, const Acc &A, double &r_x,
-                                             double &r_dd, double &r_dcon, double &r_dn) {
+                                             double &r_dd, double &r_dcon, double &r_dn, const TileDesc *next,
+                                             TileDesc *sd_slot, char *base, const SmemPlan &sp, uint64_t *bar) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int np = d.np, npath = d.p1 - d.p0, nc = d.c1 - d.c0;
     const MetaOff m = meta_off(np, npath, nc, d.nrun, d.nhb, RS);
@@ -1031,7 +1034,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
         const double *tv = (const double *)(g_smem + st.o_dcon);             // x' + dcon' (step 3)
         const double *yv = (const double *)(g_smem + A.o_y);
         // head pieces: the stage's per-path arrays are dead once step 3 is done
-        double2 *hp = (double2 *)(g_smem + st.o_xk);
+        double2 *hp = (double2 *)(g_smem + A.o_hp);
         const uint16_t *xlen = (const uint16_t *)(g_smem + st.o_meta + m.xlen);
         const int cs = max((np + NT - 1) / NT, 4);  // small tiles: fewer, longer chunks (fewer crossings)
         const int a0 = tid * cs, b0 = min(a0 + cs, np);
@@ -1081,9 +1084,18 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
             }
         }
         (void)flag;
+        // what phase 2 needs from the stage, read before the stage is released
+        const int nx = inside ? (int)xlen[tid] : 0;  // static: the layout knows which chunks a run crosses
+        const uint32_t rd1 = RS && nx > 0 ? rdst[cur] : 0u;
         TP(6)
         __syncthreads();
-        const int nx = inside ? (int)xlen[tid] : 0;  // static: the layout knows which chunks a run crosses
+        // the stage is free: the next tile's bulk copies overlap phase 2 and the
+        // end-of-tile barrier (single-stage layout)
+        if (next && tid == 0) {  // (every thread read this tile's descriptor long ago)
+            *sd_slot = *next;
+            fence_proxy_async_shared();
+            issue_tile<MODE, RS>(P, io, *sd_slot, base, sp, 0, bar);
+        }
         if (nx > 0) {  // this chunk's tail begins a run that crosses into the next nx chunks
 #pragma unroll 4
             for (int k = 1; k <= nx; ++k) {
@@ -1091,7 +1103,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
                 T += v.x;
                 L += v.y;
             }
-            acc_add<MODE, RS>(A, rdst, cur, T, L);
+            acc_add<MODE, RS>(A, &rd1, RS ? 0 : cur, T, L);  // (run slots: the slot read above)
         }
     }
     TP(4)
@@ -1178,6 +1190,7 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
     A.o_y = sp.y;
     A.o_adj = sp.adj;
     A.o_adjt = sp.adjt;
+    A.o_hp = sp.hp;
     const int t0 = P.cta_ptr[g], my = P.cta_ptr[g + 1] - t0;
     // the rollback pass (after the iteration count moved on) walks in its M
     // pass's direction: the CTA partials keep the M pass's association, so a
@@ -1191,6 +1204,9 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
     const bool keep = my <= DL && cs.dl_rev >= 0;
     const bool flip = keep && cs.dl_rev != (rev ? 1 : 0);
     auto desc_of = [&](int k) -> TileDesc { return k < DL ? cs.dl[flip ? my - 1 - k : k] : P.desc[tile_of(k)]; };
+    auto desc_ptr = [&](int k) -> const TileDesc * {
+        return k < DL ? &cs.dl[flip ? my - 1 - k : k] : &P.desc[tile_of(k)];
+    };
     const bool dbl = P.nbuf == 2;
     if (tid == 0) {
         cs.io = pass_io<MODE>(P, c);
@@ -1258,7 +1274,11 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
 #endif
         const TileDesc d = cs.sd[b];
         const StageView st = stage_view(base, sp, b, d);
-        tile_compute<MODE, RS>(P, c, io, d, st, A, r_x, r_dd, r_dcon, r_dn);
+        // single stage: the next tile's copies are issued from inside the tile,
+        // as soon as its stage is released (after the edge-run walk's first phase)
+        const bool early = !dbl && k + 1 < my;
+        tile_compute<MODE, RS>(P, c, io, d, st, A, r_x, r_dd, r_dcon, r_dn, early ? desc_ptr(k + 1) : nullptr,
+                               &cs.sd[0], base, sp, &cs.bar[0]);
 #ifdef PF_TPROBE
         const unsigned long long tb0 = clock64();
 #endif
@@ -1266,10 +1286,7 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
 #ifdef PF_TPROBE
         if (tid == 0) atomicAdd(&g_tprobe[5], clock64() - tb0);
 #endif
-        if (!dbl && tid == 0 && k + 1 < my) {  // before the fix-ups (they do not touch the stage)
-            cs.sd[0] = desc_of(k + 1);
-            issue_tile<MODE, RS>(P, io, cs.sd[0], base, sp, 0, &cs.bar[0]);
-        }
+
     }
     for (int e = tid; e < E; e += NT) {
         if (!P.acc_smem) break;  // the rows are the partials already
