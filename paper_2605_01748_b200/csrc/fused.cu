@@ -1091,7 +1091,9 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
         __syncthreads();
         // the stage is free: the next tile's bulk copies overlap phase 2 and the
         // end-of-tile barrier (single-stage layout)
-        if (next && tid == 0) {  // (every thread read this tile's descriptor long ago)
+        // (the last thread: its walk chunk is the tile's tail, usually short or
+        // empty, so the copies do not delay a crossing run's owner)
+        if (next && tid == NT - 1) {  // (every thread read this tile's descriptor long ago)
             *sd_slot = *next;
             fence_proxy_async_shared();
             issue_tile<MODE, RS>(P, io, *sd_slot, base, sp, 0, bar);
