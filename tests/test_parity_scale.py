@@ -195,3 +195,24 @@ def test_time_to_quality_one_device_pass(name):
     ref = pf.Solver(inst, pf.SolverConfig(mode="fast", max_iterations=5000)).init()
     ref.run(k)
     assert np.array_equal(ref.x(), dev.x())
+
+
+def test_time_to_quality_edges():
+    """pf_solver_time_to_quality's edge behaviour: an unreachable target runs
+    to the controller's stop and reports no k*; an exact-mode solver is refused
+    (the search replays fused-kernel snapshots); a reference vector of the
+    wrong length is an InputError."""
+    from b200_helpers import generated
+    topo, tab, ps = generated(24, 4, 0.3)
+    inst = pf.build_instance(topo, tab, ps, device=0)
+    ref = pf.solve(inst, pf.SolverConfig(mode="exact")).sums
+    s = pf.Solver(inst, pf.SolverConfig(mode="fast", max_iterations=300)).init()
+    out = s.time_to_quality(ref, 1.5, sample_every=16)
+    assert out["k_star"] is None
+    assert out["iterations"] == int(s.result().iterations) <= 300
+    assert len(out["samples"]) >= 1 and all(q <= 1.0 for _, q in out["samples"])
+    ex = pf.Solver(inst, pf.SolverConfig(mode="exact")).init()
+    with pytest.raises(pf.InputError):
+        ex.time_to_quality(ref, 0.99)
+    with pytest.raises(pf.InputError):
+        pf.Solver(inst, pf.SolverConfig(mode="fast")).init().time_to_quality(ref[:-1], 0.99)
