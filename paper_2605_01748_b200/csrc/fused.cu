@@ -1284,7 +1284,13 @@ __device__ __noinline__ void pass_tiles(const Params &P, const Ctrl &c, char *ba
 #ifdef PF_TPROBE
         const unsigned long long tb0 = clock64();
 #endif
-        __syncthreads();  // the stage is free for the next TMA (its generic writes were proxy-fenced)
+        // With the next tile's copies already issued (early), no barrier here: the
+        // walk's second phase only reads the head pieces and adds to the edge
+        // accumulators, and the next tile touches neither before its own block
+        // barrier after dual_consensus; the copies' mbarrier arrival (release)
+        // publishes the next descriptor.  Otherwise (a CTA's last tile: the
+        // accumulator flush follows; the double-buffered stage) the barrier stays.
+        if (!early) __syncthreads();
 #ifdef PF_TPROBE
         if (tid == 0) atomicAdd(&g_tprobe[5], clock64() - tb0);
 #endif
