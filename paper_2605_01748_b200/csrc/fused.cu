@@ -1039,7 +1039,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
         const int cs = max((np + NT - 1) / NT, 4);  // small tiles: fewer, longer chunks (fewer crossings)
         const int a0 = tid * cs, b0 = min(a0 + cs, np);
         double T = 0.0, L = 0.0;
-        int cur = -1, flag = 0;
+        int cur = -1;
         bool inside = false;  // the current piece started inside this chunk
         if (a0 < b0) {
             // sperm: bit 15 marks the first pair of a run, bits 0-14 the pair;
@@ -1058,8 +1058,7 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
                     if (inside) {
                         acc_add<MODE, RS>(A, rdst, cur, T, L);
                     } else {
-                        hp[tid] = make_double2(T, L);
-                        flag = 1;
+                        hp[tid] = make_double2(T, L);  // this chunk's head piece
                     }
                     cur = e;
                     inside = true;
@@ -1074,16 +1073,13 @@ __device__ __forceinline__ void tile_compute(const Params &P, const Ctrl &c, con
                 if (inside) {
                     acc_add<MODE, RS>(A, rdst, cur, T, L);
                 } else {
-                    hp[tid] = make_double2(T, L);
-                    flag = 1;
+                    hp[tid] = make_double2(T, L);  // this chunk's head piece
                 }
                 inside = false;  // nothing left to finish
             } else if (!inside) {
                 hp[tid] = make_double2(T, L);  // the whole chunk lies inside one crossing run
-                flag = 2;
             }
         }
-        (void)flag;
         // what phase 2 needs from the stage, read before the stage is released
         const int nx = inside ? (int)xlen[tid] : 0;  // static: the layout knows which chunks a run crosses
         const uint32_t rd1 = RS && nx > 0 ? rdst[cur] : 0u;
