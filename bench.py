@@ -414,6 +414,11 @@ def reference_numba(name, cpp, pep, pe, iterations=2):
     C port; the arm's value stays the port's."""
     if not os.path.isdir(os.path.join(REF_DIR, "pathfair")):
         return {"unavailable": "baseline/_ref not installed (pip install --target baseline/_ref the reference)"}
+    if int(pe.size) > 50_000_000:
+        # the reference's build_instance takes a nested-tuple PathSet: at config 3
+        # (355M pairs) that is tens of GB of Python objects and hours of work
+        return {"unavailable": f"{int(pe.size):,} pairs: the reference's PathSet (nested Python tuples) does not "
+                               f"fit a bounded run; timed at config 2 instead"}
     import tempfile
     n, k, vol, _ = CONFIGS[name]
     with tempfile.TemporaryDirectory() as td:
