@@ -224,7 +224,7 @@ struct Params {
     double *tot;            // [2E + 16] rank totals (multi-GPU): T, L, residual sums, error counts
     double *partT, *partL;  // [E][G]: edge-major, so one edge's CTA partials are contiguous
     double *res;            // [G][8]: 0 dx | 1..3 (dd, dcon, dn) parity 0 | 4..6 parity 1
-    double *res_dc;         // [E] squared dual_capacity change per edge
+    double *res_dc;         // [2][E] squared dual_capacity change per edge (halves by iteration parity)
     double *root_sums;      // [C] or null
     Ctrl *ctrl;
     int32_t *err;           // [2]: bad_coef, bad_root (INT_MAX = none)
@@ -247,6 +247,8 @@ struct Params {
 // Iteration-phase probe (tuning only, PF_FAST_PROBE): %globaltimer deltas of
 // CTA 0, thread 0, summed into g_probe[phase] (ns).
 __device__ unsigned long long g_probe[8];
+// first exchange whose slots carried the wrong epoch tag: {epoch + 1, rank, tag, iteration, counter}
+__device__ unsigned long long g_xdebug[5];
 // Tile-phase probe (tuning builds only, -DPF_TPROBE): clock64 deltas of thread 0
 // of every CTA per tile phase, summed over tiles and CTAs into g_tprobe
 // (0 TMA wait, 1 y, 2 K + commodities, 3 dcon + barrier, 4 edge runs, 5 end barrier, 7 tiles).
@@ -566,6 +568,21 @@ __device__ __forceinline__ void edge_totals(const Params &P, int e, int lane, do
         warp_edge_sums(P.partT, P.partL, P.G, P.I.E, e, lane, T, L);
 }
 
+// The per-edge squared dual_capacity changes are double-buffered by iteration
+// parity inside the persistent kernel: the edge phase of iteration k + 1 (at
+// the loop top, iteration counter k) writes half k & 1, and the controller of
+// the same iteration (counter k + 1 after the pass) reads it.  No grid barrier
+// separates one iteration's controller from the next edge phase, so with a
+// single buffer a CTA that leaves the controller early could overwrite entries
+// a slower CTA was still summing, and the CTAs' controller copies could diverge.
+// (The split multi-GPU kernels are separate launches and use half 0.)
+__device__ __forceinline__ double *res_dc_write(const Params &P, const Ctrl &c) {
+    return P.res_dc + (size_t)(c.iteration & 1) * (size_t)P.I.E;
+}
+__device__ __forceinline__ const double *res_dc_read(const Params &P, const Ctrl &c) {
+    return P.res_dc + (size_t)((c.iteration + 1) & 1) * (size_t)P.I.E;
+}
+
 // Sum of the per-edge dual_capacity residuals by the whole CTA (NT threads):
 // thread i sums edges i, i + NT, ... in order, then a warp shuffle tree and the
 // warp sums in warp order.  Every thread returns the same value.
@@ -681,7 +698,7 @@ __device__ __noinline__ void controller_step(const Params &P, Ctrl &c, double s,
 // Every CTA reduces the residual partials in the same fixed order and runs the
 // same scalar controller step on its shared-memory copy of the state.
 __device__ void controller_eval(const Params &P, Ctrl &c) {
-    const double dcs = dcs_block(P.res_dc, P.I.E);
+    const double dcs = dcs_block(res_dc_read(P, c), P.I.E);
     if (threadIdx.x < 32) {
         const int par = (int)(c.iteration & 1);
         double acc[4];  // dx, dd, dcon, dn: lane-strided over the CTAs
@@ -706,7 +723,7 @@ __device__ void controller_eval(const Params &P, Ctrl &c) {
 // slots; a warp per edge left the phase waiting on the heaviest edges).  Thread
 // t sums slots t, t + NT, ... in order (8 in flight), then a fixed block tree;
 // then kernels.py:212 and :94-96 as edge_phase.
-__device__ __noinline__ void edge_phase_rs(const Params &P, double f) {
+__device__ __noinline__ void edge_phase_rs(const Params &P, double f, double *res_dc) {
     const InstView &I = P.I;
     __shared__ double2 wsum[NT / 32];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -745,13 +762,13 @@ __device__ __noinline__ void edge_phase_rs(const Params &P, double f) {
             P.dc[e] = dnew;
             P.adj[e] = adj;
             const double d = dnew - dold;
-            P.res_dc[e] = d * d;
+            res_dc[e] = d * d;
         }
         __syncthreads();
     }
 }
 
-__device__ __noinline__ void edge_phase(const Params &P, double f) {
+__device__ __noinline__ void edge_phase(const Params &P, double f, double *res_dc) {
     const InstView &I = P.I;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int e = blockIdx.x + P.G * warp; e < I.E; e += P.G * (NT / 32)) {  // edges spread over all CTAs
@@ -766,7 +783,7 @@ __device__ __noinline__ void edge_phase(const Params &P, double f) {
             P.dc[e] = dnew;
             P.adj[e] = adj;
             const double d = dnew - dold;
-            P.res_dc[e] = d * d;
+            res_dc[e] = d * d;
         }
     }
 }
@@ -1381,6 +1398,7 @@ __device__ __noinline__ void xchg_phase(const Params &P, Ctrl &c, cg::grid_group
                 for (int j = 0; j < 7; ++j) d[j] = acc[j];
                 d[7] = e0;
                 d[8] = e1;
+                d[9] = __longlong_as_double((long long)(ep + 1));  // the slot's epoch tag
             }
         }
     }
@@ -1405,6 +1423,20 @@ __device__ __noinline__ void xchg_phase(const Params &P, Ctrl &c, cg::grid_group
                 break;
             }
             __nanosleep(64);
+        }
+        // every slot must carry this exchange's epoch tag: a mismatch (a rank
+        // out of step) stops the run with PF_ERR_COMM instead of summing stale totals
+        for (int r = 0; !s_timeout && r < P.nranks; ++r) {
+            const long long tag = __double_as_longlong(__ldcg(&xb_slot(P, P.peers[P.rank], ep, r)[2 * P.I.E + 9]));
+            if (tag != (long long)(ep + 1)) {
+                s_timeout = 2;
+                if (atomicCAS(&g_xdebug[0], 0ull, ep + 1) == 0ull) {
+                    g_xdebug[1] = (unsigned long long)r;
+                    g_xdebug[2] = (unsigned long long)tag;
+                    g_xdebug[3] = (unsigned long long)c.iteration;
+                    g_xdebug[4] = ld_acquire_sys(flag);
+                }
+            }
         }
     }
     __syncthreads();
@@ -1440,14 +1472,14 @@ __device__ __noinline__ void xchg_edge_apply(const Params &P, const Ctrl &c, dou
             P.dc[e] = dnew;
             P.adj[e] = adj;
             const double d = dnew - dold;
-            P.res_dc[e] = d * d;
+            res_dc_write(P, c)[e] = d * d;
         }
     }
 }
 
 // controller_eval from the exchanged residual sums (every CTA, same result)
 __device__ void xchg_controller_eval(const Params &P, Ctrl &c) {
-    const double dcs = dcs_block(P.res_dc, P.I.E);
+    const double dcs = dcs_block(res_dc_read(P, c), P.I.E);
     if (threadIdx.x == 0) {
         const uint64_t ep = c.xepoch - 1;
         const int64_t b = 2 * (int64_t)P.I.E;
@@ -1511,7 +1543,7 @@ __global__ void __launch_bounds__(NT, PF_MINB) k_fused(const __grid_constant__ P
             if (dist)
                 xchg_edge_apply(P, c, c.f);
             else
-                (P.ebound ? edge_phase_rs(P, c.f) : edge_phase(P, c.f));
+                (P.ebound ? edge_phase_rs(P, c.f, res_dc_write(P, c)) : edge_phase(P, c.f, res_dc_write(P, c)));
             mark(0);
             grid.sync();
             mark(1);
@@ -2243,7 +2275,7 @@ FastSolver *fast_create(const pf_instance *inst, const pf_config &cfg, cudaStrea
     F->partL.alloc(npart);
     if (F->L->run_slots) F->slots.alloc(2 * (size_t)std::max<int64_t>(F->L->nruns, 1));
     F->res.alloc((size_t)G * 8);
-    F->res_dc.alloc(E);
+    F->res_dc.alloc(2 * E);  // two halves by iteration parity (res_dc_write)
     F->err.alloc(2);
     F->ctrl.alloc(1);
     if (cfg.trace) F->root_sums.alloc(I.C ? I.C : 1);
@@ -2690,6 +2722,16 @@ int64_t fast_run(FastSolver *F, int64_t max_steps, cudaStream_t s, float *ms) {
         PF_CUDA(cudaMemcpyToSymbol(g_tprobe, z, sizeof(z)));
     }
 #endif
+    if (F->nranks) {
+        unsigned long long xd[5];
+        PF_CUDA(cudaMemcpyFromSymbol(xd, g_xdebug, sizeof(xd)));
+        if (xd[0]) {
+            fprintf(stderr, "[pf] rank %d: exchange %llu read rank %llu's slot with epoch tag %lld at iteration %llu "
+                            "(arrival counter %llu)\n", F->rank, xd[0] - 1, xd[1], (long long)xd[2], xd[3], xd[4]);
+            unsigned long long z[5] = {0, 0, 0, 0, 0};
+            PF_CUDA(cudaMemcpyToSymbol(g_xdebug, z, sizeof(z)));
+        }
+    }
     if (getenv("PF_FAST_DEBUG"))
         fprintf(stderr, "[fast run] iterations %lld, rollback passes so far %lld\n", (long long)c.iteration,
                 (long long)c.rollbacks);

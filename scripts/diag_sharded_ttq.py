@@ -31,16 +31,32 @@ if os.environ.get("DIAG_PRE"):  # an earlier sharded solver on another instance 
     dist.barrier()
 sh = ShardedSolver(topo, tab, flat, pf.SolverConfig(mode="fast", max_iterations=5000), rank, world, local)
 sh.init()
-full = pf.build_instance_flat(topo, tab, flat, device=local) if rank == 0 else None
-single = pf.Solver(full, pf.SolverConfig(mode="fast", max_iterations=5000)).init() if rank == 0 else None
-theta = pf.default_theta(full) if rank == 0 else None
+after = os.environ.get("DIAG_SINGLE_AFTER") == "1"  # rank 0's single-GPU objects only after the sharded run
+full = single = theta = None
+
+
+def make_single():
+    global full, single, theta
+    full = pf.build_instance_flat(topo, tab, flat, device=local)
+    single = pf.Solver(full, pf.SolverConfig(mode="fast", max_iterations=5000)).init()
+    theta = pf.default_theta(full)
+
+
+if rank == 0 and not after:
+    make_single()
 done = 0
 for k in [int(v) for v in os.environ.get("DIAG_KS", "10,100,1000,2500,4860").split(",")]:
     sh.run(k - done)
     if rank == 0:
-        single.run(k - done)
+        if single is None:
+            make_single()
+            single.run(k)
+        else:
+            single.run(k - done)
     done = k
     r = sh.result()
+    if r.status:
+        print(f"rank {rank}: status {r.status} at iteration {r.iterations}", flush=True)
     xg = sh.gather_x()
     if rank == 0:
         rs = single.result()
