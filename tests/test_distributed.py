@@ -308,11 +308,11 @@ def test_ipc_second_solver_in_process():
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    if os.environ.get("PF_TEST_TIMESLICED_LONG") != "1":
-        # two processes' cooperative kernels spinning on each other through one
-        # time-sliced GPU occasionally stall for minutes here (not a multi-GPU
-        # deployment); run on demand (scripts/diag_sharded_det.py covers it)
-        pytest.skip("long time-sliced multi-process run: set PF_TEST_TIMESLICED_LONG=1")
+    if os.environ.get("PF_TEST_TIMESLICED_LONG") == "0":
+        pytest.skip("long time-sliced multi-process run disabled (PF_TEST_TIMESLICED_LONG=0)")
+    # (this run used to drift from the single-GPU trajectory or stall: the CTAs'
+    # controller copies could diverge on a race over the per-edge residuals,
+    # fixed by double-buffering them by iteration parity)
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -321,9 +321,13 @@ def test_ipc_second_solver_in_process():
     ps = [ctx.Process(target=_ipc_second_solver_worker, args=(r, world, port, iters, q)) for r in range(world)]
     for p in ps:
         p.start()
-    res = sorted([q.get(timeout=600) for _ in range(world)], key=lambda t: t[0])
-    for p in ps:
-        p.join(timeout=60)
+    try:
+        res = sorted([q.get(timeout=240) for _ in range(world)], key=lambda t: t[0])
+    finally:
+        for p in ps:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
     assert all(p.exitcode == 0 for p in ps)
     states = [t[1:4] for t in res]
     assert all(s == states[0] for s in states) and states[0][0] == iters
